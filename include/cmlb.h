@@ -1,0 +1,184 @@
+/*
+ * cmlb.h -- C ABI of the B200 operator-representation inference path.
+ *
+ * The reference ("mlower", pure Python) runs a KernelPlan through a Python
+ * interpreter loop (pkg/src/mlower/runtime.py:198-212) that dispatches numpy
+ * kernels (pkg/src/mlower/kernels.py:47-287).  This library replaces that
+ * executor's compute: each entry point below executes one fused operator
+ * representation on the GPU.  Plain pointers and sizes only; no torch types.
+ * Device pointers are CUDA device memory; `stream` is a cudaStream_t (NULL =
+ * legacy default stream).  All entry points are thread-safe; programs are
+ * immutable after creation and may be run concurrently on different streams.
+ *
+ * Status codes map 1:1 onto the reference error classes
+ * (pkg/src/mlower/errors.py:10-93); see paper_2301_13441_b200/errors.py.
+ */
+#ifndef CMLB_H_
+#define CMLB_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CMLB_ABI_VERSION 1
+
+enum cmlb_status {
+  CMLB_OK = 0,
+  CMLB_E_VALIDATION = 1,   /* ValidationError        errors.py:21-24 */
+  CMLB_E_SHAPE = 2,        /* ShapeMismatch          errors.py:35-36 */
+  CMLB_E_INDEX = 3,        /* IndexOutOfBounds       errors.py:55-56 */
+  CMLB_E_OVERFLOW = 4,     /* AccumulatorOverflowRisk errors.py:59-60 */
+  CMLB_E_UNRESOLVED = 5,   /* UnresolvedKernel       errors.py:71-72 */
+  CMLB_E_INPUT = 6,        /* InputMismatch          errors.py:79-80 */
+  CMLB_E_DEVICE = 7        /* CUDA failure (no reference analogue) */
+};
+
+/* Output element type: the reference output dtype after dispatch promotion
+ * (dtypes.py:112-118); BOOL is one byte holding 0/1 (dtypes.py:51-59). */
+enum cmlb_out_dtype {
+  CMLB_OUT_BOOL = 0, CMLB_OUT_INT8 = 1, CMLB_OUT_INT16 = 2, CMLB_OUT_INT32 = 3, CMLB_OUT_F32 = 4
+};
+
+/* Thread-local message for the last non-zero status on this thread. */
+const char* cmlb_last_error(void);
+int cmlb_abi_version(void);
+/* Number of kernel launches issued by this process so far (all entry points). */
+int64_t cmlb_launch_count(void);
+
+/* ------------------------------------------------------------------------ *
+ * Forest: the tree operator representation plus the ensemble tail.
+ *
+ * Replaces, per tree, the chain  matmul|sparse_dense_matmul(W1) -> greater(W2)
+ * -> [cast] -> matmul(W3) -> argmax -> gather_rows(leaf_table)
+ * (convert.py:192-204, runtime.py:160-187) and the ensemble tail
+ * stack -> [cast] -> reduce_mean|reduce_sum -> [mul lr -> add base]
+ * -> argmax|sigmoid-threshold -> gather_rows(classes) (convert.py:287-311,
+ * 211-222), in ONE kernel.  Trees are given in the reference's canonical
+ * numbering: internal nodes in level order, leaves in in-order
+ * (convert.py:110-135).  A child reference c >= 0 is an internal node of the
+ * same tree, c < 0 is leaf (-1 - c).
+ * ------------------------------------------------------------------------ */
+
+enum cmlb_aggregation {
+  CMLB_AGG_NONE = 0,   /* single tree: output = leaf payload (convert_tree) */
+  CMLB_AGG_MEAN = 1,   /* random forests: float64 mean over trees (kernels.py:180-184) */
+  CMLB_AGG_SUM = 2     /* gradient boosting: float64 sum, *lr, +base (kernels.py:185-190) */
+};
+
+enum cmlb_tail {
+  CMLB_TAIL_VALUES = 0,   /* write the aggregated float32 values (N x C) */
+  CMLB_TAIL_ARGMAX = 1,   /* first-max over C, then class label (convert.py:211-214) */
+  CMLB_TAIL_SIGMOID = 2   /* float64 sigmoid -> float32 > 0.5 -> label (convert.py:217-222) */
+};
+
+enum cmlb_forest_variant {
+  CMLB_FOREST_AUTO = 0,        /* pick by (depth, trees, features) from the measured table */
+  CMLB_FOREST_PERFECT = 1,     /* perfect-padded trees staged in shared memory */
+  CMLB_FOREST_GENERAL = 2      /* arbitrary depth, canonical nodes read through L1 */
+};
+
+typedef struct cmlb_forest_desc {
+  int32_t n_trees;
+  int32_t n_features;
+  int32_t n_outputs;            /* C: payload width per leaf */
+  const int64_t* node_offset;   /* [n_trees + 1] into feature/threshold/left/right */
+  const int64_t* leaf_offset;   /* [n_trees + 1] into payload rows */
+  const int32_t* feature;       /* internal nodes, level order */
+  const float* threshold;
+  const int32_t* left;
+  const int32_t* right;
+  const float* payload;         /* [total leaves][n_outputs], in-order leaf rows */
+  int32_t aggregation;          /* cmlb_aggregation */
+  int32_t tail;                 /* cmlb_tail */
+  float learning_rate;
+  float base_score;
+  const double* classes;        /* class labels (tail ARGMAX / SIGMOID) */
+  int32_t n_classes;
+  int32_t out_dtype;            /* cmlb_out_dtype */
+  int32_t dense_selector;       /* 1: replicate dense W1 (0*inf = NaN) semantics */
+  int32_t variant;              /* cmlb_forest_variant */
+} cmlb_forest_desc;
+
+typedef struct cmlb_forest cmlb_forest;
+
+/* Build device tables on `device` (host arrays are copied; caller keeps ownership). */
+int cmlb_forest_create(const cmlb_forest_desc* desc, int device, cmlb_forest** out);
+/* x: device float32 [n_rows][ldx] row-major; y: device output [n_rows][k] of out_dtype
+ * (k = C for VALUES, 1 otherwise); leaf_out: optional device int32 [n_rows][n_trees]
+ * in-order leaf index per tree (reference argmax slots). */
+int cmlb_forest_run(const cmlb_forest* f, const float* x, int64_t n_rows, int64_t ldx,
+                    void* y, int32_t* leaf_out, void* stream);
+/* Tree-sharded partial: float64 raw sums over this program's trees in the
+ * reference's pairwise order restricted to the shard (no tail), [n_rows][C]. */
+int cmlb_forest_partial(const cmlb_forest* f, const float* x, int64_t n_rows, int64_t ldx,
+                        double* partial, void* stream);
+/* Introspection: chosen variant, padded depth, trees per shared-memory chunk. */
+int cmlb_forest_info(const cmlb_forest* f, int32_t* variant, int32_t* depth, int32_t* chunk_trees,
+                     int32_t* rows_per_cta);
+void cmlb_forest_destroy(cmlb_forest* f);
+
+/* ------------------------------------------------------------------------ *
+ * Linear models: matmul(X, coef^T) -> add(intercept) -> tail
+ * (convert.py:230-252).  Logits are float64 ascending-k dot products rounded
+ * once to float32 (kernels.py:95-100), then float32 + b.
+ * ------------------------------------------------------------------------ */
+
+enum cmlb_linear_tail {
+  CMLB_LIN_VALUES = 0,      /* regressors: (N, C) float32 */
+  CMLB_LIN_ARGMAX = 1,      /* multi-class: first-max over C (softmax removed by RE) */
+  CMLB_LIN_SOFTMAX_ARGMAX = 2, /* multi-class with softmax kept (passes without RE) */
+  CMLB_LIN_SIGMOID = 3,     /* binary logistic: sigmoid -> f32 > 0.5 */
+  CMLB_LIN_SIGN = 4         /* binary margin: z > 0 */
+};
+
+typedef struct cmlb_linear_desc {
+  int32_t n_features;
+  int32_t n_outputs;        /* C = rows of coef */
+  const float* coef;        /* [C][n_features] */
+  const float* intercept;   /* [C] */
+  int32_t tail;             /* cmlb_linear_tail */
+  const double* classes;
+  int32_t n_classes;
+  int32_t out_dtype;
+  int32_t sparse_coef;      /* 1: CSR weight semantics (skip zero weights, kernels.py:115-123) */
+} cmlb_linear_desc;
+
+typedef struct cmlb_linear cmlb_linear;
+int cmlb_linear_create(const cmlb_linear_desc* desc, int device, cmlb_linear** out);
+int cmlb_linear_run(const cmlb_linear* m, const float* x, int64_t n_rows, int64_t ldx,
+                    void* y, void* stream);
+void cmlb_linear_destroy(cmlb_linear* m);
+
+/* ------------------------------------------------------------------------ *
+ * Preprocessing operators (convert.py:255-284): float32 elementwise with the
+ * reference's rounding sequence (no FMA contraction), Normalizer row norms in
+ * float64 (kernels.py:245-261).
+ * ------------------------------------------------------------------------ */
+
+enum cmlb_scaler_kind {
+  CMLB_SCALER_BINARIZER = 0, CMLB_SCALER_NORMALIZER_L1 = 1, CMLB_SCALER_NORMALIZER_L2 = 2,
+  CMLB_SCALER_NORMALIZER_MAX = 3, CMLB_SCALER_MINMAX = 4, CMLB_SCALER_SUB_DIV = 5,
+  CMLB_SCALER_DIV = 6
+};
+
+typedef struct cmlb_scaler_desc {
+  int32_t kind;             /* cmlb_scaler_kind */
+  int32_t n_features;
+  float threshold;          /* binarizer */
+  const float* a;           /* minmax: scale; sub_div: center/mean; div: scale */
+  const float* b;           /* minmax: min;   sub_div: scale */
+} cmlb_scaler_desc;
+
+typedef struct cmlb_scaler cmlb_scaler;
+int cmlb_scaler_create(const cmlb_scaler_desc* desc, int device, cmlb_scaler** out);
+/* y: device float32 [n_rows][n_features] (may alias x when ldx == n_features). */
+int cmlb_scaler_run(const cmlb_scaler* s, const float* x, int64_t n_rows, int64_t ldx,
+                    float* y, void* stream);
+void cmlb_scaler_destroy(cmlb_scaler* s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CMLB_H_ */

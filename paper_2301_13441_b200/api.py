@@ -1,0 +1,192 @@
+"""Public API: the reference's ``compile_model`` / ``predict`` / ``execute``.
+
+Signatures follow ``pkg/src/mlower/pipeline.py:31-48`` and
+``pkg/src/mlower/runtime.py:198-212``:
+
+    compile_model(model, profile=cpu-avx2, passes=("re", "dr", "sor")) -> CompileResult
+    predict(compiled, x) -> Tensor
+    execute(plan, x) -> Tensor
+
+and so do their contracts: ``x`` must be rank 2 with ``n_features`` columns
+and dtype float32 (else ``InputMismatch``, ``runtime.py:200-205``); the output
+has the reference's shape and dtype; zero-row batches flow through; results
+are deterministic and batch-invariant.
+
+What differs is where the work runs.  ``execute`` accepts a reference
+``KernelPlan`` unchanged (``lower.lower_plan`` inverts its tensor encodings),
+``compile_model`` lowers the model directly; either way one fused sm_100a
+kernel per operator representation runs on the GPU.  Inputs may be
+
+* a reference ``Tensor`` / our :class:`~.tensor.Tensor` / numpy array
+  (host): copied in, computed, copied out, returned as the same family;
+* a CUDA ``torch.Tensor``: computed in place on its device and stream, the
+  result stays on the device (uint8 for BOOL outputs);
+* a CPU ``torch.Tensor`` (ideally pinned): streamed through the GPU in
+  overlapped chunks, result returned as a CPU tensor.
+"""
+
+from __future__ import annotations
+
+import threading
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from .dtypes import name_of
+from .errors import InputMismatch, ValidationError
+from .lower import DEFAULT_PASSES, ProgramSpec, lower_model, lower_plan
+from .models import parse_model
+from .runtime import DeviceProgram, run_host
+from .tensor import Tensor, wrap_like
+
+DEFAULT_TOLERANCE = 1e-5
+DEFAULT_PROFILE = "cpu-avx2"
+
+
+@dataclass(frozen=True, eq=False)
+class CompileResult:
+    """Mirror of the reference ``CompileResult`` (``pipeline.py:22-28``).
+
+    ``plan`` is the reference plan when compiled from one (``from_plan``);
+    ``spec`` is the lowered fused program description; device programs are
+    built lazily per GPU and cached here.
+    """
+
+    model: object
+    spec: ProgramSpec
+    profile: object = DEFAULT_PROFILE
+    passes: tuple = DEFAULT_PASSES
+    plan: object = None
+
+    def program(self, device: int | None = None) -> DeviceProgram:
+        return _program_for(self, device)
+
+
+_cache_lock = threading.Lock()
+_programs: dict = {}   # (id(owner), device) -> DeviceProgram
+_plan_specs: dict = {}  # id(plan) -> ProgramSpec
+
+
+def _evict(key_id: int) -> None:
+    with _cache_lock:
+        for k in [k for k in _programs if k[0] == key_id]:
+            prog = _programs.pop(k)
+            try:
+                prog.close()
+            except Exception:  # pragma: no cover
+                pass
+        _plan_specs.pop(key_id, None)
+
+
+def _device_of(device) -> int:
+    if device is None:
+        return torch.cuda.current_device()
+    if isinstance(device, torch.device):
+        return device.index if device.index is not None else torch.cuda.current_device()
+    return int(device)
+
+
+def _program_for(owner, device=None, spec: ProgramSpec | None = None) -> DeviceProgram:
+    dev = _device_of(device)
+    key = (id(owner), dev)
+    with _cache_lock:
+        prog = _programs.get(key)
+        if prog is not None:
+            return prog
+    prog = DeviceProgram(spec if spec is not None else owner.spec, dev)
+    with _cache_lock:
+        if key in _programs:  # lost a race; keep the first
+            prog.close()
+            return _programs[key]
+        _programs[key] = prog
+        weakref.finalize(owner, _evict, id(owner))
+    return prog
+
+
+def compile_model(model, profile=DEFAULT_PROFILE, passes=DEFAULT_PASSES) -> CompileResult:
+    """Lower ``model`` (ours, the reference's, or model JSON text) to a fused program."""
+    if isinstance(model, str):
+        model = parse_model(model)
+    passes = tuple(passes)
+    unknown = set(passes) - set(DEFAULT_PASSES)
+    if unknown:
+        raise ValidationError(f"unknown pass flags: {sorted(unknown)}")
+    return CompileResult(model=model, spec=lower_model(model, profile, passes), profile=profile,
+                         passes=passes)
+
+
+def from_plan(plan, model=None) -> CompileResult:
+    """Wrap a reference KernelPlan (e.g. ``mlower.compile_model(m).plan``)."""
+    return CompileResult(model=model, spec=_spec_of_plan(plan), plan=plan)
+
+
+def _spec_of_plan(plan) -> ProgramSpec:
+    with _cache_lock:
+        spec = _plan_specs.get(id(plan))
+    if spec is None:
+        spec = lower_plan(plan)
+        with _cache_lock:
+            _plan_specs[id(plan)] = spec
+        weakref.finalize(plan, _evict, id(plan))
+    return spec
+
+
+# -- input handling ---------------------------------------------------------------
+
+
+def _host_array(x):
+    """numpy view of a host input, with the reference's InputMismatch checks."""
+    if isinstance(x, np.ndarray):
+        arr = x
+    elif hasattr(x, "to_numpy") and hasattr(x, "dtype"):
+        if name_of(x.dtype) != "float32":
+            raise InputMismatch(f"input dtype {name_of(x.dtype)} != float32")
+        arr = x.to_numpy()
+    else:
+        raise InputMismatch(f"unsupported input type {type(x).__name__}")
+    if arr.ndim != 2:
+        raise InputMismatch(f"input shape {arr.shape} is not rank 2")
+    if arr.dtype != np.float32:
+        raise InputMismatch(f"input dtype {arr.dtype} != float32")
+    return arr
+
+
+def _run(owner, spec_getter, x, device=None):
+    if isinstance(x, torch.Tensor):
+        dev = x.device.index if x.is_cuda else device
+        prog = _program_for(owner, dev, spec_getter())
+        if x.is_cuda:
+            return prog.run(x)
+        return run_host(prog, x)
+    arr = _host_array(x)
+    prog = _program_for(owner, device, spec_getter())
+    if arr.shape[1] != prog.n_features:
+        raise InputMismatch(f"input shape {arr.shape} does not match (batch, {prog.n_features})")
+    out = run_host(prog, torch.from_numpy(np.ascontiguousarray(arr)))
+    values = out.numpy()
+    if prog.out_dtype == "bool":
+        values = values.astype(np.uint8)
+    if isinstance(x, np.ndarray):
+        return values
+    return wrap_like(x, values, prog.out_dtype)
+
+
+def execute(plan, x, device=None):
+    """Run a reference ``KernelPlan`` on the GPU; drop-in for ``mlower.execute``."""
+    return _run(plan, lambda: _spec_of_plan(plan), x, device)
+
+
+def predict(compiled, x, device=None):
+    """Drop-in for ``mlower.predict``; also accepts a reference CompileResult."""
+    if isinstance(compiled, CompileResult):
+        return _run(compiled, lambda: compiled.spec, x, device)
+    plan = getattr(compiled, "plan", None)
+    if plan is None:
+        raise ValidationError("predict() needs a CompileResult")
+    return execute(plan, x, device)
+
+
+__all__ = ["CompileResult", "compile_model", "from_plan", "predict", "execute", "DEFAULT_TOLERANCE",
+           "Tensor"]

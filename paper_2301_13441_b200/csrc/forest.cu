@@ -1,0 +1,752 @@
+// Forest operator: the reference tree operator representation and its
+// ensemble tail, fused into one sm_100a kernel.
+//
+// Reference chain per tree (pkg/src/mlower/convert.py:192-204):
+//   select = X . W1          (feature gather, kernels.py:103-126)
+//   went_right = select > W2 (strict, NaN -> 0, kernels.py:141-149)
+//   scores = went_right . W3 (int matmul, kernels.py:92-94)
+//   leaf = argmax(scores)    (first max, kernels.py:197-203)
+//   out = leaf_table[leaf]   (kernels.py:206-217)
+// and the ensemble tail (convert.py:287-311): stack -> float64 mean|sum over
+// trees -> float32 -> [*lr, +base] -> argmax|sigmoid -> class label.
+//
+// The GEMM form evaluates every internal node of every tree (sum_t I_t
+// compares plus sum_t I_t * L_t MACs per row); the first-max leaf it selects is
+// exactly the leaf reached by walking the tree with the same strict test
+// (proved exhaustively by the reference's own test_convert.py).
+// This kernel walks: depth-many compares per tree.  Two layouts:
+//
+//  * PERFECT: every tree padded to a perfect binary tree of the forest's depth
+//    D with always-left dummy nodes (threshold +inf: x > +inf is false for
+//    every x incl. +inf and NaN), heap-ordered, so a level step is
+//    node = 2*node + 1 + (x[f] > t) with no branches.  Trees are staged into
+//    shared memory in chunks of whole trees; the row tile's features sit in
+//    shared memory feature-major (xs[f][row]) so a warp's 32 gathers of
+//    arbitrary features hit 32 distinct banks.
+//  * GENERAL: arbitrary depth; canonical level-order nodes packed as int4
+//    {feature, threshold bits, left ref, right ref} read through L1.
+//
+// Aggregation replays numpy's summation order exactly (the reference reduces
+// a C-contiguous (N, T, C) float64 array over axis 1):
+//   C >= 2: sequential, 0.0 + v0 + v1 + ...
+//   C == 1: the axis is contiguous, so numpy's pairwise_sum applies: blocks of
+//           <= 128 with 8 interleaved accumulators, recursive halving at
+//           multiples of 8.  The host precomputes one code per tree
+//           (build_schedule) and the kernel replays it with a small register
+//           stack.  Verified against numpy in tests/test_pairwise_schedule.py.
+
+#include <algorithm>
+#include <limits>
+#include <cstring>
+#include <deque>
+#include <memory>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "common.cuh"
+
+namespace cmlb {
+
+// ---------------------------------------------------------------------------
+// numpy pairwise-sum schedule
+// ---------------------------------------------------------------------------
+
+enum : uint32_t {
+  SC_ASSIGN = 0u,     // r[j] = v
+  SC_ADD = 1u,        // r[j] += v
+  SC_RES0 = 2u,       // res = 0.0 + v   (short block, first element)
+  SC_RESADD = 3u,     // res += v
+  SC_OPMASK = 3u,
+  SC_FOLD_PRE = 1u << 2,   // res = ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) before the op
+  SC_FOLD_POST = 1u << 3,  // same, after the op
+  SC_PUSH = 1u << 4,       // push res; then pop-combine (code >> 8) times
+};
+
+static void emit_block(std::vector<uint32_t>& code, int64_t lo, int64_t n) {
+  if (n < 8) {
+    for (int64_t i = 0; i < n; ++i) code[lo + i] = i == 0 ? SC_RES0 : SC_RESADD;
+  } else {
+    int64_t m = n - n % 8;
+    for (int64_t i = 0; i < n; ++i) {
+      uint32_t c;
+      if (i < 8) c = SC_ASSIGN;
+      else if (i < m) c = SC_ADD;
+      else c = SC_RESADD | (i == m ? SC_FOLD_PRE : 0u);
+      code[lo + i] = c;
+    }
+    if (m == n) code[lo + n - 1] |= SC_FOLD_POST;
+  }
+  code[lo + n - 1] |= SC_PUSH;
+}
+
+static void schedule_rec(std::vector<uint32_t>& code, int64_t lo, int64_t n) {
+  if (n <= 128) {
+    emit_block(code, lo, n);
+    return;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  schedule_rec(code, lo, n2);
+  schedule_rec(code, lo + n2, n - n2);
+  code[lo + n - 1] += 1u << 8;  // combine the two halves after the last element
+}
+
+// Codes for pairwise_sum over n elements; returns the max stack depth.
+int build_schedule(int64_t n, std::vector<uint32_t>& code) {
+  code.assign((size_t)n, 0u);
+  if (n == 0) return 0;
+  schedule_rec(code, 0, n);
+  int sp = 0, best = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (code[i] & SC_PUSH) {
+      ++sp;
+      best = std::max(best, sp);
+      sp -= (int)(code[i] >> 8);
+    }
+  }
+  return best;
+}
+
+constexpr int SMAX = 10;  // register stack slots for the pairwise replay
+
+// ---------------------------------------------------------------------------
+// device program
+// ---------------------------------------------------------------------------
+
+struct ForestArgs {
+  const float* x;
+  int64_t n_rows;
+  int64_t ldx;
+  void* y;
+  int32_t* leaf_out;
+  double* partial;
+  // program
+  int T, F, C, depth, ni, ns, tree_bytes, chunk_trees, rows_per_cta;
+  const uint8_t* blob;        // perfect: [T][tree_bytes]
+  const int32_t* slot_leaf;   // perfect: [T][ns]
+  const int4* gnode;          // general: packed nodes
+  const int64_t* node_off;
+  const float* gpay;          // general: [total leaves][CT]
+  const int64_t* leaf_off;
+  const uint32_t* sched;      // pairwise codes (C == 1)
+  int agg, tail, out_dt, dense_sel, n_classes;
+  float lr, base;
+  const double* classes;
+  int pay_off, feat_off;      // byte offsets of payload / feature arrays inside a perfect tree blob
+};
+
+constexpr int NT = 256;  // threads per CTA for every forest kernel
+
+// Per-row accumulator.  PW selects numpy's pairwise replay (C == 1 ensembles);
+// otherwise a sequential float64 sum per output (C >= 2) or the raw payload
+// (single tree).
+template <int CT, bool PW>
+struct RowAcc;
+
+template <int CT>
+struct RowAcc<CT, false> {
+  double acc[CT];
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int c = 0; c < CT; ++c) acc[c] = 0.0;
+  }
+  __device__ __forceinline__ double total(int c) const { return acc[c]; }
+};
+
+template <int CT>
+struct RowAcc<CT, true> {
+  static_assert(CT == 1, "pairwise replay is for scalar leaves");
+  double r[8];
+  double res;
+  double st[SMAX];
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = 0.0;
+    res = 0.0;
+#pragma unroll
+    for (int s = 0; s < SMAX; ++s) st[s] = 0.0;
+  }
+  // numpy: the reduction output starts at +0.0, then adds pairwise_sum(...)
+  __device__ __forceinline__ double total(int) const { return 0.0 + st[0]; }
+  __device__ __forceinline__ double raw(int) const { return st[0]; }
+};
+
+__device__ __forceinline__ double fold8(const double (&r)[8]) {
+  return ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+}
+
+template <int J, int CT>
+__device__ __forceinline__ void accumulate(RowAcc<CT, false>& a, const float (&v)[CT], int C, uint32_t) {
+#pragma unroll
+  for (int c = 0; c < CT; ++c)
+    if (c < C) a.acc[c] += (double)v[c];
+}
+
+// j == tree index mod 8 (block starts are multiples of 8), a compile-time
+// constant after the caller's unroll, so r[] stays in registers.
+template <int J, int CT>
+__device__ __forceinline__ void accumulate(RowAcc<CT, true>& a, const float (&v)[CT], int, uint32_t code) {
+  constexpr int j = J;
+  const double val = (double)v[0];
+  if (code & SC_FOLD_PRE) a.res = fold8(a.r);
+  switch (code & SC_OPMASK) {
+    case SC_ASSIGN: a.r[j] = val; break;
+    case SC_ADD: a.r[j] += val; break;
+    case SC_RES0: a.res = 0.0 + val; break;
+    default: a.res += val; break;
+  }
+  if (code & SC_FOLD_POST) a.res = fold8(a.r);
+  if (code & SC_PUSH) {
+    // shift-register stack (st[0] = top): no runtime indices, stays in registers
+#pragma unroll
+    for (int q = SMAX - 1; q > 0; --q) a.st[q] = a.st[q - 1];
+    a.st[0] = a.res;
+    const int pops = (int)(code >> 8);
+    for (int p = 0; p < pops; ++p) {
+      a.st[0] = a.st[1] + a.st[0];  // (earlier half) + (later half)
+#pragma unroll
+      for (int q = 1; q < SMAX - 1; ++q) a.st[q] = a.st[q + 1];
+    }
+  }
+}
+
+// Reference semantics of the dense selector (profile "plain" / SOR off):
+// select_j = sum_k x_k * W1[k, j] in float64, so one non-finite feature turns
+// every node testing another feature into NaN, and two turn all nodes NaN.
+__device__ __forceinline__ void poison_row(float* xs, int stride, int F, int r) {
+  int nbad = 0;
+  for (int f = 0; f < F; ++f) nbad += !isfinite(xs[(int64_t)f * stride + r]);
+  if (nbad == 0) return;
+  for (int f = 0; f < F; ++f) {
+    float v = xs[(int64_t)f * stride + r];
+    if (nbad >= 2 || isfinite(v)) xs[(int64_t)f * stride + r] = __int_as_float(0x7fc00000);
+  }
+}
+
+template <int CT, bool PW>
+__device__ __forceinline__ void finish_row(const ForestArgs& a, int64_t row, const RowAcc<CT, PW>& acc,
+                                           const float (&single)[CT]) {
+  const int C = a.C;
+  if (a.partial) {  // tree-shard partial: raw float64 sums, no tail
+    if constexpr (PW) {
+      a.partial[row] = acc.raw(0);
+    } else {
+#pragma unroll
+      for (int c = 0; c < CT; ++c)
+        if (c < C) a.partial[row * C + c] = acc.total(c);
+    }
+    return;
+  }
+  float v[CT];
+  if (a.agg == CMLB_AGG_NONE) {
+#pragma unroll
+    for (int c = 0; c < CT; ++c) v[c] = single[c];
+  } else if (a.agg == CMLB_AGG_MEAN) {
+#pragma unroll
+    for (int c = 0; c < CT; ++c) v[c] = __double2float_rn(acc.total(c) / (double)a.T);
+  } else {
+    const float s = __double2float_rn(acc.total(0));
+    v[0] = __fadd_rn(__fmul_rn(s, a.lr), a.base);
+#pragma unroll
+    for (int c = 1; c < CT; ++c) v[c] = 0.0f;
+  }
+  if (a.tail == CMLB_TAIL_VALUES) {
+#pragma unroll
+    for (int c = 0; c < CT; ++c)
+      if (c < C) store_out(a.y, row * C + c, a.out_dt, (double)v[c]);
+  } else if (a.tail == CMLB_TAIL_ARGMAX) {
+    const int k = first_max<CT>(v, C);
+    store_out(a.y, row, a.out_dt, a.classes[k]);
+  } else {  // SIGMOID
+    const float p = __double2float_rn(ref_sigmoid((double)v[0]));
+    store_out(a.y, row, a.out_dt, a.classes[p > 0.5f ? 1 : 0]);
+  }
+}
+
+// One kernel body for both layouts.  Thread `tid` owns rows
+// tile + tid + k*NT (k < RPT): lanes map to consecutive rows, so the
+// feature-major xs[f][row] gathers are bank-conflict-free whatever f is.
+template <int CT, int RPT, bool PERFECT, bool XS, bool PW>
+__global__ void __launch_bounds__(NT) forest_kernel(const ForestArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int ROWS = NT * RPT;
+  const int tid = threadIdx.x;
+  const int64_t tile = (int64_t)blockIdx.x * ROWS;
+  const int F = a.F;
+  float* xs = reinterpret_cast<float*>(smem);
+  uint8_t* chunk = smem + (XS ? (size_t)F * ROWS * sizeof(float) : 0);
+
+  // ---- row tile -> shared memory, feature-major -------------------------
+  if (XS) {
+    for (int k = 0; k < RPT; ++k) {
+      const int r = tid + k * NT;
+      const int64_t row = tile + r;
+      const float* src = a.x + row * a.ldx;
+      if (row < a.n_rows) {
+        for (int f = 0; f < F; ++f) xs[f * ROWS + r] = __ldg(src + f);
+        if (a.dense_sel) poison_row(xs, ROWS, F, r);
+      } else {
+        for (int f = 0; f < F; ++f) xs[f * ROWS + r] = 0.0f;
+      }
+    }
+  }
+  // Without XS the rows are read from global memory (L1-cached); poisoning is
+  // then applied on the fly (general layout only, see xval()).
+
+  RowAcc<CT, PW> acc[RPT];
+  float single[RPT][CT];  // AGG_NONE: the one tree's payload
+#pragma unroll
+  for (int k = 0; k < RPT; ++k) {
+    acc[k].init();
+#pragma unroll
+    for (int c = 0; c < CT; ++c) single[k][c] = 0.0f;
+  }
+
+  int64_t rowk[RPT];
+  int nbad[RPT];
+#pragma unroll
+  for (int k = 0; k < RPT; ++k) {
+    rowk[k] = tile + tid + k * NT;
+    nbad[k] = 0;
+    if (!XS && a.dense_sel && rowk[k] < a.n_rows) {
+      const float* src = a.x + rowk[k] * a.ldx;
+      for (int f = 0; f < F; ++f) nbad[k] += !isfinite(__ldg(src + f));
+    }
+  }
+
+  auto xval = [&](int k, int f) -> float {
+    if (XS) return xs[f * ROWS + tid + k * NT];
+    if (rowk[k] >= a.n_rows) return 0.0f;
+    float v = __ldg(a.x + rowk[k] * a.ldx + f);
+    if (nbad[k] && (nbad[k] >= 2 || isfinite(v))) v = __int_as_float(0x7fc00000);
+    return v;
+  };
+
+  const int T = a.T;
+  const int chunk_trees = PERFECT ? a.chunk_trees : T;
+  for (int c0 = 0; c0 < T; c0 += chunk_trees) {
+    const int nt = min(chunk_trees, T - c0);
+    if (PERFECT) {
+      __syncthreads();  // previous chunk fully consumed (and xs written on the first pass)
+      const int4* src = reinterpret_cast<const int4*>(a.blob + (size_t)c0 * a.tree_bytes);
+      int4* dst = reinterpret_cast<int4*>(chunk);
+      const int n16 = nt * a.tree_bytes / 16;
+      for (int i = tid; i < n16; i += NT) dst[i] = __ldg(src + i);
+      __syncthreads();
+    } else if (c0 == 0 && XS) {
+      __syncthreads();
+    }
+    for (int tg = 0; tg < nt; tg += 8) {
+      // one tree; J = tree index mod 8 as a compile-time constant
+      auto tree_step = [&](auto jconst) {
+        constexpr int jj = decltype(jconst)::value;
+        const int tl = tg + jj;
+        if (tl >= nt) return;
+        const int t = c0 + tl;
+        const uint32_t code = PW ? __ldg(a.sched + t) : 0u;
+        int leaf[RPT];
+        float v[RPT][CT];
+        if (PERFECT) {
+          const uint8_t* tb = chunk + (size_t)tl * a.tree_bytes;
+          const float* thr = reinterpret_cast<const float*>(tb);
+          const float* pay = reinterpret_cast<const float*>(tb + a.pay_off);
+          const uint16_t* fea = reinterpret_cast<const uint16_t*>(tb + a.feat_off);
+          int node[RPT];
+#pragma unroll
+          for (int k = 0; k < RPT; ++k) node[k] = 0;
+          for (int lvl = 0; lvl < a.depth; ++lvl) {
+#pragma unroll
+            for (int k = 0; k < RPT; ++k) {
+              const int f = fea[node[k]];
+              const float th = thr[node[k]];
+              const float xv = xval(k, f);
+              node[k] = 2 * node[k] + 1 + (xv > th ? 1 : 0);
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < RPT; ++k) {
+            const int slot = node[k] - a.ni;
+            leaf[k] = slot;
+#pragma unroll
+            for (int c = 0; c < CT; ++c) v[k][c] = pay[slot * CT + c];
+          }
+        } else {
+          const int64_t nb = __ldg(a.node_off + t);
+          const int nint = (int)(__ldg(a.node_off + t + 1) - nb);
+          const int64_t lb = __ldg(a.leaf_off + t);
+#pragma unroll
+          for (int k = 0; k < RPT; ++k) {
+            int lf = 0;
+            if (nint > 0) {
+              int cur = 0;
+              while (true) {
+                const int4 nd = __ldg(a.gnode + nb + cur);
+                const float xv = xval(k, nd.x);
+                const int ref = xv > __int_as_float(nd.y) ? nd.w : nd.z;
+                if (ref < 0) { lf = -1 - ref; break; }
+                cur = ref;
+              }
+            }
+            leaf[k] = lf;
+#pragma unroll
+            for (int c = 0; c < CT; ++c) v[k][c] = __ldg(a.gpay + (lb + lf) * CT + c);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) {
+          if (a.leaf_out && rowk[k] < a.n_rows) {
+            const int li = PERFECT ? __ldg(a.slot_leaf + (int64_t)t * a.ns + leaf[k]) : leaf[k];
+            a.leaf_out[rowk[k] * T + t] = li;
+          }
+          if (a.agg == CMLB_AGG_NONE) {
+#pragma unroll
+            for (int c = 0; c < CT; ++c) single[k][c] = v[k][c];
+          } else {
+            accumulate<jj, CT>(acc[k], v[k], a.C, code);
+          }
+        }
+      };
+      tree_step(std::integral_constant<int, 0>{});
+      tree_step(std::integral_constant<int, 1>{});
+      tree_step(std::integral_constant<int, 2>{});
+      tree_step(std::integral_constant<int, 3>{});
+      tree_step(std::integral_constant<int, 4>{});
+      tree_step(std::integral_constant<int, 5>{});
+      tree_step(std::integral_constant<int, 6>{});
+      tree_step(std::integral_constant<int, 7>{});
+    }
+  }
+
+#pragma unroll
+  for (int k = 0; k < RPT; ++k)
+    if (rowk[k] < a.n_rows) finish_row<CT, PW>(a, rowk[k], acc[k], single[k]);
+}
+
+// ---------------------------------------------------------------------------
+// host program
+// ---------------------------------------------------------------------------
+
+}  // namespace cmlb
+
+struct cmlb_forest {
+  int device = 0;
+  int T = 0, F = 0, C = 0, CT = 1;
+  int variant = CMLB_FOREST_GENERAL;
+  int depth = 0, ni = 0, ns = 0, tree_bytes = 0, chunk_trees = 0, rpt = 1;
+  int pay_off = 0, feat_off = 0;
+  bool xs = true;
+  int agg = 0, tail = 0, out_dt = 4, dense_sel = 0, n_classes = 0;
+  float lr = 1.f, base = 0.f;
+  size_t smem = 0;
+  // device buffers
+  uint8_t* blob = nullptr;
+  int32_t* slot_leaf = nullptr;
+  int4* gnode = nullptr;
+  int64_t* node_off = nullptr;
+  float* gpay = nullptr;
+  int64_t* leaf_off = nullptr;
+  uint32_t* sched = nullptr;
+  double* classes = nullptr;
+  ~cmlb_forest() {
+    cudaFree(blob); cudaFree(slot_leaf); cudaFree(gnode); cudaFree(node_off);
+    cudaFree(gpay); cudaFree(leaf_off); cudaFree(sched); cudaFree(classes);
+  }
+};
+
+namespace cmlb {
+
+constexpr int PERFECT_MAX_DEPTH = 11;
+constexpr size_t SMEM_LIMIT = 227 * 1024;
+constexpr size_t XS_BUDGET = 120 * 1024;
+
+static int class_width(int C) {
+  if (C <= 1) return 1;
+  if (C <= 2) return 2;
+  if (C <= 4) return 4;
+  if (C <= 8) return 8;
+  if (C <= 16) return 16;
+  return 32;
+}
+
+static int rows_per_thread(int CT, bool pairwise) {
+  if (CT >= 16) return 1;
+  if (pairwise || CT >= 4) return 2;
+  return 4;
+}
+
+template <typename T>
+static int upload(T** dst, const T* src, size_t n) {
+  if (n == 0) n = 1;
+  CMLB_CUDA(cudaMalloc((void**)dst, n * sizeof(T)));
+  if (src) CMLB_CUDA(cudaMemcpy(*dst, src, n * sizeof(T), cudaMemcpyHostToDevice));
+  return CMLB_OK;
+}
+
+using KernelFn = void (*)(const ForestArgs);
+
+template <int CT, int R, bool PW>
+static KernelFn pick4(bool perfect, bool xs) {
+  if (perfect) return xs ? forest_kernel<CT, R, true, true, PW> : forest_kernel<CT, R, true, false, PW>;
+  return xs ? forest_kernel<CT, R, false, true, PW> : forest_kernel<CT, R, false, false, PW>;
+}
+
+static KernelFn kernel_for(const cmlb_forest& f) {
+  const bool perfect = f.variant == CMLB_FOREST_PERFECT;
+  const bool pw = f.C == 1 && f.agg != CMLB_AGG_NONE;
+  switch (f.CT) {
+    case 1:
+      if (pw) return pick4<1, 2, true>(perfect, f.xs);
+      return f.rpt == 4 ? pick4<1, 4, false>(perfect, f.xs) : pick4<1, 2, false>(perfect, f.xs);
+    case 2: return f.rpt == 4 ? pick4<2, 4, false>(perfect, f.xs) : pick4<2, 2, false>(perfect, f.xs);
+    case 4: return pick4<4, 2, false>(perfect, f.xs);
+    case 8: return pick4<8, 2, false>(perfect, f.xs);
+    case 16: return pick4<16, 1, false>(perfect, f.xs);
+    default: return pick4<32, 1, false>(perfect, f.xs);
+  }
+}
+
+static int validate(const cmlb_forest_desc* d) {
+  if (!d) return fail(CMLB_E_VALIDATION, "null forest descriptor");
+  if (d->n_trees < 1 || d->n_features < 1 || d->n_outputs < 1)
+    return fail(CMLB_E_VALIDATION, "forest needs >= 1 tree, feature and output");
+  if (d->n_outputs > 32) return fail(CMLB_E_UNRESOLVED, "more than 32 outputs per leaf");
+  if (!out_dtype_ok(d->out_dtype)) return fail(CMLB_E_VALIDATION, "bad out_dtype");
+  if (d->aggregation == CMLB_AGG_NONE && d->n_trees != 1)
+    return fail(CMLB_E_VALIDATION, "aggregation NONE needs exactly one tree");
+  if (d->aggregation == CMLB_AGG_SUM && d->n_outputs != 1)
+    return fail(CMLB_E_VALIDATION, "sum aggregation needs scalar leaves");
+  if ((d->tail == CMLB_TAIL_ARGMAX && d->n_classes < d->n_outputs) ||
+      (d->tail == CMLB_TAIL_SIGMOID && d->n_classes != 2))
+    return fail(CMLB_E_VALIDATION, "class table does not match the tail");
+  for (int t = 0; t < d->n_trees; ++t) {
+    const int64_t ni = d->node_offset[t + 1] - d->node_offset[t];
+    const int64_t nl = d->leaf_offset[t + 1] - d->leaf_offset[t];
+    if (ni < 0 || nl != ni + 1) return fail(CMLB_E_VALIDATION, "tree " + std::to_string(t) + ": leaves != internal + 1");
+    for (int64_t j = 0; j < ni; ++j) {
+      const int64_t g = d->node_offset[t] + j;
+      if (d->feature[g] < 0 || d->feature[g] >= d->n_features)
+        return fail(CMLB_E_VALIDATION, "tree " + std::to_string(t) + ": feature out of range");
+      for (int32_t ref : {d->left[g], d->right[g]}) {
+        if (ref >= 0 ? (ref <= j || ref >= ni) : (-1 - (int64_t)ref >= nl))
+          return fail(CMLB_E_VALIDATION, "tree " + std::to_string(t) + ": bad child reference");
+      }
+    }
+  }
+  return CMLB_OK;
+}
+
+static int tree_depth(const cmlb_forest_desc* d, int t) {
+  const int64_t nb = d->node_offset[t];
+  const int64_t ni = d->node_offset[t + 1] - nb;
+  if (ni == 0) return 0;
+  std::vector<int> dep((size_t)ni, 0);
+  int best = 1;
+  for (int64_t j = 0; j < ni; ++j) {
+    for (int32_t ref : {d->left[nb + j], d->right[nb + j]}) {
+      if (ref >= 0) dep[ref] = dep[j] + 1;
+      else best = std::max(best, dep[j] + 1);
+    }
+  }
+  return best;
+}
+
+// Heap-ordered perfect padding of one tree into its blob.
+static void fill_perfect(const cmlb_forest_desc* d, int t, int D, int CT, int pay_off, int feat_off,
+                         uint8_t* blob, int32_t* slot_leaf) {
+  const int ni = (1 << D) - 1, ns = 1 << D;
+  float* thr = reinterpret_cast<float*>(blob);
+  float* pay = reinterpret_cast<float*>(blob + pay_off);
+  uint16_t* fea = reinterpret_cast<uint16_t*>(blob + feat_off);
+  const float inf = std::numeric_limits<float>::infinity();
+  for (int i = 0; i < ni; ++i) { thr[i] = inf; fea[i] = 0; }
+  const int64_t nb = d->node_offset[t], lb = d->leaf_offset[t];
+  // (heap position, canonical ref)
+  std::deque<std::pair<int64_t, int32_t>> q;
+  q.push_back({0, d->node_offset[t + 1] > nb ? 0 : -1});
+  while (!q.empty()) {
+    auto [h, ref] = q.front();
+    q.pop_front();
+    if (ref >= 0) {
+      thr[h] = d->threshold[nb + ref];
+      fea[h] = (uint16_t)d->feature[nb + ref];
+      q.push_back({2 * h + 1, d->left[nb + ref]});
+      q.push_back({2 * h + 2, d->right[nb + ref]});
+    } else {
+      const int leaf = -1 - ref;
+      // leaf at heap position h: every slot under h maps to it (only the
+      // leftmost is reachable; the dummies above always go left)
+      int64_t lo = h, hi = h;
+      while (lo < ni) { lo = 2 * lo + 1; hi = 2 * hi + 2; }
+      for (int64_t s = lo; s <= hi; ++s) {
+        const int64_t slot = s - ni;
+        slot_leaf[slot] = leaf;
+        for (int c = 0; c < CT; ++c)
+          pay[slot * CT + c] = c < d->n_outputs ? d->payload[(lb + leaf) * d->n_outputs + c] : 0.0f;
+      }
+    }
+  }
+  (void)ns;
+}
+
+static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out) {
+  if (int s = validate(d)) return s;
+  std::unique_ptr<cmlb_forest> f(new cmlb_forest());
+  DeviceGuard guard(device);
+  f->device = device;
+  f->T = d->n_trees; f->F = d->n_features; f->C = d->n_outputs;
+  f->CT = class_width(f->C);
+  f->agg = d->aggregation; f->tail = d->tail; f->out_dt = d->out_dtype;
+  f->dense_sel = d->dense_selector ? 1 : 0;
+  f->lr = d->learning_rate; f->base = d->base_score;
+  f->n_classes = d->n_classes;
+  const bool pairwise = f->C == 1 && f->agg != CMLB_AGG_NONE;
+  f->rpt = rows_per_thread(f->CT, pairwise);
+
+  int D = 0;
+  for (int t = 0; t < f->T; ++t) D = std::max(D, tree_depth(d, t));
+  f->depth = D;
+
+  // pairwise schedule
+  std::vector<uint32_t> sched;
+  if (build_schedule(f->T, sched) > SMAX)
+    return fail(CMLB_E_UNRESOLVED, "ensemble too large for the exact pairwise replay stack");
+  if (int s = upload(&f->sched, sched.data(), sched.size())) return s;
+
+  // general layout (always built: also the fallback)
+  const int64_t total_int = d->node_offset[f->T], total_leaf = d->leaf_offset[f->T];
+  {
+    std::vector<int4> nodes((size_t)std::max<int64_t>(total_int, 1));
+    for (int64_t g = 0; g < total_int; ++g) {
+      float th = d->threshold[g];
+      int bits;
+      std::memcpy(&bits, &th, 4);
+      nodes[g] = make_int4(d->feature[g], bits, d->left[g], d->right[g]);
+    }
+    std::vector<float> pay((size_t)std::max<int64_t>(total_leaf, 1) * f->CT, 0.0f);
+    for (int64_t l = 0; l < total_leaf; ++l)
+      for (int c = 0; c < f->C; ++c) pay[l * f->CT + c] = d->payload[l * f->C + c];
+    if (int s = upload(&f->gnode, nodes.data(), nodes.size())) return s;
+    if (int s = upload(&f->gpay, pay.data(), pay.size())) return s;
+    if (int s = upload(&f->node_off, d->node_offset, (size_t)f->T + 1)) return s;
+    if (int s = upload(&f->leaf_off, d->leaf_offset, (size_t)f->T + 1)) return s;
+  }
+
+  // variant choice: perfect when the padded tree fits the shared-memory plan
+  const int rows = NT * f->rpt;
+  const size_t xs_bytes = (size_t)f->F * rows * sizeof(float);
+  f->xs = xs_bytes <= XS_BUDGET;
+  int want = d->variant;
+  bool perfect_ok = D >= 1 && D <= PERFECT_MAX_DEPTH && f->F <= 65535 && f->CT <= 8 && f->xs;
+  if (perfect_ok) {
+    f->ni = (1 << D) - 1;
+    f->ns = 1 << D;
+    f->pay_off = f->ni * 4;
+    f->feat_off = f->pay_off + f->ns * f->CT * 4;
+    f->tree_bytes = (int)(((size_t)f->feat_off + (size_t)f->ni * 2 + 15) / 16 * 16);
+    const size_t avail = SMEM_LIMIT - xs_bytes;
+    int chunk = (int)(avail / f->tree_bytes) / 8 * 8;
+    if (chunk < 8) perfect_ok = false;
+    f->chunk_trees = std::min(chunk, (f->T + 7) / 8 * 8);
+  }
+  if (want == CMLB_FOREST_AUTO) want = perfect_ok ? CMLB_FOREST_PERFECT : CMLB_FOREST_GENERAL;
+  if (want == CMLB_FOREST_PERFECT && !perfect_ok)
+    return fail(CMLB_E_UNRESOLVED, "perfect layout does not fit (depth/outputs/features)");
+  f->variant = want;
+
+  if (f->variant == CMLB_FOREST_PERFECT) {
+    std::vector<uint8_t> blob((size_t)f->T * f->tree_bytes, 0);
+    std::vector<int32_t> slot_leaf((size_t)f->T * f->ns, 0);
+    for (int t = 0; t < f->T; ++t)
+      fill_perfect(d, t, D, f->CT, f->pay_off, f->feat_off, blob.data() + (size_t)t * f->tree_bytes,
+                   slot_leaf.data() + (size_t)t * f->ns);
+    if (int s = upload(&f->blob, blob.data(), blob.size())) return s;
+    if (int s = upload(&f->slot_leaf, slot_leaf.data(), slot_leaf.size())) return s;
+    f->smem = xs_bytes + (size_t)f->chunk_trees * f->tree_bytes;
+  } else {
+    f->chunk_trees = f->T;
+    f->smem = f->xs ? xs_bytes : 0;
+  }
+
+  if (f->tail != CMLB_TAIL_VALUES || d->n_classes > 0)
+    if (int s = upload(&f->classes, d->classes, (size_t)std::max(d->n_classes, 1))) return s;
+
+  KernelFn k = kernel_for(*f);
+  if (!k) return fail(CMLB_E_UNRESOLVED, "no kernel instantiation for this forest shape");
+  CMLB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f->smem));
+  *out = f.release();
+  return CMLB_OK;
+}
+
+static int run_forest(const cmlb_forest* f, const float* x, int64_t n_rows, int64_t ldx, void* y,
+                      int32_t* leaf_out, double* partial, void* stream) {
+  if (!f) return fail(CMLB_E_VALIDATION, "null forest");
+  if (n_rows < 0 || ldx < f->F) return fail(CMLB_E_INPUT, "bad input extents");
+  if (n_rows == 0) return CMLB_OK;
+  if (!x || (!y && !partial)) return fail(CMLB_E_VALIDATION, "null input/output pointer");
+  DeviceGuard guard(f->device);
+  ForestArgs a{};
+  a.x = x; a.n_rows = n_rows; a.ldx = ldx; a.y = y; a.leaf_out = leaf_out; a.partial = partial;
+  a.T = f->T; a.F = f->F; a.C = f->C; a.depth = f->depth; a.ni = f->ni; a.ns = f->ns;
+  a.tree_bytes = f->tree_bytes; a.chunk_trees = f->chunk_trees; a.rows_per_cta = NT * f->rpt;
+  a.blob = f->blob; a.slot_leaf = f->slot_leaf; a.gnode = f->gnode; a.node_off = f->node_off;
+  a.gpay = f->gpay; a.leaf_off = f->leaf_off; a.sched = f->sched;
+  a.agg = f->agg; a.tail = f->tail; a.out_dt = f->out_dt; a.dense_sel = f->dense_sel;
+  a.n_classes = f->n_classes; a.lr = f->lr; a.base = f->base; a.classes = f->classes;
+  a.pay_off = f->pay_off; a.feat_off = f->feat_off;
+  KernelFn k = kernel_for(*f);
+  const int64_t rows = (int64_t)NT * f->rpt;
+  const int64_t grid = ceil_div(n_rows, rows);
+  if (grid > 0x7fffffff) return fail(CMLB_E_INPUT, "too many rows for one launch");
+  k<<<(unsigned)grid, NT, f->smem, (cudaStream_t)stream>>>(a);
+  note_launch();
+  CMLB_CUDA(cudaGetLastError());
+  return CMLB_OK;
+}
+
+}  // namespace cmlb
+
+extern "C" {
+
+int cmlb_forest_create(const cmlb_forest_desc* desc, int device, cmlb_forest** out) {
+  if (!out) return cmlb::fail(CMLB_E_VALIDATION, "null output handle");
+  *out = nullptr;
+  try {
+    return cmlb::make_forest(desc, device, out);
+  } catch (const std::exception& e) {
+    return cmlb::fail(CMLB_E_DEVICE, std::string("forest create: ") + e.what());
+  }
+}
+
+int cmlb_forest_run(const cmlb_forest* f, const float* x, int64_t n_rows, int64_t ldx, void* y,
+                    int32_t* leaf_out, void* stream) {
+  return cmlb::run_forest(f, x, n_rows, ldx, y, leaf_out, nullptr, stream);
+}
+
+int cmlb_forest_partial(const cmlb_forest* f, const float* x, int64_t n_rows, int64_t ldx,
+                        double* partial, void* stream) {
+  if (!partial) return cmlb::fail(CMLB_E_VALIDATION, "null partial buffer");
+  return cmlb::run_forest(f, x, n_rows, ldx, nullptr, nullptr, partial, stream);
+}
+
+int cmlb_forest_info(const cmlb_forest* f, int32_t* variant, int32_t* depth, int32_t* chunk_trees,
+                     int32_t* rows_per_cta) {
+  if (!f) return cmlb::fail(CMLB_E_VALIDATION, "null forest");
+  if (variant) *variant = f->variant;
+  if (depth) *depth = f->depth;
+  if (chunk_trees) *chunk_trees = f->chunk_trees;
+  if (rows_per_cta) *rows_per_cta = cmlb::NT * f->rpt;
+  return CMLB_OK;
+}
+
+void cmlb_forest_destroy(cmlb_forest* f) { delete f; }
+
+// Host-only helper exported for tests: the pairwise schedule codes.
+int cmlb_debug_pairwise_schedule(int64_t n, uint32_t* codes) {
+  std::vector<uint32_t> v;
+  int depth = cmlb::build_schedule(n, v);
+  if (codes) std::copy(v.begin(), v.end(), codes);
+  return depth;
+}
+
+}  // extern "C"
