@@ -18,6 +18,7 @@ from paper_2301_13441_b200 import api, lower  # noqa: E402
 from paper_2301_13441_b200 import _native as N  # noqa: E402
 from paper_2301_13441_b200.planio import load_plan_file  # noqa: E402
 from paper_2301_13441_b200.runtime import DeviceProgram  # noqa: E402
+from paper_2301_13441_b200.errors import UnresolvedKernel  # noqa: E402
 
 
 def _same(got, want):
@@ -53,7 +54,11 @@ def test_leaf_indices_and_variants(name, variant):
     if variant == N.FOREST_PERFECT and (max(t.depth() for t in st.trees) > 11
                                          or max(t.depth() for t in st.trees) == 0):
         pytest.skip("too deep / no internal node for the perfect layout")
-    prog = DeviceProgram(spec, 0, forest_variant=variant)
+    try:
+        prog = DeviceProgram(spec, 0, forest_variant=variant)
+    except UnresolvedKernel:
+        assert variant == N.FOREST_PERFECT
+        pytest.skip("perfect layout does not fit this forest")
     x = torch.from_numpy(case.x).cuda()
     leaves = torch.full((x.shape[0], len(st.trees)), -7, dtype=torch.int32, device="cuda")
     y = prog.run(x, leaf_out=leaves)
