@@ -122,7 +122,7 @@ struct ForestArgs {
   int32_t* leaf_out;
   double* partial;
   // program
-  int T, F, C, depth, ni, ns, tree_bytes, chunk_trees, rows_per_cta;
+  int T, F, C, depth, ni, ns, tree_bytes, chunk_trees, rows_per_cta, stage_cap;
   const uint8_t* blob;        // perfect: [T][tree_bytes]
   const int32_t* slot_leaf;   // perfect: [T][ns]
   const int4* gnode;          // general: packed nodes
@@ -134,6 +134,10 @@ struct ForestArgs {
   float lr, base;
   const double* classes;
   int pay_off, feat_off;      // byte offsets of payload / feature arrays inside a perfect tree blob
+  // ranked variant: per-feature sorted unique thresholds
+  const float* uthr;
+  const int32_t* uoff;        // [F + 1]
+  int node_off_bytes;         // byte offset of the node words inside a ranked tree blob
 };
 
 constexpr int NT = 256;  // threads per CTA for every forest kernel
@@ -424,6 +428,157 @@ __global__ void __launch_bounds__(NT) forest_kernel(const ForestArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// RANKED variant: perfect trees with rank-quantized thresholds
+// ---------------------------------------------------------------------------
+//
+// For feature f let U_f be the sorted unique thresholds the forest tests on f.
+// With rank(x) = #{u in U_f : u < x}:   x > U_f[k]  <=>  rank(x) > k   exactly
+// (NaN compares false -> rank 0 -> goes left; +inf -> |U_f| -> right of every
+// finite threshold; dummy nodes use k = 0xFFFF, never exceeded because
+// |U_f| <= 65534).  So each row is ranked once per feature (binary search in
+// shared memory, U_f staged per feature) and every node becomes ONE 32-bit
+// word (rank << 16 | feature): a tree level costs one node load and one u16
+// rank load instead of feature + threshold + float x loads.
+
+__device__ __forceinline__ int count_less(const float* u, int n, float x) {
+  int pos = 0;
+  for (int step = n ? (1 << (31 - __clz(n))) : 0; step > 0; step >>= 1)
+    if (pos + step <= n && u[pos + step - 1] < x) pos += step;
+  return pos;
+}
+
+template <int CT, int NTT, int RPT, bool PW>
+__global__ void __launch_bounds__(NTT) forest_ranked_kernel(const ForestArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int ROWS = NTT * RPT;
+  const int tid = threadIdx.x;
+  const int64_t tile = (int64_t)blockIdx.x * ROWS;
+  const int F = a.F;
+  uint16_t* xr = reinterpret_cast<uint16_t*>(smem);
+  uint8_t* chunk = smem + (((size_t)F * ROWS * 2 + 15) & ~(size_t)15);
+
+  int64_t rowk[RPT];
+  int nbad[RPT];
+#pragma unroll
+  for (int k = 0; k < RPT; ++k) {
+    rowk[k] = tile + tid + k * NTT;
+    nbad[k] = 0;
+    if (a.dense_sel && rowk[k] < a.n_rows) {
+      const float* src = a.x + rowk[k] * a.ldx;
+      for (int f = 0; f < F; ++f) nbad[k] += !isfinite(__ldg(src + f));
+    }
+  }
+
+  // ---- rank the row tile, eight features per global read burst -----------
+  const int half = a.stage_cap;  // floats per staging buffer (two buffers)
+  float* stage0 = reinterpret_cast<float*>(chunk);
+  for (int g0 = 0; g0 < F; g0 += 8) {
+    float xv[RPT][8];
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) {
+      const float* src = a.x + rowk[k] * a.ldx;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float v = 0.0f;
+        if (rowk[k] < a.n_rows && g0 + j < F) {
+          v = __ldg(src + g0 + j);
+          if (nbad[k] && (nbad[k] >= 2 || isfinite(v))) v = __int_as_float(0x7fc00000);
+        }
+        xv[k][j] = v;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int f = g0 + j;
+      if (f < F) {  // uniform across the CTA
+        float* stage = stage0 + (f & 1) * half;
+        const int u0 = __ldg(a.uoff + f), nf = __ldg(a.uoff + f + 1) - u0;
+        for (int i = tid; i < nf; i += NTT) stage[i] = __ldg(a.uthr + u0 + i);
+        __syncthreads();  // stage f ready; every reader of stage f-2's buffer is done
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) xr[f * ROWS + tid + k * NTT] = (uint16_t)count_less(stage, nf, xv[k][j]);
+      }
+    }
+  }
+
+  RowAcc<CT, PW> acc[RPT];
+#pragma unroll
+  for (int k = 0; k < RPT; ++k) acc[k].init();
+
+  const int T = a.T;
+  const int D = a.depth;
+  const int NI = a.ni;
+  for (int c0 = 0; c0 < T; c0 += a.chunk_trees) {
+    const int nt = min(a.chunk_trees, T - c0);
+    __syncthreads();  // ranks complete / previous chunk consumed
+    {
+      const int4* src = reinterpret_cast<const int4*>(a.blob + (size_t)c0 * a.tree_bytes);
+      int4* dst = reinterpret_cast<int4*>(chunk);
+      const int n16 = nt * a.tree_bytes / 16;
+      for (int i = tid; i < n16; i += NTT) dst[i] = __ldg(src + i);
+    }
+    __syncthreads();
+    for (int tg = 0; tg < nt; tg += 8) {
+      // two trees per step (J, J+1): four independent walks per thread
+      auto pair_step = [&](auto jconst) {
+        constexpr int J = decltype(jconst)::value;
+        const int tl0 = tg + J;
+        if (tl0 >= nt) return;
+        const bool has1 = tl0 + 1 < nt;
+        const uint8_t* tb0 = chunk + (size_t)tl0 * a.tree_bytes;
+        const uint8_t* tb1 = has1 ? tb0 + a.tree_bytes : tb0;
+        const uint32_t* nd0 = reinterpret_cast<const uint32_t*>(tb0 + a.node_off_bytes);
+        const uint32_t* nd1 = reinterpret_cast<const uint32_t*>(tb1 + a.node_off_bytes);
+        int i0[RPT], i1[RPT];
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) { i0[k] = 0; i1[k] = 0; }
+        for (int lvl = 0; lvl < D; ++lvl) {
+#pragma unroll
+          for (int k = 0; k < RPT; ++k) {
+            const int rk = tid + k * NTT;
+            const uint32_t w0 = nd0[i0[k]];
+            const uint32_t w1 = nd1[i1[k]];
+            const uint32_t r0 = xr[(w0 & 0xFFFFu) * ROWS + rk];
+            const uint32_t r1 = xr[(w1 & 0xFFFFu) * ROWS + rk];
+            i0[k] = 2 * i0[k] + 1 + (r0 > (w0 >> 16) ? 1 : 0);
+            i1[k] = 2 * i1[k] + 1 + (r1 > (w1 >> 16) ? 1 : 0);
+          }
+        }
+        const float* pay0 = reinterpret_cast<const float*>(tb0);
+        const float* pay1 = reinterpret_cast<const float*>(tb1);
+        const int t0 = c0 + tl0;
+        const uint32_t code0 = PW ? __ldg(a.sched + t0) : 0u;
+        const uint32_t code1 = (PW && has1) ? __ldg(a.sched + t0 + 1) : 0u;
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) {
+          const int s0 = i0[k] - NI, s1 = i1[k] - NI;
+          float v0[CT], v1[CT];
+#pragma unroll
+          for (int c = 0; c < CT; ++c) { v0[c] = pay0[s0 * CT + c]; v1[c] = pay1[s1 * CT + c]; }
+          if (a.leaf_out && rowk[k] < a.n_rows) {
+            a.leaf_out[rowk[k] * T + t0] = __ldg(a.slot_leaf + (int64_t)t0 * a.ns + s0);
+            if (has1) a.leaf_out[rowk[k] * T + t0 + 1] = __ldg(a.slot_leaf + (int64_t)(t0 + 1) * a.ns + s1);
+          }
+          accumulate<J, CT>(acc[k], v0, a.C, code0);
+          if (has1) accumulate<J + 1, CT>(acc[k], v1, a.C, code1);
+        }
+      };
+      pair_step(std::integral_constant<int, 0>{});
+      pair_step(std::integral_constant<int, 2>{});
+      pair_step(std::integral_constant<int, 4>{});
+      pair_step(std::integral_constant<int, 6>{});
+    }
+  }
+
+  float none[CT];
+#pragma unroll
+  for (int c = 0; c < CT; ++c) none[c] = 0.0f;
+#pragma unroll
+  for (int k = 0; k < RPT; ++k)
+    if (rowk[k] < a.n_rows) finish_row<CT, PW>(a, rowk[k], acc[k], none);
+}
+
+// ---------------------------------------------------------------------------
 // host program
 // ---------------------------------------------------------------------------
 
@@ -448,9 +603,13 @@ struct cmlb_forest {
   int64_t* leaf_off = nullptr;
   uint32_t* sched = nullptr;
   double* classes = nullptr;
+  float* uthr = nullptr;
+  int32_t* uoff = nullptr;
+  int ntt = 256, stage_cap = 0, node_off_bytes = 0;
   ~cmlb_forest() {
     cudaFree(blob); cudaFree(slot_leaf); cudaFree(gnode); cudaFree(node_off);
     cudaFree(gpay); cudaFree(leaf_off); cudaFree(sched); cudaFree(classes);
+    cudaFree(uthr); cudaFree(uoff);
   }
 };
 
@@ -491,7 +650,25 @@ static KernelFn pick4(bool perfect, bool xs) {
   return xs ? forest_kernel<CT, R, false, true, PW> : forest_kernel<CT, R, false, false, PW>;
 }
 
+template <int CT, bool PW>
+static KernelFn ranked3(int ntt, int rpt) {
+  if (ntt == 512) return forest_ranked_kernel<CT, 512, 2, PW>;
+  if (rpt == 2) return forest_ranked_kernel<CT, 256, 2, PW>;
+  return forest_ranked_kernel<CT, 256, 1, PW>;
+}
+
+static KernelFn ranked_for(const cmlb_forest& f) {
+  const bool pw = f.C == 1;
+  switch (f.CT) {
+    case 1: return pw ? ranked3<1, true>(f.ntt, f.rpt) : ranked3<1, false>(f.ntt, f.rpt);
+    case 2: return ranked3<2, false>(f.ntt, f.rpt);
+    case 4: return ranked3<4, false>(f.ntt, f.rpt);
+    default: return ranked3<8, false>(f.ntt, f.rpt);
+  }
+}
+
 static KernelFn kernel_for(const cmlb_forest& f) {
+  if (f.variant == CMLB_FOREST_RANKED) return ranked_for(f);
   const bool perfect = f.variant == CMLB_FOREST_PERFECT;
   const bool pw = f.C == 1 && f.agg != CMLB_AGG_NONE;
   switch (f.CT) {
@@ -589,6 +766,42 @@ static void fill_perfect(const cmlb_forest_desc* d, int t, int D, int CT, int pa
   (void)ns;
 }
 
+// Heap-ordered perfect padding with rank-quantized node words:
+// blob = [payload: ns x CT floats][nodes: ni x u32 (rank << 16 | feature)].
+static void fill_ranked(const cmlb_forest_desc* d, int t, int D, int CT, int node_off_bytes,
+                        const std::vector<std::vector<float>>& U, uint8_t* blob, int32_t* slot_leaf) {
+  const int ni = (1 << D) - 1;
+  float* pay = reinterpret_cast<float*>(blob);
+  uint32_t* nodes = reinterpret_cast<uint32_t*>(blob + node_off_bytes);
+  for (int i = 0; i < ni; ++i) nodes[i] = 0xFFFFu << 16;  // always left
+  const int64_t nb = d->node_offset[t], lb = d->leaf_offset[t];
+  std::deque<std::pair<int64_t, int32_t>> q;
+  q.push_back({0, d->node_offset[t + 1] > nb ? 0 : -1});
+  while (!q.empty()) {
+    auto [h, ref] = q.front();
+    q.pop_front();
+    if (ref >= 0) {
+      const int f = d->feature[nb + ref];
+      const float th = d->threshold[nb + ref];
+      const auto& u = U[f];
+      const uint32_t rank = (uint32_t)(std::lower_bound(u.begin(), u.end(), th) - u.begin());
+      nodes[h] = (rank << 16) | (uint32_t)f;
+      q.push_back({2 * h + 1, d->left[nb + ref]});
+      q.push_back({2 * h + 2, d->right[nb + ref]});
+    } else {
+      const int leaf = -1 - ref;
+      int64_t lo = h, hi = h;
+      while (lo < ni) { lo = 2 * lo + 1; hi = 2 * hi + 2; }
+      for (int64_t sidx = lo; sidx <= hi; ++sidx) {
+        const int64_t slot = sidx - ni;
+        slot_leaf[slot] = leaf;
+        for (int c = 0; c < CT; ++c)
+          pay[slot * CT + c] = c < d->n_outputs ? d->payload[(lb + leaf) * d->n_outputs + c] : 0.0f;
+      }
+    }
+  }
+}
+
 static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out) {
   if (int s = validate(d)) return s;
   std::unique_ptr<cmlb_forest> f(new cmlb_forest());
@@ -649,12 +862,78 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
     if (chunk < 8) perfect_ok = false;
     f->chunk_trees = std::min(chunk, (f->T + 7) / 8 * 8);
   }
-  if (want == CMLB_FOREST_AUTO) want = perfect_ok ? CMLB_FOREST_PERFECT : CMLB_FOREST_GENERAL;
+  // ranked plan: per-feature sorted unique thresholds, smem split between the
+  // u16 rank tile, two staging buffers (ranking) and the tree chunk (walk)
+  std::vector<std::vector<float>> U;
+  bool ranked_ok = D >= 1 && D <= PERFECT_MAX_DEPTH && f->CT <= 8 && f->agg != CMLB_AGG_NONE;
+  int r_ntt = 0, r_rpt = 0, r_chunk = 0, r_tree_bytes = 0, r_node_off = 0, r_stage = 0;
+  size_t r_smem = 0;
+  if (ranked_ok) {
+    U.assign(f->F, {});
+    for (int64_t g = 0; g < total_int; ++g) U[d->feature[g]].push_back(d->threshold[g]);
+    size_t max_nf = 0;
+    for (auto& u : U) {
+      std::sort(u.begin(), u.end());
+      u.erase(std::unique(u.begin(), u.end()), u.end());
+      max_nf = std::max(max_nf, u.size());
+    }
+    const int ni_r = (1 << D) - 1, ns_r = 1 << D;
+    r_node_off = ns_r * f->CT * 4;
+    r_tree_bytes = (int)(((size_t)r_node_off + (size_t)ni_r * 4 + 15) / 16 * 16);
+    ranked_ok = max_nf <= 65534;
+    const int cands[3][2] = {{512, 2}, {256, 2}, {256, 1}};
+    bool found = false;
+    for (int ci = 0; ci < 3 && ranked_ok && !found; ++ci) {
+      const int ntt = cands[ci][0], rpt = cands[ci][1];
+      if (f->C == 1 && ntt == 512) continue;  // pairwise replay: register budget
+      const size_t xr = ((size_t)f->F * ntt * rpt * 2 + 15) / 16 * 16;
+      if (xr + 2 * 4 * max_nf + 64 > SMEM_LIMIT) continue;
+      const size_t avail = SMEM_LIMIT - xr;
+      const int chunk = (int)(avail / r_tree_bytes) / 8 * 8;
+      if (chunk < 8) continue;
+      r_ntt = ntt; r_rpt = rpt;
+      r_chunk = std::min(chunk, (f->T + 7) / 8 * 8);
+      const size_t chunk_bytes = std::max((size_t)r_chunk * r_tree_bytes, 2 * 4 * max_nf + 32);
+      r_stage = (int)((max_nf + 3) / 4 * 4);
+      r_smem = xr + std::max(chunk_bytes, (size_t)2 * 4 * r_stage);
+      if (r_smem > SMEM_LIMIT) continue;
+      found = true;
+    }
+    ranked_ok = ranked_ok && found;
+  }
+
+  if (want == CMLB_FOREST_AUTO)
+    want = ranked_ok ? CMLB_FOREST_RANKED : (perfect_ok ? CMLB_FOREST_PERFECT : CMLB_FOREST_GENERAL);
   if (want == CMLB_FOREST_PERFECT && !perfect_ok)
     return fail(CMLB_E_UNRESOLVED, "perfect layout does not fit (depth/outputs/features)");
+  if (want == CMLB_FOREST_RANKED && !ranked_ok)
+    return fail(CMLB_E_UNRESOLVED, "ranked layout does not fit (depth/outputs/thresholds)");
   f->variant = want;
 
-  if (f->variant == CMLB_FOREST_PERFECT) {
+  if (f->variant == CMLB_FOREST_RANKED) {
+    f->ntt = r_ntt; f->rpt = r_rpt; f->chunk_trees = r_chunk; f->tree_bytes = r_tree_bytes;
+    f->node_off_bytes = r_node_off; f->stage_cap = r_stage; f->smem = r_smem;
+    f->ni = (1 << D) - 1; f->ns = 1 << D;
+    std::vector<uint8_t> blob((size_t)f->T * f->tree_bytes, 0);
+    std::vector<int32_t> slot_leaf((size_t)f->T * f->ns, 0);
+    for (int t = 0; t < f->T; ++t)
+      fill_ranked(d, t, D, f->CT, f->node_off_bytes, U, blob.data() + (size_t)t * f->tree_bytes,
+                  slot_leaf.data() + (size_t)t * f->ns);
+    std::vector<float> uthr;
+    std::vector<int32_t> uoff(f->F + 1, 0);
+    for (int k = 0; k < f->F; ++k) {
+      uthr.insert(uthr.end(), U[k].begin(), U[k].end());
+      uoff[k + 1] = (int32_t)uthr.size();
+    }
+    if (int st = upload(&f->blob, blob.data(), blob.size())) return st;
+    if (int st = upload(&f->slot_leaf, slot_leaf.data(), slot_leaf.size())) return st;
+    if (int st = upload(&f->uthr, uthr.data(), uthr.size())) return st;
+    if (int st = upload(&f->uoff, uoff.data(), uoff.size())) return st;
+  }
+
+  if (f->variant == CMLB_FOREST_RANKED) {
+    // built above
+  } else if (f->variant == CMLB_FOREST_PERFECT) {
     std::vector<uint8_t> blob((size_t)f->T * f->tree_bytes, 0);
     std::vector<int32_t> slot_leaf((size_t)f->T * f->ns, 0);
     for (int t = 0; t < f->T; ++t)
@@ -694,11 +973,13 @@ static int run_forest(const cmlb_forest* f, const float* x, int64_t n_rows, int6
   a.agg = f->agg; a.tail = f->tail; a.out_dt = f->out_dt; a.dense_sel = f->dense_sel;
   a.n_classes = f->n_classes; a.lr = f->lr; a.base = f->base; a.classes = f->classes;
   a.pay_off = f->pay_off; a.feat_off = f->feat_off;
+  a.uthr = f->uthr; a.uoff = f->uoff; a.stage_cap = f->stage_cap; a.node_off_bytes = f->node_off_bytes;
   KernelFn k = kernel_for(*f);
-  const int64_t rows = (int64_t)NT * f->rpt;
+  const int threads = f->variant == CMLB_FOREST_RANKED ? f->ntt : NT;
+  const int64_t rows = (int64_t)threads * f->rpt;
   const int64_t grid = ceil_div(n_rows, rows);
   if (grid > 0x7fffffff) return fail(CMLB_E_INPUT, "too many rows for one launch");
-  k<<<(unsigned)grid, NT, f->smem, (cudaStream_t)stream>>>(a);
+  k<<<(unsigned)grid, threads, f->smem, (cudaStream_t)stream>>>(a);
   note_launch();
   CMLB_CUDA(cudaGetLastError());
   return CMLB_OK;
@@ -735,7 +1016,7 @@ int cmlb_forest_info(const cmlb_forest* f, int32_t* variant, int32_t* depth, int
   if (variant) *variant = f->variant;
   if (depth) *depth = f->depth;
   if (chunk_trees) *chunk_trees = f->chunk_trees;
-  if (rows_per_cta) *rows_per_cta = cmlb::NT * f->rpt;
+  if (rows_per_cta) *rows_per_cta = (f->variant == CMLB_FOREST_RANKED ? f->ntt : cmlb::NT) * f->rpt;
   return CMLB_OK;
 }
 

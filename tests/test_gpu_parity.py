@@ -45,20 +45,20 @@ def test_execute_reference_plan(name):
     assert _same(got.astype(np.float64), case.want)
 
 
-@pytest.mark.parametrize("variant", [N.FOREST_PERFECT, N.FOREST_GENERAL])
+@pytest.mark.parametrize("variant", [N.FOREST_PERFECT, N.FOREST_GENERAL, N.FOREST_RANKED])
 @pytest.mark.parametrize("name", [n for n in gc.case_names() if gc.get(n).leaves is not None])
 def test_leaf_indices_and_variants(name, variant):
     case = gc.get(name)
     spec = lower.lower_model(case.model, case.profile, case.passes)
     st = spec.stages[0]
-    if variant == N.FOREST_PERFECT and (max(t.depth() for t in st.trees) > 11
-                                         or max(t.depth() for t in st.trees) == 0):
+    if variant in (N.FOREST_PERFECT, N.FOREST_RANKED) and (max(t.depth() for t in st.trees) > 11
+                                                            or max(t.depth() for t in st.trees) == 0):
         pytest.skip("too deep / no internal node for the perfect layout")
     try:
         prog = DeviceProgram(spec, 0, forest_variant=variant)
     except UnresolvedKernel:
-        assert variant == N.FOREST_PERFECT
-        pytest.skip("perfect layout does not fit this forest")
+        assert variant in (N.FOREST_PERFECT, N.FOREST_RANKED)
+        pytest.skip("perfect/ranked layout does not fit this forest")
     x = torch.from_numpy(case.x).cuda()
     leaves = torch.full((x.shape[0], len(st.trees)), -7, dtype=torch.int32, device="cuda")
     y = prog.run(x, leaf_out=leaves)
@@ -159,13 +159,21 @@ def test_large_synthetic_vs_c_oracle(T, depth, F, C, gbdt, n):
     x[::997, 3] = np.nan
     x[::1013, 5] = np.inf
     want, want_leaves = fast.forest_predict(fast.PackedForest(m), x, want_leaves=True)
-    compiled = api.compile_model(m)
-    prog = compiled.program(0)
+    spec = lower.lower_model(m)
     xd = torch.from_numpy(x).cuda()
-    leaves = torch.empty((n, T), dtype=torch.int32, device="cuda")
-    y = prog.run(xd, leaf_out=leaves).cpu().numpy().astype(np.float64)
-    np.testing.assert_array_equal(leaves.cpu().numpy(), want_leaves)
-    assert _same(y, want)
+    ran = 0
+    for variant in (N.FOREST_AUTO, N.FOREST_RANKED, N.FOREST_PERFECT, N.FOREST_GENERAL):
+        try:
+            prog = DeviceProgram(spec, 0, forest_variant=variant)
+        except UnresolvedKernel:
+            continue
+        leaves = torch.empty((n, T), dtype=torch.int32, device="cuda")
+        y = prog.run(xd, leaf_out=leaves).cpu().numpy().astype(np.float64)
+        np.testing.assert_array_equal(leaves.cpu().numpy(), want_leaves)
+        assert _same(y, want), f"variant {variant} ({prog.forest().info()})"
+        prog.close()
+        ran += 1
+    assert ran >= 2
 
 
 def test_pinned_host_streaming_matches_device():
