@@ -36,6 +36,7 @@
 //           stack.  Verified against numpy in tests/test_pairwise_schedule.py.
 
 #include <algorithm>
+#include <cstdlib>
 #include <limits>
 #include <cstring>
 #include <deque>
@@ -447,21 +448,33 @@ __device__ __forceinline__ int count_less(const float* u, int n, float x) {
   return pos;
 }
 
-template <int CT, int NTT, int RPT, bool PW>
+template <int CT, int NTT, int RPT, int TI, bool PW>
 __global__ void __launch_bounds__(NTT) forest_ranked_kernel(const ForestArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int ROWS = NTT * RPT;
+  static_assert(ROWS % 64 == 0, "rank tile interleave needs 64-row groups");
+  static_assert(TI == 2 || TI == 4, "trees per step");
   const int tid = threadIdx.x;
   const int64_t tile = (int64_t)blockIdx.x * ROWS;
   const int F = a.F;
   uint16_t* xr = reinterpret_cast<uint16_t*>(smem);
-  uint8_t* chunk = smem + (((size_t)F * ROWS * 2 + 15) & ~(size_t)15);
+  const uint32_t chunk_off = (uint32_t)(((size_t)F * ROWS * 2 + 15) & ~(size_t)15);
+  uint8_t* chunk = smem + chunk_off;
 
+  // Rank tile layout: u16 rank of (feature f, row r) at byte f*ROWS*2 + pb(r)
+  // with pb(r) = 2*((r/64)*64 + (r%32)*2 + (r/32)%2): rows r and r+32 share a
+  // 32-bit word, so lane l of every warp owns bank l for every feature and the
+  // per-level gathers are conflict-free whatever features the lanes test.
+  // Node words carry the feature as that byte offset (f*ROWS*2 < 65536, its
+  // bits disjoint from pb's), so a gather address is one LOP3.
   int64_t rowk[RPT];
+  uint32_t pb[RPT];
   int nbad[RPT];
 #pragma unroll
   for (int k = 0; k < RPT; ++k) {
-    rowk[k] = tile + tid + k * NTT;
+    const int r = tid + k * NTT;
+    rowk[k] = tile + r;
+    pb[k] = 2u * (uint32_t)(((r >> 6) << 6) | ((r & 31) << 1) | ((r >> 5) & 1));
     nbad[k] = 0;
     if (a.dense_sel && rowk[k] < a.n_rows) {
       const float* src = a.x + rowk[k] * a.ldx;
@@ -495,8 +508,10 @@ __global__ void __launch_bounds__(NTT) forest_ranked_kernel(const ForestArgs a) 
         const int u0 = __ldg(a.uoff + f), nf = __ldg(a.uoff + f + 1) - u0;
         for (int i = tid; i < nf; i += NTT) stage[i] = __ldg(a.uthr + u0 + i);
         __syncthreads();  // stage f ready; every reader of stage f-2's buffer is done
+        uint8_t* xrow = reinterpret_cast<uint8_t*>(xr) + (size_t)f * ROWS * 2;
 #pragma unroll
-        for (int k = 0; k < RPT; ++k) xr[f * ROWS + tid + k * NTT] = (uint16_t)count_less(stage, nf, xv[k][j]);
+        for (int k = 0; k < RPT; ++k)
+          *reinterpret_cast<uint16_t*>(xrow + pb[k]) = (uint16_t)count_less(stage, nf, xv[k][j]);
       }
     }
   }
@@ -507,7 +522,7 @@ __global__ void __launch_bounds__(NTT) forest_ranked_kernel(const ForestArgs a) 
 
   const int T = a.T;
   const int D = a.depth;
-  const int NI = a.ni;
+  const uint8_t* xrb = reinterpret_cast<const uint8_t*>(xr);
   for (int c0 = 0; c0 < T; c0 += a.chunk_trees) {
     const int nt = min(a.chunk_trees, T - c0);
     __syncthreads();  // ranks complete / previous chunk consumed
@@ -519,54 +534,75 @@ __global__ void __launch_bounds__(NTT) forest_ranked_kernel(const ForestArgs a) 
     }
     __syncthreads();
     for (int tg = 0; tg < nt; tg += 8) {
-      // two trees per step (J, J+1): four independent walks per thread
-      auto pair_step = [&](auto jconst) {
+      // TI trees per step: TI * RPT independent walks per thread.  Nodes are
+      // addressed by byte offset o inside dynamic shared memory; the children
+      // of the node at o are at 2*o + (4 - base) and 4 bytes further.
+      auto group_step = [&](auto jconst) {
         constexpr int J = decltype(jconst)::value;
         const int tl0 = tg + J;
         if (tl0 >= nt) return;
-        const bool has1 = tl0 + 1 < nt;
-        const uint8_t* tb0 = chunk + (size_t)tl0 * a.tree_bytes;
-        const uint8_t* tb1 = has1 ? tb0 + a.tree_bytes : tb0;
-        const uint32_t* nd0 = reinterpret_cast<const uint32_t*>(tb0 + a.node_off_bytes);
-        const uint32_t* nd1 = reinterpret_cast<const uint32_t*>(tb1 + a.node_off_bytes);
-        int i0[RPT], i1[RPT];
+        uint32_t base[TI], cst[TI];
+        bool has[TI];
 #pragma unroll
-        for (int k = 0; k < RPT; ++k) { i0[k] = 0; i1[k] = 0; }
+        for (int q = 0; q < TI; ++q) {
+          has[q] = tl0 + q < nt;
+          const int tl = has[q] ? tl0 + q : tl0;
+          base[q] = chunk_off + (uint32_t)tl * a.tree_bytes + a.node_off_bytes;
+          cst[q] = 4u - base[q];
+        }
+        uint32_t o[TI][RPT];
+#pragma unroll
+        for (int q = 0; q < TI; ++q)
+#pragma unroll
+          for (int k = 0; k < RPT; ++k) o[q][k] = base[q];
         for (int lvl = 0; lvl < D; ++lvl) {
 #pragma unroll
-          for (int k = 0; k < RPT; ++k) {
-            const int rk = tid + k * NTT;
-            const uint32_t w0 = nd0[i0[k]];
-            const uint32_t w1 = nd1[i1[k]];
-            const uint32_t r0 = xr[(w0 & 0xFFFFu) * ROWS + rk];
-            const uint32_t r1 = xr[(w1 & 0xFFFFu) * ROWS + rk];
-            i0[k] = 2 * i0[k] + 1 + (r0 > (w0 >> 16) ? 1 : 0);
-            i1[k] = 2 * i1[k] + 1 + (r1 > (w1 >> 16) ? 1 : 0);
+          for (int q = 0; q < TI; ++q) {
+#pragma unroll
+            for (int k = 0; k < RPT; ++k) {
+              const uint32_t w = *reinterpret_cast<const uint32_t*>(smem + o[q][k]);
+              const uint32_t rk = *reinterpret_cast<const uint16_t*>(xrb + ((w & 0xFFFFu) | pb[k]));
+              uint32_t nx = 2u * o[q][k] + cst[q];
+              if (rk > (w >> 16)) nx += 4u;
+              o[q][k] = nx;
+            }
           }
         }
-        const float* pay0 = reinterpret_cast<const float*>(tb0);
-        const float* pay1 = reinterpret_cast<const float*>(tb1);
         const int t0 = c0 + tl0;
-        const uint32_t code0 = PW ? __ldg(a.sched + t0) : 0u;
-        const uint32_t code1 = (PW && has1) ? __ldg(a.sched + t0 + 1) : 0u;
+        auto finish_tree = [&](auto qconst) {
+          constexpr int q = decltype(qconst)::value;
+          if constexpr (q < TI) {
+            if (!has[q]) return;
+            const int t = t0 + q;
+            const uint32_t code = PW ? __ldg(a.sched + t) : 0u;
+            const uint8_t* tb = smem + base[q] - a.node_off_bytes;
 #pragma unroll
-        for (int k = 0; k < RPT; ++k) {
-          const int s0 = i0[k] - NI, s1 = i1[k] - NI;
-          float v0[CT], v1[CT];
+            for (int k = 0; k < RPT; ++k) {
+              const int slot = (int)((o[q][k] - base[q]) >> 2) - a.ni;
+              const float* pay = reinterpret_cast<const float*>(tb) + slot * CT;
+              float v[CT];
 #pragma unroll
-          for (int c = 0; c < CT; ++c) { v0[c] = pay0[s0 * CT + c]; v1[c] = pay1[s1 * CT + c]; }
-          if (a.leaf_out && rowk[k] < a.n_rows) {
-            a.leaf_out[rowk[k] * T + t0] = __ldg(a.slot_leaf + (int64_t)t0 * a.ns + s0);
-            if (has1) a.leaf_out[rowk[k] * T + t0 + 1] = __ldg(a.slot_leaf + (int64_t)(t0 + 1) * a.ns + s1);
+              for (int c = 0; c < CT; ++c) v[c] = pay[c];
+              if (a.leaf_out && rowk[k] < a.n_rows)
+                a.leaf_out[rowk[k] * T + t] = __ldg(a.slot_leaf + (int64_t)t * a.ns + slot);
+              accumulate<(J + q) & 7, CT>(acc[k], v, a.C, code);
+            }
           }
-          accumulate<J, CT>(acc[k], v0, a.C, code0);
-          if (has1) accumulate<J + 1, CT>(acc[k], v1, a.C, code1);
-        }
+        };
+        finish_tree(std::integral_constant<int, 0>{});
+        finish_tree(std::integral_constant<int, 1>{});
+        finish_tree(std::integral_constant<int, 2>{});
+        finish_tree(std::integral_constant<int, 3>{});
       };
-      pair_step(std::integral_constant<int, 0>{});
-      pair_step(std::integral_constant<int, 2>{});
-      pair_step(std::integral_constant<int, 4>{});
-      pair_step(std::integral_constant<int, 6>{});
+      if constexpr (TI == 2) {
+        group_step(std::integral_constant<int, 0>{});
+        group_step(std::integral_constant<int, 2>{});
+        group_step(std::integral_constant<int, 4>{});
+        group_step(std::integral_constant<int, 6>{});
+      } else {
+        group_step(std::integral_constant<int, 0>{});
+        group_step(std::integral_constant<int, 4>{});
+      }
     }
   }
 
@@ -605,7 +641,7 @@ struct cmlb_forest {
   double* classes = nullptr;
   float* uthr = nullptr;
   int32_t* uoff = nullptr;
-  int ntt = 256, stage_cap = 0, node_off_bytes = 0;
+  int ntt = 256, stage_cap = 0, node_off_bytes = 0, rcfg = 0;
   ~cmlb_forest() {
     cudaFree(blob); cudaFree(slot_leaf); cudaFree(gnode); cudaFree(node_off);
     cudaFree(gpay); cudaFree(leaf_off); cudaFree(sched); cudaFree(classes);
@@ -650,20 +686,38 @@ static KernelFn pick4(bool perfect, bool xs) {
   return xs ? forest_kernel<CT, R, false, true, PW> : forest_kernel<CT, R, false, false, PW>;
 }
 
+// Ranked launch configurations: (threads, rows per thread, trees per step).
+struct RankedCfg { int ntt, rpt, ti; };
+constexpr RankedCfg RANKED_CFGS[] = {
+    {512, 2, 2}, {512, 2, 4}, {1024, 1, 2}, {1024, 1, 4}, {256, 2, 2}, {256, 1, 2}, {128, 2, 2}};
+constexpr int N_RANKED_CFGS = sizeof(RANKED_CFGS) / sizeof(RANKED_CFGS[0]);
+
 template <int CT, bool PW>
-static KernelFn ranked3(int ntt, int rpt) {
-  if (ntt == 512) return forest_ranked_kernel<CT, 512, 2, PW>;
-  if (rpt == 2) return forest_ranked_kernel<CT, 256, 2, PW>;
-  return forest_ranked_kernel<CT, 256, 1, PW>;
+static KernelFn ranked_cfg(int cfg) {
+  if constexpr (!PW && CT <= 2) {
+    switch (cfg) {
+      case 0: return forest_ranked_kernel<CT, 512, 2, 2, PW>;
+      case 1: return forest_ranked_kernel<CT, 512, 2, 4, PW>;
+      case 2: return forest_ranked_kernel<CT, 1024, 1, 2, PW>;
+      case 3: return forest_ranked_kernel<CT, 1024, 1, 4, PW>;
+      default: break;
+    }
+  }
+  switch (cfg) {
+    case 4: return forest_ranked_kernel<CT, 256, 2, 2, PW>;
+    case 5: return forest_ranked_kernel<CT, 256, 1, 2, PW>;
+    case 6: return forest_ranked_kernel<CT, 128, 2, 2, PW>;
+    default: return nullptr;
+  }
 }
 
 static KernelFn ranked_for(const cmlb_forest& f) {
   const bool pw = f.C == 1;
   switch (f.CT) {
-    case 1: return pw ? ranked3<1, true>(f.ntt, f.rpt) : ranked3<1, false>(f.ntt, f.rpt);
-    case 2: return ranked3<2, false>(f.ntt, f.rpt);
-    case 4: return ranked3<4, false>(f.ntt, f.rpt);
-    default: return ranked3<8, false>(f.ntt, f.rpt);
+    case 1: return pw ? ranked_cfg<1, true>(f.rcfg) : ranked_cfg<1, false>(f.rcfg);
+    case 2: return ranked_cfg<2, false>(f.rcfg);
+    case 4: return ranked_cfg<4, false>(f.rcfg);
+    default: return ranked_cfg<8, false>(f.rcfg);
   }
 }
 
@@ -768,7 +822,7 @@ static void fill_perfect(const cmlb_forest_desc* d, int t, int D, int CT, int pa
 
 // Heap-ordered perfect padding with rank-quantized node words:
 // blob = [payload: ns x CT floats][nodes: ni x u32 (rank << 16 | feature)].
-static void fill_ranked(const cmlb_forest_desc* d, int t, int D, int CT, int node_off_bytes,
+static void fill_ranked(const cmlb_forest_desc* d, int t, int D, int CT, int node_off_bytes, int rows,
                         const std::vector<std::vector<float>>& U, uint8_t* blob, int32_t* slot_leaf) {
   const int ni = (1 << D) - 1;
   float* pay = reinterpret_cast<float*>(blob);
@@ -785,7 +839,7 @@ static void fill_ranked(const cmlb_forest_desc* d, int t, int D, int CT, int nod
       const float th = d->threshold[nb + ref];
       const auto& u = U[f];
       const uint32_t rank = (uint32_t)(std::lower_bound(u.begin(), u.end(), th) - u.begin());
-      nodes[h] = (rank << 16) | (uint32_t)f;
+      nodes[h] = (rank << 16) | (uint32_t)(f * rows * 2);
       q.push_back({2 * h + 1, d->left[nb + ref]});
       q.push_back({2 * h + 2, d->right[nb + ref]});
     } else {
@@ -865,6 +919,7 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
   // ranked plan: per-feature sorted unique thresholds, smem split between the
   // u16 rank tile, two staging buffers (ranking) and the tree chunk (walk)
   std::vector<std::vector<float>> U;
+  const int saved_rpt = f->rpt;
   bool ranked_ok = D >= 1 && D <= PERFECT_MAX_DEPTH && f->CT <= 8 && f->agg != CMLB_AGG_NONE;
   int r_ntt = 0, r_rpt = 0, r_chunk = 0, r_tree_bytes = 0, r_node_off = 0, r_stage = 0;
   size_t r_smem = 0;
@@ -881,12 +936,19 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
     r_node_off = ns_r * f->CT * 4;
     r_tree_bytes = (int)(((size_t)r_node_off + (size_t)ni_r * 4 + 15) / 16 * 16);
     ranked_ok = max_nf <= 65534;
-    const int cands[3][2] = {{512, 2}, {256, 2}, {256, 1}};
+    // preference order (measured on B200); CMLB_RANKED_CFG forces one
+    std::vector<int> order = {2, 0, 4, 5, 6};
+    if (const char* env = getenv("CMLB_RANKED_CFG")) order = {atoi(env)};
     bool found = false;
-    for (int ci = 0; ci < 3 && ranked_ok && !found; ++ci) {
-      const int ntt = cands[ci][0], rpt = cands[ci][1];
-      if (f->C == 1 && ntt == 512) continue;  // pairwise replay: register budget
-      const size_t xr = ((size_t)f->F * ntt * rpt * 2 + 15) / 16 * 16;
+    for (size_t oi = 0; oi < order.size() && ranked_ok && !found; ++oi) {
+      const int ci = order[oi];
+      if (ci < 0 || ci >= N_RANKED_CFGS) continue;
+      const int ntt = RANKED_CFGS[ci].ntt, rpt = RANKED_CFGS[ci].rpt;
+      const int rows = ntt * rpt;
+      f->rcfg = ci; f->rpt = rpt;
+      if (ranked_for(*f) == nullptr) continue;        // not instantiated for this shape
+      if ((size_t)f->F * rows * 2 > 65536) continue;  // feature byte offset must fit 16 bits
+      const size_t xr = ((size_t)f->F * rows * 2 + 15) / 16 * 16;
       if (xr + 2 * 4 * max_nf + 64 > SMEM_LIMIT) continue;
       const size_t avail = SMEM_LIMIT - xr;
       const int chunk = (int)(avail / r_tree_bytes) / 8 * 8;
@@ -902,6 +964,7 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
     ranked_ok = ranked_ok && found;
   }
 
+  f->rpt = saved_rpt;
   if (want == CMLB_FOREST_AUTO)
     want = ranked_ok ? CMLB_FOREST_RANKED : (perfect_ok ? CMLB_FOREST_PERFECT : CMLB_FOREST_GENERAL);
   if (want == CMLB_FOREST_PERFECT && !perfect_ok)
@@ -917,7 +980,7 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
     std::vector<uint8_t> blob((size_t)f->T * f->tree_bytes, 0);
     std::vector<int32_t> slot_leaf((size_t)f->T * f->ns, 0);
     for (int t = 0; t < f->T; ++t)
-      fill_ranked(d, t, D, f->CT, f->node_off_bytes, U, blob.data() + (size_t)t * f->tree_bytes,
+      fill_ranked(d, t, D, f->CT, f->node_off_bytes, f->ntt * f->rpt, U, blob.data() + (size_t)t * f->tree_bytes,
                   slot_leaf.data() + (size_t)t * f->ns);
     std::vector<float> uthr;
     std::vector<int32_t> uoff(f->F + 1, 0);

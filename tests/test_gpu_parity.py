@@ -198,3 +198,24 @@ def test_scaler_then_forest_composition():
     y = api.predict(api.compile_model(rf.model), scaled.astype(np.float32))
     want, _ = sem.predict(rf.model, scaled.astype(np.float32))
     assert _same(y.astype(np.float64), want)
+
+
+@pytest.mark.parametrize("cfg", range(7))
+def test_ranked_launch_configs(cfg, monkeypatch):
+    """Every ranked launch configuration (CMLB_RANKED_CFG) is bit-exact."""
+    monkeypatch.setenv("CMLB_RANKED_CFG", str(cfg))
+    rng = np.random.default_rng(100 + cfg)
+    for m, F in ((_synthetic_forest(rng, 37, 8, 28, 2), 28), (_synthetic_forest(rng, 150, 7, 20, 1, True), 20),
+                 (_synthetic_forest(rng, 20, 6, 12, 3), 12)):
+        x = rng.standard_normal((30_000, F)).astype(np.float32)
+        x[::101, 2] = np.nan
+        want, want_leaves = fast.forest_predict(fast.PackedForest(m), x, want_leaves=True)
+        try:
+            prog = DeviceProgram(lower.lower_model(m), 0, forest_variant=N.FOREST_RANKED)
+        except UnresolvedKernel:
+            continue  # configuration not instantiated for this shape
+        leaves = torch.empty((x.shape[0], len(m.trees)), dtype=torch.int32, device="cuda")
+        y = prog.run(torch.from_numpy(x).cuda(), leaf_out=leaves).cpu().numpy().astype(np.float64)
+        np.testing.assert_array_equal(leaves.cpu().numpy(), want_leaves)
+        assert _same(y, want), (cfg, prog.forest().info())
+        prog.close()
