@@ -136,8 +136,10 @@ struct ForestArgs {
   const double* classes;
   int pay_off, feat_off;      // byte offsets of payload / feature arrays inside a perfect tree blob
   // ranked variant: per-feature sorted unique thresholds
-  const float* uthr;
+  const float* uthr;          // per feature: sorted unique thresholds in Eytzinger (BFS) order
   const int32_t* uoff;        // [F + 1]
+  const uint16_t* umap;       // per feature: Eytzinger position -> sorted index (even-aligned)
+  const int32_t* moff;        // [F + 1] offsets into umap (even)
   int node_off_bytes;         // byte offset of the node words inside a ranked tree blob
 };
 
@@ -441,11 +443,39 @@ __global__ void __launch_bounds__(NT) forest_kernel(const ForestArgs a) {
 // word (rank << 16 | feature): a tree level costs one node load and one u16
 // rank load instead of feature + threshold + float x loads.
 
-__device__ __forceinline__ int count_less(const float* u, int n, float x) {
-  int pos = 0;
-  for (int step = n ? (1 << (31 - __clz(n))) : 0; step > 0; step >>= 1)
-    if (pos + step <= n && u[pos + step - 1] < x) pos += step;
-  return pos;
+// Count of thresholds < x by an Eytzinger (breadth-first) search: level k of
+// the implicit tree is 2^k consecutive floats, so the first five levels are
+// bank-conflict-free across a warp (a power-of-two binary search over a
+// sorted array sends every lane of a step to the same bank).  The final
+// position is the lower_bound element, mapped back to its sorted index.
+__device__ __forceinline__ int count_less_eyt(const float* ue, const uint16_t* map, int n, float x) {
+  int k = 1;
+  while (k <= n) k = 2 * k + (ue[k - 1] < x ? 1 : 0);
+  k >>= __ffs(~k);
+  return k ? (int)map[k - 1] : n;
+}
+
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gmem_src) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+template <int CT>
+__device__ __forceinline__ void load_payload(const float* p, float (&v)[CT]) {
+  if constexpr (CT == 1) {
+    v[0] = p[0];
+  } else if constexpr (CT == 2) {
+    const float2 q = *reinterpret_cast<const float2*>(p);
+    v[0] = q.x; v[1] = q.y;
+  } else {
+#pragma unroll
+    for (int c = 0; c < CT; c += 4) {
+      const float4 q = *reinterpret_cast<const float4*>(p + c);
+      v[c] = q.x; v[c + 1] = q.y; v[c + 2] = q.z; v[c + 3] = q.w;
+    }
+  }
 }
 
 template <int CT, int NTT, int RPT, int TI, bool PW>
@@ -482,9 +512,23 @@ __global__ void __launch_bounds__(NTT) forest_ranked_kernel(const ForestArgs a) 
     }
   }
 
-  // ---- rank the row tile, eight features per global read burst -----------
-  const int half = a.stage_cap;  // floats per staging buffer (two buffers)
-  float* stage0 = reinterpret_cast<float*>(chunk);
+  // ---- rank the row tile ---------------------------------------------------
+  // Feature f's Eytzinger thresholds + index map are staged with cp.async into
+  // buffer f&1 while the CTA searches feature f-1's buffer (double buffering:
+  // one barrier per feature).  Row values are read eight features at a time.
+  const int cap = a.stage_cap;  // thresholds per staging buffer
+  auto stage_f = [&](int b) { return reinterpret_cast<float*>(chunk) + (size_t)b * (cap + cap / 2); };
+  auto issue_stage = [&](int f) {
+    float* fb = stage_f(f & 1);
+    uint32_t* mb = reinterpret_cast<uint32_t*>(fb + cap);
+    const int u0 = __ldg(a.uoff + f), nf = __ldg(a.uoff + f + 1) - u0;
+    const int m0 = __ldg(a.moff + f);
+    for (int i = tid; i < nf; i += NTT) cp_async4(fb + i, a.uthr + u0 + i);
+    const uint32_t* msrc = reinterpret_cast<const uint32_t*>(a.umap + m0);
+    for (int i = tid; i < (nf + 1) / 2; i += NTT) cp_async4(mb + i, msrc + i);
+    cp_async_commit();
+  };
+  issue_stage(0);
   for (int g0 = 0; g0 < F; g0 += 8) {
     float xv[RPT][8];
 #pragma unroll
@@ -504,14 +548,16 @@ __global__ void __launch_bounds__(NTT) forest_ranked_kernel(const ForestArgs a) 
     for (int j = 0; j < 8; ++j) {
       const int f = g0 + j;
       if (f < F) {  // uniform across the CTA
-        float* stage = stage0 + (f & 1) * half;
-        const int u0 = __ldg(a.uoff + f), nf = __ldg(a.uoff + f + 1) - u0;
-        for (int i = tid; i < nf; i += NTT) stage[i] = __ldg(a.uthr + u0 + i);
-        __syncthreads();  // stage f ready; every reader of stage f-2's buffer is done
+        cp_async_wait_all();
+        __syncthreads();  // stage f landed for everyone; buffer (f+1)&1 is free
+        if (f + 1 < F) issue_stage(f + 1);
+        const float* fb = stage_f(f & 1);
+        const uint16_t* mb = reinterpret_cast<const uint16_t*>(fb + cap);
+        const int nf = __ldg(a.uoff + f + 1) - __ldg(a.uoff + f);
         uint8_t* xrow = reinterpret_cast<uint8_t*>(xr) + (size_t)f * ROWS * 2;
 #pragma unroll
         for (int k = 0; k < RPT; ++k)
-          *reinterpret_cast<uint16_t*>(xrow + pb[k]) = (uint16_t)count_less(stage, nf, xv[k][j]);
+          *reinterpret_cast<uint16_t*>(xrow + pb[k]) = (uint16_t)count_less_eyt(fb, mb, nf, xv[k][j]);
       }
     }
   }
@@ -579,10 +625,8 @@ __global__ void __launch_bounds__(NTT) forest_ranked_kernel(const ForestArgs a) 
 #pragma unroll
             for (int k = 0; k < RPT; ++k) {
               const int slot = (int)((o[q][k] - base[q]) >> 2) - a.ni;
-              const float* pay = reinterpret_cast<const float*>(tb) + slot * CT;
               float v[CT];
-#pragma unroll
-              for (int c = 0; c < CT; ++c) v[c] = pay[c];
+              load_payload<CT>(reinterpret_cast<const float*>(tb) + slot * CT, v);
               if (a.leaf_out && rowk[k] < a.n_rows)
                 a.leaf_out[rowk[k] * T + t] = __ldg(a.slot_leaf + (int64_t)t * a.ns + slot);
               accumulate<(J + q) & 7, CT>(acc[k], v, a.C, code);
@@ -641,11 +685,13 @@ struct cmlb_forest {
   double* classes = nullptr;
   float* uthr = nullptr;
   int32_t* uoff = nullptr;
+  uint16_t* umap = nullptr;
+  int32_t* moff = nullptr;
   int ntt = 256, stage_cap = 0, node_off_bytes = 0, rcfg = 0;
   ~cmlb_forest() {
     cudaFree(blob); cudaFree(slot_leaf); cudaFree(gnode); cudaFree(node_off);
     cudaFree(gpay); cudaFree(leaf_off); cudaFree(sched); cudaFree(classes);
-    cudaFree(uthr); cudaFree(uoff);
+    cudaFree(uthr); cudaFree(uoff); cudaFree(umap); cudaFree(moff);
   }
 };
 
@@ -949,15 +995,16 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
       if (ranked_for(*f) == nullptr) continue;        // not instantiated for this shape
       if ((size_t)f->F * rows * 2 > 65536) continue;  // feature byte offset must fit 16 bits
       const size_t xr = ((size_t)f->F * rows * 2 + 15) / 16 * 16;
-      if (xr + 2 * 4 * max_nf + 64 > SMEM_LIMIT) continue;
+      const size_t cap = (max_nf + 7) / 8 * 8;
+      const size_t stage_bytes = 2 * (cap * 4 + cap * 2);
+      if (xr + stage_bytes > SMEM_LIMIT) continue;
       const size_t avail = SMEM_LIMIT - xr;
       const int chunk = (int)(avail / r_tree_bytes) / 8 * 8;
       if (chunk < 8) continue;
       r_ntt = ntt; r_rpt = rpt;
       r_chunk = std::min(chunk, (f->T + 7) / 8 * 8);
-      const size_t chunk_bytes = std::max((size_t)r_chunk * r_tree_bytes, 2 * 4 * max_nf + 32);
-      r_stage = (int)((max_nf + 3) / 4 * 4);
-      r_smem = xr + std::max(chunk_bytes, (size_t)2 * 4 * r_stage);
+      r_stage = (int)cap;
+      r_smem = xr + std::max((size_t)r_chunk * r_tree_bytes, stage_bytes);
       if (r_smem > SMEM_LIMIT) continue;
       found = true;
     }
@@ -982,16 +1029,42 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
     for (int t = 0; t < f->T; ++t)
       fill_ranked(d, t, D, f->CT, f->node_off_bytes, f->ntt * f->rpt, U, blob.data() + (size_t)t * f->tree_bytes,
                   slot_leaf.data() + (size_t)t * f->ns);
+    // per feature: Eytzinger order of the sorted unique thresholds + the map
+    // from Eytzinger position back to sorted index
     std::vector<float> uthr;
-    std::vector<int32_t> uoff(f->F + 1, 0);
+    std::vector<uint16_t> umap;
+    std::vector<int32_t> uoff(f->F + 1, 0), moff(f->F + 1, 0);
     for (int k = 0; k < f->F; ++k) {
-      uthr.insert(uthr.end(), U[k].begin(), U[k].end());
+      const auto& u = U[k];
+      const size_t n = u.size();
+      std::vector<float> e(n);
+      std::vector<uint16_t> m(n);
+      size_t next = 0;
+      // in-order walk of the implicit tree assigns sorted elements to BFS slots
+      std::vector<std::pair<size_t, bool>> st;
+      size_t node = 1;
+      while (node <= n || !st.empty()) {
+        if (node <= n) { st.push_back({node, false}); node = 2 * node; continue; }
+        node = st.back().first;
+        st.pop_back();
+        e[node - 1] = u[next];
+        m[node - 1] = (uint16_t)next;
+        ++next;
+        node = 2 * node + 1;
+      }
+      uthr.insert(uthr.end(), e.begin(), e.end());
       uoff[k + 1] = (int32_t)uthr.size();
+      moff[k] = (int32_t)umap.size();
+      umap.insert(umap.end(), m.begin(), m.end());
+      if (umap.size() % 2) umap.push_back(0);
     }
+    moff[f->F] = (int32_t)umap.size();
     if (int st = upload(&f->blob, blob.data(), blob.size())) return st;
     if (int st = upload(&f->slot_leaf, slot_leaf.data(), slot_leaf.size())) return st;
     if (int st = upload(&f->uthr, uthr.data(), uthr.size())) return st;
     if (int st = upload(&f->uoff, uoff.data(), uoff.size())) return st;
+    if (int st = upload(&f->umap, umap.data(), umap.size())) return st;
+    if (int st = upload(&f->moff, moff.data(), moff.size())) return st;
   }
 
   if (f->variant == CMLB_FOREST_RANKED) {
@@ -1036,7 +1109,7 @@ static int run_forest(const cmlb_forest* f, const float* x, int64_t n_rows, int6
   a.agg = f->agg; a.tail = f->tail; a.out_dt = f->out_dt; a.dense_sel = f->dense_sel;
   a.n_classes = f->n_classes; a.lr = f->lr; a.base = f->base; a.classes = f->classes;
   a.pay_off = f->pay_off; a.feat_off = f->feat_off;
-  a.uthr = f->uthr; a.uoff = f->uoff; a.stage_cap = f->stage_cap; a.node_off_bytes = f->node_off_bytes;
+  a.uthr = f->uthr; a.uoff = f->uoff; a.umap = f->umap; a.moff = f->moff; a.stage_cap = f->stage_cap; a.node_off_bytes = f->node_off_bytes;
   KernelFn k = kernel_for(*f);
   const int threads = f->variant == CMLB_FOREST_RANKED ? f->ntt : NT;
   const int64_t rows = (int64_t)threads * f->rpt;
