@@ -303,9 +303,9 @@ def main(argv=None):
         achieved_gbs = rows_per_s_kernel * BYTES_ROW / 1e9
         traffic = None
         tpath = os.path.join(ROOT, "profiles", "traffic_rf500.json")
-        if os.path.exists(tpath):
+        if os.path.exists(tpath):  # ncu dram__bytes_read+write per row, scaled to this launch
             with open(tpath) as fh:
-                traffic = json.load(fh).get("dram_bytes_per_launch")
+                traffic = json.load(fh)["dram_bytes_per_row"] * n
         line = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,

@@ -141,6 +141,7 @@ struct ForestArgs {
   const uint16_t* umap;       // per feature: Eytzinger position -> sorted index (even-aligned)
   const int32_t* moff;        // [F + 1] offsets into umap (even)
   int node_off_bytes;         // byte offset of the node words inside a ranked tree blob
+  int stage_off;              // byte offset of the ranking staging area inside the chunk area
 };
 
 constexpr int NT = 256;  // threads per CTA for every forest kernel
@@ -462,6 +463,39 @@ __device__ __forceinline__ void cp_async4(void* smem_dst, const void* gmem_src) 
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
+// TMA bulk copies (global -> shared) completing on an mbarrier.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile("{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n"
+               ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+template <int CT>
+__device__ __forceinline__ void load_payload_shared(uint32_t addr, float (&v)[CT]) {
+  if constexpr (CT == 1) {
+    asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(v[0]) : "r"(addr));
+  } else if constexpr (CT == 2) {
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];\n" : "=f"(v[0]), "=f"(v[1]) : "r"(addr));
+  } else {
+#pragma unroll
+    for (int c = 0; c < CT; c += 4)
+      asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                   : "=f"(v[c]), "=f"(v[c + 1]), "=f"(v[c + 2]), "=f"(v[c + 3]) : "r"(addr + c * 4));
+  }
+}
+
 template <int CT>
 __device__ __forceinline__ void load_payload(const float* p, float (&v)[CT]) {
   if constexpr (CT == 1) {
@@ -479,7 +513,7 @@ __device__ __forceinline__ void load_payload(const float* p, float (&v)[CT]) {
 }
 
 template <int CT, int NTT, int RPT, int TI, bool PW>
-__global__ void __launch_bounds__(NTT) forest_ranked_kernel(const ForestArgs a) {
+__global__ void __launch_bounds__(NTT, 1) forest_ranked_kernel(const ForestArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int ROWS = NTT * RPT;
   static_assert(ROWS % 64 == 0, "rank tile interleave needs 64-row groups");
@@ -490,6 +524,30 @@ __global__ void __launch_bounds__(NTT) forest_ranked_kernel(const ForestArgs a) 
   uint16_t* xr = reinterpret_cast<uint16_t*>(smem);
   const uint32_t chunk_off = (uint32_t)(((size_t)F * ROWS * 2 + 15) & ~(size_t)15);
   uint8_t* chunk = smem + chunk_off;
+  // Two tree buffers of chunk_trees trees each, filled by TMA bulk copies one
+  // chunk ahead of the walk.  The ranking staging area lives in buffer 1 when
+  // it fits there (a.stage_off != 0), so chunk 0 streams in during ranking.
+  __shared__ __align__(8) uint64_t tree_bar[2];
+  const uint32_t buf_bytes = (uint32_t)a.chunk_trees * a.tree_bytes;
+  const int T = a.T;
+  const int nchunks = (T + a.chunk_trees - 1) / a.chunk_trees;
+  auto issue_chunk = [&](int ci) {  // thread 0 only
+    const int c0 = ci * a.chunk_trees;
+    const uint32_t bytes = (uint32_t)min(a.chunk_trees, T - c0) * a.tree_bytes;
+    uint8_t* dst = chunk + (ci & 1) * buf_bytes;
+    const uint8_t* src = a.blob + (size_t)c0 * a.tree_bytes;
+    fence_proxy_async();
+    mbar_expect_tx(&tree_bar[ci & 1], bytes);
+    for (uint32_t off = 0; off < bytes; off += 32768u)
+      bulk_g2s(dst + off, src + off, min(32768u, bytes - off), &tree_bar[ci & 1]);
+  };
+  if (tid == 0) {
+    mbar_init(&tree_bar[0], 1);
+    mbar_init(&tree_bar[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (tid == 0 && a.stage_off) issue_chunk(0);
 
   // Rank tile layout: u16 rank of (feature f, row r) at byte f*ROWS*2 + pb(r)
   // with pb(r) = 2*((r/64)*64 + (r%32)*2 + (r/32)%2): rows r and r+32 share a
@@ -517,7 +575,7 @@ __global__ void __launch_bounds__(NTT) forest_ranked_kernel(const ForestArgs a) 
   // buffer f&1 while the CTA searches feature f-1's buffer (double buffering:
   // one barrier per feature).  Row values are read eight features at a time.
   const int cap = a.stage_cap;  // thresholds per staging buffer
-  auto stage_f = [&](int b) { return reinterpret_cast<float*>(chunk) + (size_t)b * (cap + cap / 2); };
+  auto stage_f = [&](int b) { return reinterpret_cast<float*>(chunk + a.stage_off) + (size_t)b * (cap + cap / 2); };
   auto issue_stage = [&](int f) {
     float* fb = stage_f(f & 1);
     uint32_t* mb = reinterpret_cast<uint32_t*>(fb + cap);
@@ -566,88 +624,104 @@ __global__ void __launch_bounds__(NTT) forest_ranked_kernel(const ForestArgs a) 
 #pragma unroll
   for (int k = 0; k < RPT; ++k) acc[k].init();
 
-  const int T = a.T;
   const int D = a.depth;
   const uint8_t* xrb = reinterpret_cast<const uint8_t*>(xr);
-  for (int c0 = 0; c0 < T; c0 += a.chunk_trees) {
-    const int nt = min(a.chunk_trees, T - c0);
-    __syncthreads();  // ranks complete / previous chunk consumed
-    {
-      const int4* src = reinterpret_cast<const int4*>(a.blob + (size_t)c0 * a.tree_bytes);
-      int4* dst = reinterpret_cast<int4*>(chunk);
-      const int n16 = nt * a.tree_bytes / 16;
-      for (int i = tid; i < n16; i += NTT) dst[i] = __ldg(src + i);
+  const uint32_t smem_base = smem_u32(smem);
+
+  // Walk TI trees starting at chunk-local index tl0 for every row of this
+  // thread, then fold their leaf payloads into the row accumulators.  J is the
+  // pairwise-sum lane of tree tl0 (a compile-time constant when PW).
+  auto walk_group = [&](auto jconst, auto leafconst, uint32_t buf_off, int c0, int tl0, int nt) {
+    constexpr int J = decltype(jconst)::value;
+    constexpr bool LEAF = decltype(leafconst)::value;
+    uint32_t base[TI], cst[TI];
+    bool has[TI];
+#pragma unroll
+    for (int q = 0; q < TI; ++q) {
+      has[q] = tl0 + q < nt;
+      const int tl = has[q] ? tl0 + q : tl0;
+      base[q] = buf_off + (uint32_t)tl * a.tree_bytes + a.node_off_bytes;
+      cst[q] = 4u - base[q];
     }
-    __syncthreads();
-    for (int tg = 0; tg < nt; tg += 8) {
-      // TI trees per step: TI * RPT independent walks per thread.  Nodes are
-      // addressed by byte offset o inside dynamic shared memory; the children
-      // of the node at o are at 2*o + (4 - base) and 4 bytes further.
-      auto group_step = [&](auto jconst) {
-        constexpr int J = decltype(jconst)::value;
-        const int tl0 = tg + J;
-        if (tl0 >= nt) return;
-        uint32_t base[TI], cst[TI];
-        bool has[TI];
+    // Nodes are addressed by byte offset o inside dynamic shared memory; the
+    // children of the node at o are at 2*o + (4 - base) and 4 bytes further.
+    uint32_t o[TI][RPT];
 #pragma unroll
-        for (int q = 0; q < TI; ++q) {
-          has[q] = tl0 + q < nt;
-          const int tl = has[q] ? tl0 + q : tl0;
-          base[q] = chunk_off + (uint32_t)tl * a.tree_bytes + a.node_off_bytes;
-          cst[q] = 4u - base[q];
+    for (int q = 0; q < TI; ++q)
+#pragma unroll
+      for (int k = 0; k < RPT; ++k) o[q][k] = base[q];
+    auto level = [&]() {
+#pragma unroll
+      for (int q = 0; q < TI; ++q) {
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) {
+          const uint32_t w = *reinterpret_cast<const uint32_t*>(smem + o[q][k]);
+          const uint32_t rk = *reinterpret_cast<const uint16_t*>(xrb + ((w & 0xFFFFu) | pb[k]));
+          uint32_t nx = 2u * o[q][k] + cst[q];
+          if (rk > (w >> 16)) nx += 4u;
+          o[q][k] = nx;
         }
-        uint32_t o[TI][RPT];
-#pragma unroll
-        for (int q = 0; q < TI; ++q)
-#pragma unroll
-          for (int k = 0; k < RPT; ++k) o[q][k] = base[q];
-        for (int lvl = 0; lvl < D; ++lvl) {
-#pragma unroll
-          for (int q = 0; q < TI; ++q) {
-#pragma unroll
-            for (int k = 0; k < RPT; ++k) {
-              const uint32_t w = *reinterpret_cast<const uint32_t*>(smem + o[q][k]);
-              const uint32_t rk = *reinterpret_cast<const uint16_t*>(xrb + ((w & 0xFFFFu) | pb[k]));
-              uint32_t nx = 2u * o[q][k] + cst[q];
-              if (rk > (w >> 16)) nx += 4u;
-              o[q][k] = nx;
-            }
-          }
-        }
-        const int t0 = c0 + tl0;
-        auto finish_tree = [&](auto qconst) {
-          constexpr int q = decltype(qconst)::value;
-          if constexpr (q < TI) {
-            if (!has[q]) return;
-            const int t = t0 + q;
-            const uint32_t code = PW ? __ldg(a.sched + t) : 0u;
-            const uint8_t* tb = smem + base[q] - a.node_off_bytes;
-#pragma unroll
-            for (int k = 0; k < RPT; ++k) {
-              const int slot = (int)((o[q][k] - base[q]) >> 2) - a.ni;
-              float v[CT];
-              load_payload<CT>(reinterpret_cast<const float*>(tb) + slot * CT, v);
-              if (a.leaf_out && rowk[k] < a.n_rows)
-                a.leaf_out[rowk[k] * T + t] = __ldg(a.slot_leaf + (int64_t)t * a.ns + slot);
-              accumulate<(J + q) & 7, CT>(acc[k], v, a.C, code);
-            }
-          }
-        };
-        finish_tree(std::integral_constant<int, 0>{});
-        finish_tree(std::integral_constant<int, 1>{});
-        finish_tree(std::integral_constant<int, 2>{});
-        finish_tree(std::integral_constant<int, 3>{});
-      };
-      if constexpr (TI == 2) {
-        group_step(std::integral_constant<int, 0>{});
-        group_step(std::integral_constant<int, 2>{});
-        group_step(std::integral_constant<int, 4>{});
-        group_step(std::integral_constant<int, 6>{});
-      } else {
-        group_step(std::integral_constant<int, 0>{});
-        group_step(std::integral_constant<int, 4>{});
       }
+    };
+    int lvl = 0;
+    for (; lvl + 2 <= D; lvl += 2) { level(); level(); }
+    if (lvl < D) level();
+    const int t0 = c0 + tl0;
+    auto finish_tree = [&](auto qconst) {
+      constexpr int q = decltype(qconst)::value;
+      if constexpr (q < TI) {
+        if (!has[q]) return;
+        const int t = t0 + q;
+        const uint32_t code = PW ? __ldg(a.sched + t) : 0u;
+        const uint32_t tb = smem_base + base[q] - a.node_off_bytes;  // 16-aligned blob start
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) {
+          const int slot = (int)((o[q][k] - base[q]) >> 2) - a.ni;
+          float v[CT];
+          load_payload_shared<CT>(tb + (uint32_t)slot * (CT * 4), v);
+          if constexpr (LEAF) {
+            if (rowk[k] < a.n_rows) a.leaf_out[rowk[k] * T + t] = __ldg(a.slot_leaf + (int64_t)t * a.ns + slot);
+          }
+          accumulate<(J + q) & 7, CT>(acc[k], v, a.C, code);
+        }
+      }
+    };
+    finish_tree(std::integral_constant<int, 0>{});
+    finish_tree(std::integral_constant<int, 1>{});
+    finish_tree(std::integral_constant<int, 2>{});
+    finish_tree(std::integral_constant<int, 3>{});
+  };
+
+  auto walk_chunk = [&](auto leafconst, uint32_t buf_off, int c0, int nt) {
+    if constexpr (PW) {
+      // pairwise replay: tree t goes to lane t % 8, so unroll by 8
+      for (int tg = 0; tg < nt; tg += 8) {
+        if constexpr (TI == 2) {
+          walk_group(std::integral_constant<int, 0>{}, leafconst, buf_off, c0, tg + 0, nt);
+          if (tg + 2 < nt) walk_group(std::integral_constant<int, 2>{}, leafconst, buf_off, c0, tg + 2, nt);
+          if (tg + 4 < nt) walk_group(std::integral_constant<int, 4>{}, leafconst, buf_off, c0, tg + 4, nt);
+          if (tg + 6 < nt) walk_group(std::integral_constant<int, 6>{}, leafconst, buf_off, c0, tg + 6, nt);
+        } else {
+          walk_group(std::integral_constant<int, 0>{}, leafconst, buf_off, c0, tg + 0, nt);
+          if (tg + 4 < nt) walk_group(std::integral_constant<int, 4>{}, leafconst, buf_off, c0, tg + 4, nt);
+        }
+      }
+    } else {
+      for (int tl = 0; tl < nt; tl += TI) walk_group(std::integral_constant<int, 0>{}, leafconst, buf_off, c0, tl, nt);
     }
+  };
+
+  __syncthreads();  // ranks complete; staging buffers no longer read
+  if (tid == 0 && !a.stage_off) issue_chunk(0);
+  for (int ci = 0; ci < nchunks; ++ci) {
+    const int c0 = ci * a.chunk_trees;
+    const int nt = min(a.chunk_trees, T - c0);
+    if (tid == 0 && ci + 1 < nchunks) issue_chunk(ci + 1);  // buffer freed by last iteration's barrier
+    mbar_wait(&tree_bar[ci & 1], (uint32_t)(ci >> 1) & 1u);
+    const uint32_t buf_off = chunk_off + (uint32_t)(ci & 1) * buf_bytes;
+    if (a.leaf_out) walk_chunk(std::true_type{}, buf_off, c0, nt);
+    else walk_chunk(std::false_type{}, buf_off, c0, nt);
+    __syncthreads();  // every thread done with this buffer before it is refilled
   }
 
   float none[CT];
@@ -687,7 +761,7 @@ struct cmlb_forest {
   int32_t* uoff = nullptr;
   uint16_t* umap = nullptr;
   int32_t* moff = nullptr;
-  int ntt = 256, stage_cap = 0, node_off_bytes = 0, rcfg = 0;
+  int ntt = 256, stage_cap = 0, node_off_bytes = 0, rcfg = 0, stage_off = 0;
   ~cmlb_forest() {
     cudaFree(blob); cudaFree(slot_leaf); cudaFree(gnode); cudaFree(node_off);
     cudaFree(gpay); cudaFree(leaf_off); cudaFree(sched); cudaFree(classes);
@@ -698,7 +772,7 @@ struct cmlb_forest {
 namespace cmlb {
 
 constexpr int PERFECT_MAX_DEPTH = 11;
-constexpr size_t SMEM_LIMIT = 227 * 1024;
+constexpr size_t SMEM_LIMIT = 227 * 1024 - 256;  // leave room for static shared (mbarriers)
 constexpr size_t XS_BUDGET = 120 * 1024;
 
 static int class_width(int C) {
@@ -967,7 +1041,7 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
   std::vector<std::vector<float>> U;
   const int saved_rpt = f->rpt;
   bool ranked_ok = D >= 1 && D <= PERFECT_MAX_DEPTH && f->CT <= 8 && f->agg != CMLB_AGG_NONE;
-  int r_ntt = 0, r_rpt = 0, r_chunk = 0, r_tree_bytes = 0, r_node_off = 0, r_stage = 0;
+  int r_ntt = 0, r_rpt = 0, r_chunk = 0, r_tree_bytes = 0, r_node_off = 0, r_stage = 0, r_stage_off = 0;
   size_t r_smem = 0;
   if (ranked_ok) {
     U.assign(f->F, {});
@@ -983,7 +1057,7 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
     r_tree_bytes = (int)(((size_t)r_node_off + (size_t)ni_r * 4 + 15) / 16 * 16);
     ranked_ok = max_nf <= 65534;
     // preference order (measured on B200); CMLB_RANKED_CFG forces one
-    std::vector<int> order = {2, 0, 4, 5, 6};
+    std::vector<int> order = {1, 3, 0, 2, 4, 5, 6};
     if (const char* env = getenv("CMLB_RANKED_CFG")) order = {atoi(env)};
     bool found = false;
     for (size_t oi = 0; oi < order.size() && ranked_ok && !found; ++oi) {
@@ -999,12 +1073,20 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
       const size_t stage_bytes = 2 * (cap * 4 + cap * 2);
       if (xr + stage_bytes > SMEM_LIMIT) continue;
       const size_t avail = SMEM_LIMIT - xr;
-      const int chunk = (int)(avail / r_tree_bytes) / 8 * 8;
+      // two tree buffers (double-buffered TMA), trees per buffer a multiple of 8
+      int chunk = (int)(avail / (2 * (size_t)r_tree_bytes)) / 8 * 8;
       if (chunk < 8) continue;
+      chunk = std::min(chunk, (f->T + 7) / 8 * 8);
+      const size_t buf = (size_t)chunk * r_tree_bytes;
+      if (stage_bytes > 2 * buf) {
+        // staging does not fit the chunk area of this shape
+        if (xr + stage_bytes > SMEM_LIMIT) continue;
+      }
       r_ntt = ntt; r_rpt = rpt;
-      r_chunk = std::min(chunk, (f->T + 7) / 8 * 8);
+      r_chunk = chunk;
       r_stage = (int)cap;
-      r_smem = xr + std::max((size_t)r_chunk * r_tree_bytes, stage_bytes);
+      r_stage_off = stage_bytes <= buf ? (int)buf : 0;
+      r_smem = xr + std::max(2 * buf, stage_bytes);
       if (r_smem > SMEM_LIMIT) continue;
       found = true;
     }
@@ -1022,7 +1104,7 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
 
   if (f->variant == CMLB_FOREST_RANKED) {
     f->ntt = r_ntt; f->rpt = r_rpt; f->chunk_trees = r_chunk; f->tree_bytes = r_tree_bytes;
-    f->node_off_bytes = r_node_off; f->stage_cap = r_stage; f->smem = r_smem;
+    f->node_off_bytes = r_node_off; f->stage_cap = r_stage; f->smem = r_smem; f->stage_off = r_stage_off;
     f->ni = (1 << D) - 1; f->ns = 1 << D;
     std::vector<uint8_t> blob((size_t)f->T * f->tree_bytes, 0);
     std::vector<int32_t> slot_leaf((size_t)f->T * f->ns, 0);
@@ -1109,7 +1191,7 @@ static int run_forest(const cmlb_forest* f, const float* x, int64_t n_rows, int6
   a.agg = f->agg; a.tail = f->tail; a.out_dt = f->out_dt; a.dense_sel = f->dense_sel;
   a.n_classes = f->n_classes; a.lr = f->lr; a.base = f->base; a.classes = f->classes;
   a.pay_off = f->pay_off; a.feat_off = f->feat_off;
-  a.uthr = f->uthr; a.uoff = f->uoff; a.umap = f->umap; a.moff = f->moff; a.stage_cap = f->stage_cap; a.node_off_bytes = f->node_off_bytes;
+  a.uthr = f->uthr; a.uoff = f->uoff; a.umap = f->umap; a.moff = f->moff; a.stage_cap = f->stage_cap; a.node_off_bytes = f->node_off_bytes; a.stage_off = f->stage_off;
   KernelFn k = kernel_for(*f);
   const int threads = f->variant == CMLB_FOREST_RANKED ? f->ntt : NT;
   const int64_t rows = (int64_t)threads * f->rpt;
