@@ -115,6 +115,13 @@ int cmlb_forest_run(const cmlb_forest* f, const float* x, int64_t n_rows, int64_
  * reference's pairwise order restricted to the shard (no tail), [n_rows][C]. */
 int cmlb_forest_partial(const cmlb_forest* f, const float* x, int64_t n_rows, int64_t ldx,
                         double* partial, void* stream);
+/* Tree-shard combine + tail on this (whole-forest) program's tail parameters:
+ * partials = device float64 [n_shards][n_rows][C], each the raw sum of one
+ * contiguous tree range; merges = host int32 pairs (a, b) applied in order as
+ * p[a] += p[b] (the shard nodes of numpy's pairwise recursion, leaving the sum
+ * in p[0]); then the reference tail (kernels.py:180-190, convert.py:297-311). */
+int cmlb_forest_finish(const cmlb_forest* f, const double* partials, int32_t n_shards, const int32_t* merges,
+                       int32_t n_merges, int64_t n_rows, void* y, void* stream);
 /* Introspection: chosen variant, padded depth, trees per shared-memory chunk. */
 int cmlb_forest_info(const cmlb_forest* f, int32_t* variant, int32_t* depth, int32_t* chunk_trees,
                      int32_t* rows_per_cta);

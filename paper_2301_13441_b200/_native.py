@@ -66,6 +66,7 @@ SIGNATURES = {
     "cmlb_forest_create": (C.c_int, [P(ForestDesc), C.c_int, P(c_vp)]),
     "cmlb_forest_run": (C.c_int, [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp]),
     "cmlb_forest_partial": (C.c_int, [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp]),
+    "cmlb_forest_finish": (C.c_int, [c_vp, c_vp, c_i32, P(c_i32), c_i32, c_i64, c_vp, c_vp]),
     "cmlb_forest_info": (C.c_int, [c_vp, P(c_i32), P(c_i32), P(c_i32), P(c_i32)]),
     "cmlb_forest_destroy": (None, [c_vp]),
     "cmlb_linear_create": (C.c_int, [P(LinearDesc), C.c_int, P(c_vp)]),

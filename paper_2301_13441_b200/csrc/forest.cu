@@ -232,29 +232,21 @@ __device__ __forceinline__ void poison_row(float* xs, int stride, int F, int r) 
   }
 }
 
-template <int CT, bool PW>
-__device__ __forceinline__ void finish_row(const ForestArgs& a, int64_t row, const RowAcc<CT, PW>& acc,
-                                           const float (&single)[CT]) {
+// Tail of the ensemble (convert.py:297-311): float64 totals -> float32 mean or
+// float32 sum*lr+base -> values / first-max class / sigmoid class.
+template <int CT>
+__device__ __forceinline__ void finish_totals(const ForestArgs& a, int64_t row, const double (&total)[CT],
+                                              const float (&single)[CT]) {
   const int C = a.C;
-  if (a.partial) {  // tree-shard partial: raw float64 sums, no tail
-    if constexpr (PW) {
-      a.partial[row] = acc.raw(0);
-    } else {
-#pragma unroll
-      for (int c = 0; c < CT; ++c)
-        if (c < C) a.partial[row * C + c] = acc.total(c);
-    }
-    return;
-  }
   float v[CT];
   if (a.agg == CMLB_AGG_NONE) {
 #pragma unroll
     for (int c = 0; c < CT; ++c) v[c] = single[c];
   } else if (a.agg == CMLB_AGG_MEAN) {
 #pragma unroll
-    for (int c = 0; c < CT; ++c) v[c] = __double2float_rn(acc.total(c) / (double)a.T);
+    for (int c = 0; c < CT; ++c) v[c] = __double2float_rn(total[c] / (double)a.T);
   } else {
-    const float s = __double2float_rn(acc.total(0));
+    const float s = __double2float_rn(total[0]);
     v[0] = __fadd_rn(__fmul_rn(s, a.lr), a.base);
 #pragma unroll
     for (int c = 1; c < CT; ++c) v[c] = 0.0f;
@@ -270,6 +262,53 @@ __device__ __forceinline__ void finish_row(const ForestArgs& a, int64_t row, con
     const float p = __double2float_rn(ref_sigmoid((double)v[0]));
     store_out(a.y, row, a.out_dt, a.classes[p > 0.5f ? 1 : 0]);
   }
+}
+
+template <int CT, bool PW>
+__device__ __forceinline__ void finish_row(const ForestArgs& a, int64_t row, const RowAcc<CT, PW>& acc,
+                                           const float (&single)[CT]) {
+  const int C = a.C;
+  if (a.partial) {  // tree-shard partial: raw float64 sums, no tail
+    if constexpr (PW) {
+      a.partial[row] = acc.raw(0);
+    } else {
+#pragma unroll
+      for (int c = 0; c < CT; ++c)
+        if (c < C) a.partial[row * C + c] = acc.total(c);
+    }
+    return;
+  }
+  double total[CT];
+#pragma unroll
+  for (int c = 0; c < CT; ++c) total[c] = acc.total(c);
+  finish_totals<CT>(a, row, total, single);
+}
+
+// Tree-shard combine + tail.  partials: [n_shards][n_rows][C] raw float64 sums
+// of contiguous tree ranges; merges (a, b) are applied in order as
+// p[a] += p[b] (the shard-level nodes of numpy's pairwise recursion, see
+// paper_2301_13441_b200/shard.py), leaving the whole-forest sum in p[0].
+constexpr int MAX_MERGES = 64;
+struct MergePlan { int32_t n; int32_t a[MAX_MERGES]; int32_t b[MAX_MERGES]; };
+
+template <int CT>
+__global__ void forest_finish_kernel(const ForestArgs a, const double* partials, int n_shards, MergePlan mp) {
+  const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (row >= a.n_rows) return;
+  const int C = a.C;
+  const int64_t stride = a.n_rows * C;
+  double total[CT];
+  float none[CT];
+#pragma unroll
+  for (int c = 0; c < CT; ++c) {
+    none[c] = 0.0f;
+    if (c >= C) { total[c] = 0.0; continue; }
+    double p[64];
+    for (int s = 0; s < n_shards; ++s) p[s] = partials[s * stride + row * C + c];
+    for (int m = 0; m < mp.n; ++m) p[mp.a[m]] = p[mp.a[m]] + p[mp.b[m]];
+    total[c] = C == 1 ? 0.0 + p[0] : p[0];
+  }
+  finish_totals<CT>(a, row, total, none);
 }
 
 // One kernel body for both layouts.  Thread `tid` owns rows
@@ -1226,6 +1265,39 @@ int cmlb_forest_partial(const cmlb_forest* f, const float* x, int64_t n_rows, in
                         double* partial, void* stream) {
   if (!partial) return cmlb::fail(CMLB_E_VALIDATION, "null partial buffer");
   return cmlb::run_forest(f, x, n_rows, ldx, nullptr, nullptr, partial, stream);
+}
+
+int cmlb_forest_finish(const cmlb_forest* f, const double* partials, int32_t n_shards, const int32_t* merges,
+                       int32_t n_merges, int64_t n_rows, void* y, void* stream) {
+  using namespace cmlb;
+  if (!f) return fail(CMLB_E_VALIDATION, "null forest");
+  if (n_shards < 1 || n_shards > 64 || n_merges < 0 || n_merges > MAX_MERGES || (n_merges && !merges))
+    return fail(CMLB_E_VALIDATION, "bad shard merge plan");
+  if (n_rows < 0) return fail(CMLB_E_INPUT, "bad row count");
+  if (n_rows == 0) return CMLB_OK;
+  MergePlan mp{};
+  mp.n = n_merges;
+  for (int i = 0; i < n_merges; ++i) {
+    mp.a[i] = merges[2 * i];
+    mp.b[i] = merges[2 * i + 1];
+    if (mp.a[i] < 0 || mp.a[i] >= n_shards || mp.b[i] < 0 || mp.b[i] >= n_shards)
+      return fail(CMLB_E_VALIDATION, "merge index out of range");
+  }
+  DeviceGuard guard(f->device);
+  ForestArgs a{};
+  a.n_rows = n_rows; a.y = y; a.T = f->T; a.C = f->C; a.agg = f->agg; a.tail = f->tail; a.out_dt = f->out_dt;
+  a.lr = f->lr; a.base = f->base; a.classes = f->classes; a.n_classes = f->n_classes;
+  const unsigned grid = (unsigned)ceil_div(n_rows, 256);
+  switch (f->CT) {
+    case 1: forest_finish_kernel<1><<<grid, 256, 0, (cudaStream_t)stream>>>(a, partials, n_shards, mp); break;
+    case 2: forest_finish_kernel<2><<<grid, 256, 0, (cudaStream_t)stream>>>(a, partials, n_shards, mp); break;
+    case 4: forest_finish_kernel<4><<<grid, 256, 0, (cudaStream_t)stream>>>(a, partials, n_shards, mp); break;
+    case 8: forest_finish_kernel<8><<<grid, 256, 0, (cudaStream_t)stream>>>(a, partials, n_shards, mp); break;
+    default: return fail(CMLB_E_UNRESOLVED, "tree-sharded finish supports up to 8 outputs");
+  }
+  note_launch();
+  CMLB_CUDA(cudaGetLastError());
+  return CMLB_OK;
 }
 
 int cmlb_forest_info(const cmlb_forest* f, int32_t* variant, int32_t* depth, int32_t* chunk_trees,

@@ -219,3 +219,35 @@ def test_ranked_launch_configs(cfg, monkeypatch):
         np.testing.assert_array_equal(leaves.cpu().numpy(), want_leaves)
         assert _same(y, want), (cfg, prog.forest().info())
         prog.close()
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+def test_tree_sharded_gbr_is_bit_exact(world):
+    """Tree shards (pairwise recursion nodes) -> partials -> ordered combine +
+    tail on the GPU == the single-program result == the C oracle (config 3 shape,
+    scaled down).  The NCCL path only adds the all-gather transport."""
+    import ctypes
+    from dataclasses import replace
+    from paper_2301_13441_b200 import shard
+    from paper_2301_13441_b200.lower import ProgramSpec
+    rng = np.random.default_rng(world)
+    m = _synthetic_forest(rng, 1000, 10, 90, 1, gbdt=True)
+    x = rng.standard_normal((20_000, 90)).astype(np.float32)
+    want, _ = fast.forest_predict(fast.PackedForest(m), x)
+    spec = lower.lower_model(m).stages[0]
+    ranges, merges = shard.pairwise_tree_shards(len(spec.trees), world)
+    xd = torch.from_numpy(x).cuda()
+    parts = torch.empty((world, x.shape[0], 1), dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+    for i, (lo, hi) in enumerate(ranges):
+        prog = DeviceProgram(ProgramSpec([replace(spec, trees=spec.trees[lo:hi])], 90), 0)
+        prog.forest().partial(xd, parts[i], x.shape[0], 90, stream)
+    full = DeviceProgram(ProgramSpec([spec], 90), 0)
+    y = torch.empty((x.shape[0], 1), dtype=torch.float32, device="cuda")
+    mm = np.asarray(merges, np.int32).reshape(-1)
+    N.check(N.lib().cmlb_forest_finish(full.forest().handle, parts.data_ptr(), world,
+                                       mm.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), len(merges),
+                                       x.shape[0], y.data_ptr(), stream))
+    single = full.run(xd)
+    assert torch.equal(y, single)
+    assert _same(y.cpu().numpy().astype(np.float64), want)
