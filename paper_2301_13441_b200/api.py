@@ -70,13 +70,11 @@ _plan_specs: dict = {}  # id(plan) -> ProgramSpec
 
 
 def _evict(key_id: int) -> None:
+    # drop the cache entries only: a caller may still hold the DeviceProgram,
+    # which frees its device tables itself when it is collected
     with _cache_lock:
         for k in [k for k in _programs if k[0] == key_id]:
-            prog = _programs.pop(k)
-            try:
-                prog.close()
-            except Exception:  # pragma: no cover
-                pass
+            _programs.pop(k)
         _plan_specs.pop(key_id, None)
 
 

@@ -142,6 +142,7 @@ struct ForestArgs {
   const int32_t* moff;        // [F + 1] offsets into umap (even)
   int node_off_bytes;         // byte offset of the node words inside a ranked tree blob
   int stage_off;              // byte offset of the ranking staging area inside the chunk area
+  int stage_bufs;             // 1 or 2 staging buffers
 };
 
 constexpr int NT = 256;  // threads per CTA for every forest kernel
@@ -614,7 +615,12 @@ __global__ void __launch_bounds__(NTT, 1) forest_ranked_kernel(const ForestArgs 
   // buffer f&1 while the CTA searches feature f-1's buffer (double buffering:
   // one barrier per feature).  Row values are read eight features at a time.
   const int cap = a.stage_cap;  // thresholds per staging buffer
-  auto stage_f = [&](int b) { return reinterpret_cast<float*>(chunk + a.stage_off) + (size_t)b * (cap + cap / 2); };
+  // two staging buffers when they fit (a.stage_bufs == 2: prefetch feature f+1
+  // while searching f), else one (an extra barrier per feature)
+  const bool dbl = a.stage_bufs == 2;
+  auto stage_f = [&](int b) {
+    return reinterpret_cast<float*>(chunk + a.stage_off) + (size_t)(dbl ? b : 0) * (cap + cap / 2);
+  };
   auto issue_stage = [&](int f) {
     float* fb = stage_f(f & 1);
     uint32_t* mb = reinterpret_cast<uint32_t*>(fb + cap);
@@ -645,9 +651,13 @@ __global__ void __launch_bounds__(NTT, 1) forest_ranked_kernel(const ForestArgs 
     for (int j = 0; j < 8; ++j) {
       const int f = g0 + j;
       if (f < F) {  // uniform across the CTA
+        if (!dbl && f > 0) {
+          __syncthreads();  // everyone done searching f-1 in the single buffer
+          issue_stage(f);
+        }
         cp_async_wait_all();
         __syncthreads();  // stage f landed for everyone; buffer (f+1)&1 is free
-        if (f + 1 < F) issue_stage(f + 1);
+        if (dbl && f + 1 < F) issue_stage(f + 1);
         const float* fb = stage_f(f & 1);
         const uint16_t* mb = reinterpret_cast<const uint16_t*>(fb + cap);
         const int nf = __ldg(a.uoff + f + 1) - __ldg(a.uoff + f);
@@ -694,10 +704,12 @@ __global__ void __launch_bounds__(NTT, 1) forest_ranked_kernel(const ForestArgs 
       for (int q = 0; q < TI; ++q) {
 #pragma unroll
         for (int k = 0; k < RPT; ++k) {
+          // w = (feature row offset in 4-byte words) << 16 | threshold rank; ranks
+          // are < 2^14, so w >> 14 is exactly the feature's byte offset
           const uint32_t w = *reinterpret_cast<const uint32_t*>(smem + o[q][k]);
-          const uint32_t rk = *reinterpret_cast<const uint16_t*>(xrb + ((w & 0xFFFFu) | pb[k]));
+          const uint32_t rk = *reinterpret_cast<const uint16_t*>(xrb + ((w >> 14) + pb[k]));
           uint32_t nx = 2u * o[q][k] + cst[q];
-          if (rk > (w >> 16)) nx += 4u;
+          if (rk > (w & 0xFFFFu)) nx += 4u;
           o[q][k] = nx;
         }
       }
@@ -800,7 +812,7 @@ struct cmlb_forest {
   int32_t* uoff = nullptr;
   uint16_t* umap = nullptr;
   int32_t* moff = nullptr;
-  int ntt = 256, stage_cap = 0, node_off_bytes = 0, rcfg = 0, stage_off = 0;
+  int ntt = 256, stage_cap = 0, node_off_bytes = 0, rcfg = 0, stage_off = 0, stage_bufs = 2;
   ~cmlb_forest() {
     cudaFree(blob); cudaFree(slot_leaf); cudaFree(gnode); cudaFree(node_off);
     cudaFree(gpay); cudaFree(leaf_off); cudaFree(sched); cudaFree(classes);
@@ -848,7 +860,7 @@ static KernelFn pick4(bool perfect, bool xs) {
 // Ranked launch configurations: (threads, rows per thread, trees per step).
 struct RankedCfg { int ntt, rpt, ti; };
 constexpr RankedCfg RANKED_CFGS[] = {
-    {512, 2, 2}, {512, 2, 4}, {1024, 1, 2}, {1024, 1, 4}, {256, 2, 2}, {256, 1, 2}, {128, 2, 2}};
+    {512, 2, 2}, {512, 2, 4}, {1024, 1, 2}, {1024, 1, 4}, {256, 2, 2}, {256, 1, 2}, {128, 2, 2}, {512, 1, 2}};
 constexpr int N_RANKED_CFGS = sizeof(RANKED_CFGS) / sizeof(RANKED_CFGS[0]);
 
 template <int CT, bool PW>
@@ -866,6 +878,7 @@ static KernelFn ranked_cfg(int cfg) {
     case 4: return forest_ranked_kernel<CT, 256, 2, 2, PW>;
     case 5: return forest_ranked_kernel<CT, 256, 1, 2, PW>;
     case 6: return forest_ranked_kernel<CT, 128, 2, 2, PW>;
+    case 7: return forest_ranked_kernel<CT, 512, 1, 2, PW>;
     default: return nullptr;
   }
 }
@@ -986,7 +999,7 @@ static void fill_ranked(const cmlb_forest_desc* d, int t, int D, int CT, int nod
   const int ni = (1 << D) - 1;
   float* pay = reinterpret_cast<float*>(blob);
   uint32_t* nodes = reinterpret_cast<uint32_t*>(blob + node_off_bytes);
-  for (int i = 0; i < ni; ++i) nodes[i] = 0xFFFFu << 16;  // always left
+  for (int i = 0; i < ni; ++i) nodes[i] = 0x3FFFu;  // feature 0, rank 16383: always left
   const int64_t nb = d->node_offset[t], lb = d->leaf_offset[t];
   std::deque<std::pair<int64_t, int32_t>> q;
   q.push_back({0, d->node_offset[t + 1] > nb ? 0 : -1});
@@ -998,7 +1011,7 @@ static void fill_ranked(const cmlb_forest_desc* d, int t, int D, int CT, int nod
       const float th = d->threshold[nb + ref];
       const auto& u = U[f];
       const uint32_t rank = (uint32_t)(std::lower_bound(u.begin(), u.end(), th) - u.begin());
-      nodes[h] = (rank << 16) | (uint32_t)(f * rows * 2);
+      nodes[h] = ((uint32_t)(f * rows / 2) << 16) | rank;
       q.push_back({2 * h + 1, d->left[nb + ref]});
       q.push_back({2 * h + 2, d->right[nb + ref]});
     } else {
@@ -1080,7 +1093,7 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
   std::vector<std::vector<float>> U;
   const int saved_rpt = f->rpt;
   bool ranked_ok = D >= 1 && D <= PERFECT_MAX_DEPTH && f->CT <= 8 && f->agg != CMLB_AGG_NONE;
-  int r_ntt = 0, r_rpt = 0, r_chunk = 0, r_tree_bytes = 0, r_node_off = 0, r_stage = 0, r_stage_off = 0;
+  int r_ntt = 0, r_rpt = 0, r_chunk = 0, r_tree_bytes = 0, r_node_off = 0, r_stage = 0, r_stage_off = 0, r_stage_bufs = 2;
   size_t r_smem = 0;
   if (ranked_ok) {
     U.assign(f->F, {});
@@ -1094,9 +1107,9 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
     const int ni_r = (1 << D) - 1, ns_r = 1 << D;
     r_node_off = ns_r * f->CT * 4;
     r_tree_bytes = (int)(((size_t)r_node_off + (size_t)ni_r * 4 + 15) / 16 * 16);
-    ranked_ok = max_nf <= 65534;
+    ranked_ok = max_nf <= 16382;  // ranks < 2^14 (see the node word layout)
     // preference order (measured on B200); CMLB_RANKED_CFG forces one
-    std::vector<int> order = {1, 3, 0, 2, 4, 5, 6};
+    std::vector<int> order = {1, 3, 0, 2, 7, 4, 5, 6};
     if (const char* env = getenv("CMLB_RANKED_CFG")) order = {atoi(env)};
     bool found = false;
     for (size_t oi = 0; oi < order.size() && ranked_ok && !found; ++oi) {
@@ -1106,27 +1119,26 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
       const int rows = ntt * rpt;
       f->rcfg = ci; f->rpt = rpt;
       if (ranked_for(*f) == nullptr) continue;        // not instantiated for this shape
-      if ((size_t)f->F * rows * 2 > 65536) continue;  // feature byte offset must fit 16 bits
-      const size_t xr = ((size_t)f->F * rows * 2 + 15) / 16 * 16;
+      if ((size_t)f->F * rows / 2 > 65535) continue;  // feature word offset must fit 16 bits
       const size_t cap = (max_nf + 7) / 8 * 8;
-      const size_t stage_bytes = 2 * (cap * 4 + cap * 2);
-      if (xr + stage_bytes > SMEM_LIMIT) continue;
+      const size_t xr = ((size_t)f->F * rows * 2 + 15) / 16 * 16;
+      if (xr + cap * 6 > SMEM_LIMIT) continue;
       const size_t avail = SMEM_LIMIT - xr;
       // two tree buffers (double-buffered TMA), trees per buffer a multiple of 8
       int chunk = (int)(avail / (2 * (size_t)r_tree_bytes)) / 8 * 8;
       if (chunk < 8) continue;
       chunk = std::min(chunk, (f->T + 7) / 8 * 8);
       const size_t buf = (size_t)chunk * r_tree_bytes;
-      if (stage_bytes > 2 * buf) {
-        // staging does not fit the chunk area of this shape
-        if (xr + stage_bytes > SMEM_LIMIT) continue;
-      }
+      // staging: double buffer if it fits next to the tree buffers, else single
+      int nbufs = xr + std::max(2 * buf, 2 * cap * 6) <= SMEM_LIMIT ? 2 : 1;
+      const size_t stage_bytes = (size_t)nbufs * cap * 6;
+      if (xr + std::max(2 * buf, stage_bytes) > SMEM_LIMIT) continue;
       r_ntt = ntt; r_rpt = rpt;
       r_chunk = chunk;
       r_stage = (int)cap;
+      r_stage_bufs = nbufs;
       r_stage_off = stage_bytes <= buf ? (int)buf : 0;
       r_smem = xr + std::max(2 * buf, stage_bytes);
-      if (r_smem > SMEM_LIMIT) continue;
       found = true;
     }
     ranked_ok = ranked_ok && found;
@@ -1143,7 +1155,7 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
 
   if (f->variant == CMLB_FOREST_RANKED) {
     f->ntt = r_ntt; f->rpt = r_rpt; f->chunk_trees = r_chunk; f->tree_bytes = r_tree_bytes;
-    f->node_off_bytes = r_node_off; f->stage_cap = r_stage; f->smem = r_smem; f->stage_off = r_stage_off;
+    f->node_off_bytes = r_node_off; f->stage_cap = r_stage; f->smem = r_smem; f->stage_off = r_stage_off; f->stage_bufs = r_stage_bufs;
     f->ni = (1 << D) - 1; f->ns = 1 << D;
     std::vector<uint8_t> blob((size_t)f->T * f->tree_bytes, 0);
     std::vector<int32_t> slot_leaf((size_t)f->T * f->ns, 0);
@@ -1230,7 +1242,7 @@ static int run_forest(const cmlb_forest* f, const float* x, int64_t n_rows, int6
   a.agg = f->agg; a.tail = f->tail; a.out_dt = f->out_dt; a.dense_sel = f->dense_sel;
   a.n_classes = f->n_classes; a.lr = f->lr; a.base = f->base; a.classes = f->classes;
   a.pay_off = f->pay_off; a.feat_off = f->feat_off;
-  a.uthr = f->uthr; a.uoff = f->uoff; a.umap = f->umap; a.moff = f->moff; a.stage_cap = f->stage_cap; a.node_off_bytes = f->node_off_bytes; a.stage_off = f->stage_off;
+  a.uthr = f->uthr; a.uoff = f->uoff; a.umap = f->umap; a.moff = f->moff; a.stage_cap = f->stage_cap; a.node_off_bytes = f->node_off_bytes; a.stage_off = f->stage_off; a.stage_bufs = f->stage_bufs;
   KernelFn k = kernel_for(*f);
   const int threads = f->variant == CMLB_FOREST_RANKED ? f->ntt : NT;
   const int64_t rows = (int64_t)threads * f->rpt;

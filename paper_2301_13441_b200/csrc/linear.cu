@@ -9,11 +9,12 @@
 // full-rate-enough FP64 (unlike B300) for this to stay near the HBM roof:
 // 1M x 784 x 10 -> 7.8 GFMA vs 3.1 GB of X.
 //
-// Layout: 128 threads, 2 rows per thread, K staged in chunks of 32 features.
+// Layout: 128 threads, 2 rows per thread, K staged in chunks of 16 features.
 // X chunk in shared memory as xs[k][row] with an odd row stride (conflict-free
 // for both the coalesced fill and the per-row reads); the weight chunk as
 // float64 ws[k][c], read as warp-wide broadcasts.
 
+#include <cstdint>
 #include <memory>
 #include <string>
 #include <vector>
@@ -59,15 +60,24 @@ __device__ __forceinline__ double pw_small(const double (&e)[CM], int n) {
   return 0.0 + res;
 }
 
+// X is streamed in K-chunks of 16 features: each thread holds its share of
+// chunk c+1 in registers (float4 loads, coalesced across the row) while the
+// CTA computes on chunk c from shared memory, so HBM latency overlaps the FP64
+// FMA chains.  The chunk is stored transposed (xs[k][row], odd stride) so the
+// per-row reads are conflict-free; W is read as broadcast double2 pairs.
 template <int CM, int LRPT, int LKC>
 __global__ void __launch_bounds__(LNT) linear_kernel(const LinearArgs a) {
   constexpr int LROWS = LNT * LRPT;
-  constexpr int LXS = LROWS + 1;  // odd stride
+  constexpr int LXS = LROWS + 1;       // odd stride
+  constexpr int CE = (CM + 1) / 2 * 2;  // classes padded to pairs
+  constexpr int NV = LROWS * LKC / 4 / LNT;  // float4 per thread per chunk
+  static_assert(LKC == 16 && NV * LNT * 4 == LROWS * LKC, "chunk shape");
   __shared__ float xs[LKC * LXS];
-  __shared__ double ws[LKC * CM];
+  __shared__ __align__(16) double ws[LKC * CE];
   const int tid = threadIdx.x;
   const int64_t tile = (int64_t)blockIdx.x * LROWS;
   const int F = a.F, C = a.C;
+  const bool vec = (a.ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
 
   double acc[LRPT][CM];
 #pragma unroll
@@ -75,31 +85,71 @@ __global__ void __launch_bounds__(LNT) linear_kernel(const LinearArgs a) {
 #pragma unroll
     for (int c = 0; c < CM; ++c) acc[k][c] = 0.0;
 
-  for (int k0 = 0; k0 < F; k0 += LKC) {
-    const int kc = min(LKC, F - k0);
-    __syncthreads();
-    for (int i = tid; i < LROWS * LKC; i += LNT) {
-      const int r = i / LKC, kk = i % LKC;
+  float4 pre[NV];
+  auto load_chunk = [&](int k0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int idx = tid + LNT * i;
+      const int r = idx >> 2, part = idx & 3;
       const int64_t row = tile + r;
-      float v = 0.0f;
-      if (kk < kc && row < a.n_rows) v = __ldg(a.x + row * a.ldx + k0 + kk);
-      xs[kk * LXS + r] = v;
+      const int k = k0 + part * 4;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (row < a.n_rows) {
+        const float* src = a.x + row * a.ldx + k;
+        if (vec && k + 4 <= F) {
+          v = __ldg(reinterpret_cast<const float4*>(src));
+        } else {
+          if (k < F) v.x = __ldg(src);
+          if (k + 1 < F) v.y = __ldg(src + 1);
+          if (k + 2 < F) v.z = __ldg(src + 2);
+          if (k + 3 < F) v.w = __ldg(src + 3);
+        }
+      }
+      pre[i] = v;
     }
-    for (int i = tid; i < LKC * CM; i += LNT) {
-      const int kk = i / CM, c = i % CM;
-      ws[i] = (kk < kc && c < C) ? (double)__ldg(a.w + (int64_t)c * F + k0 + kk) : 0.0;
+  };
+  auto store_chunk = [&](int k0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int idx = tid + LNT * i;
+      const int r = idx >> 2, part = idx & 3;
+      float* dst = xs + (part * 4) * LXS + r;
+      dst[0] = pre[i].x;
+      dst[LXS] = pre[i].y;
+      dst[2 * LXS] = pre[i].z;
+      dst[3 * LXS] = pre[i].w;
     }
+    for (int i = tid; i < LKC * CE; i += LNT) {
+      const int kk = i / CE, c = i % CE;
+      ws[i] = (k0 + kk < F && c < C) ? (double)__ldg(a.w + (int64_t)c * F + k0 + kk) : 0.0;
+    }
+  };
+
+  load_chunk(0);
+  for (int k0 = 0; k0 < F; k0 += LKC) {
+    __syncthreads();  // previous chunk consumed
+    store_chunk(k0);
     __syncthreads();
+    if (k0 + LKC < F) load_chunk(k0 + LKC);  // in flight during the FMAs below
+    const int kc = min(LKC, F - k0);
     for (int kk = 0; kk < kc; ++kk) {
       double xv[LRPT];
 #pragma unroll
       for (int k = 0; k < LRPT; ++k) xv[k] = (double)xs[kk * LXS + tid + k * LNT];
+      const double2* w2 = reinterpret_cast<const double2*>(ws + kk * CE);
 #pragma unroll
-      for (int c = 0; c < CM; ++c) {
-        const double wv = ws[kk * CM + c];
-        if (c < C && !(a.sparse && wv == 0.0)) {
+      for (int c2 = 0; c2 < CE / 2; ++c2) {
+        const double2 wv = w2[c2];
 #pragma unroll
-          for (int k = 0; k < LRPT; ++k) acc[k][c] = fma(xv[k], wv, acc[k][c]);
+        for (int h = 0; h < 2; ++h) {
+          const int c = 2 * c2 + h;
+          if (c < CM) {
+            const double wc = h ? wv.y : wv.x;
+            if (c < C && !(a.sparse && wc == 0.0)) {
+#pragma unroll
+              for (int k = 0; k < LRPT; ++k) acc[k][c] = fma(xv[k], wc, acc[k][c]);
+            }
+          }
         }
       }
     }
@@ -159,14 +209,14 @@ using LinFn = void (*)(const LinearArgs);
 // (kernel, rows per CTA) by output count
 static LinFn linear_for(int C, int* rows) {
   *rows = LNT * 2;
-  if (C <= 1) return linear_kernel<1, 2, 32>;
-  if (C <= 2) return linear_kernel<2, 2, 32>;
-  if (C <= 4) return linear_kernel<4, 2, 32>;
-  if (C <= 8) return linear_kernel<8, 2, 32>;
-  if (C <= 10) return linear_kernel<10, 2, 32>;
-  if (C <= 16) return linear_kernel<16, 2, 32>;
+  if (C <= 1) return linear_kernel<1, 2, 16>;
+  if (C <= 2) return linear_kernel<2, 2, 16>;
+  if (C <= 4) return linear_kernel<4, 2, 16>;
+  if (C <= 8) return linear_kernel<8, 2, 16>;
+  if (C <= 10) return linear_kernel<10, 2, 16>;
+  if (C <= 16) return linear_kernel<16, 2, 16>;
   *rows = LNT;
-  if (C <= 32) return linear_kernel<32, 1, 32>;
+  if (C <= 32) return linear_kernel<32, 1, 16>;
   if (C <= 64) return linear_kernel<64, 1, 16>;
   return nullptr;
 }
