@@ -216,6 +216,8 @@ def main(argv=None):
     ap.add_argument("--rows", type=int, default=10_000_000)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--variant", default="auto", choices=["auto", "ranked", "perfect", "general", "mma"],
+                    help="force a forest kernel variant (measurement; default: the measured AUTO choice)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
@@ -233,7 +235,13 @@ def main(argv=None):
     dev = torch.device("cuda", torch.cuda.current_device())
     model, mu, sigma = load_model()
     compiled = api.compile_model(model)
-    prog = compiled.program(dev.index)
+    if args.variant == "auto":
+        prog = compiled.program(dev.index)
+    else:
+        from paper_2301_13441_b200.runtime import DeviceProgram
+        prog = DeviceProgram(compiled.spec, dev.index, forest_variant={
+            "ranked": N.FOREST_RANKED, "perfect": N.FOREST_PERFECT, "general": N.FOREST_GENERAL,
+            "mma": N.FOREST_MMA}[args.variant])
     info = prog.forest().info()
     n = args.rows
 

@@ -77,7 +77,8 @@ enum cmlb_forest_variant {
   CMLB_FOREST_AUTO = 0,        /* pick by (depth, trees, features) from the measured table */
   CMLB_FOREST_PERFECT = 1,     /* perfect-padded trees staged in shared memory */
   CMLB_FOREST_GENERAL = 2,     /* arbitrary depth, canonical nodes read through L1 */
-  CMLB_FOREST_RANKED = 3       /* perfect trees, rank-quantized thresholds: one word per node */
+  CMLB_FOREST_RANKED = 3,      /* perfect trees, rank-quantized thresholds: one word per node */
+  CMLB_FOREST_MMA = 4          /* the GEMM form on tcgen05 kind::i8: bits x path matrix in TMEM */
 };
 
 typedef struct cmlb_forest_desc {

@@ -50,7 +50,7 @@ class ScalerDesc(C.Structure):
 # enum values (cmlb.h)
 AGG_NONE, AGG_MEAN, AGG_SUM = 0, 1, 2
 TAIL_VALUES, TAIL_ARGMAX, TAIL_SIGMOID = 0, 1, 2
-FOREST_AUTO, FOREST_PERFECT, FOREST_GENERAL, FOREST_RANKED = 0, 1, 2, 3
+FOREST_AUTO, FOREST_PERFECT, FOREST_GENERAL, FOREST_RANKED, FOREST_MMA = 0, 1, 2, 3, 4
 LIN_VALUES, LIN_ARGMAX, LIN_SOFTMAX_ARGMAX, LIN_SIGMOID, LIN_SIGN = 0, 1, 2, 3, 4
 (SCALER_BINARIZER, SCALER_NORM_L1, SCALER_NORM_L2, SCALER_NORM_MAX, SCALER_MINMAX,
  SCALER_SUB_DIV, SCALER_DIV) = range(7)

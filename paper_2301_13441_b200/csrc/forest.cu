@@ -143,6 +143,8 @@ struct ForestArgs {
   int node_off_bytes;         // byte offset of the node words inside a ranked tree blob
   int stage_off;              // byte offset of the ranking staging area inside the chunk area
   int stage_bufs;             // 1 or 2 staging buffers
+  // MMA variant
+  int mma_k, mma_n, mma_feat_off, mma_thr_off, mma_pay_off;
 };
 
 constexpr int NT = 256;  // threads per CTA for every forest kernel
@@ -517,9 +519,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
                ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
+// Bounded wait: a barrier that never completes traps (kernel error) instead of
+// hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile("{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n"
-               ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+  const uint32_t addr = smem_u32(bar);
+  for (uint32_t spin = 0;; ++spin) {
+    uint32_t done;
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                 : "=r"(done) : "r"(addr), "r"(parity) : "memory");
+    if (done) return;
+    if (spin > (1u << 26)) __trap();
+  }
 }
 
 template <int CT>
@@ -784,6 +794,165 @@ __global__ void __launch_bounds__(NTT, 1) forest_ranked_kernel(const ForestArgs 
 }
 
 // ---------------------------------------------------------------------------
+// MMA variant: the reference's GEMM form on 5th-generation tensor cores
+// ---------------------------------------------------------------------------
+//
+// The operator representation of a tree (convert.py:192-204) evaluated as the
+// path-matrix product it is written as, with the Hummingbird-style encoding of
+// went_right bits g (u8, A operand, 128 rows x K) times
+// C^T (s8 {-1, 0, +1}, B operand, N leaves x K), accumulated in TMEM (s32) by
+// tcgen05.mma.kind::i8.  A bias column (A = 1, B = -D[l], D[l] = right turns
+// on the path to l; padded leaves get +1) makes the selected leaf the unique
+// l with score == 0, so the epilogue (tcgen05.ld) is a zero test per column.
+// Bit-exact with the walk (same strict x > t bits); it exists to measure the
+// GEMM form the north star names against the traversal.
+constexpr int MMA_M = 128;
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  // K-major, no swizzle: ((8 rows, groups), 2 K-halves) : ((16 B, SBO), LBO); version 1 (sm_100)
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+}
+
+template <int CT, bool PW>
+__global__ void __launch_bounds__(MMA_M, 1) forest_mma_kernel(const ForestArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ __align__(8) uint64_t blob_bar[2];
+  __shared__ __align__(8) uint64_t mma_bar;
+  __shared__ uint32_t tmem_slot;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int F = a.F, T = a.T;
+  const int K = a.mma_k, N = a.mma_n;
+  const int64_t row = (int64_t)blockIdx.x * MMA_M + tid;
+  const bool valid = row < a.n_rows;
+
+  float* xs = reinterpret_cast<float*>(smem);                 // [F][128]
+  const uint32_t a_off = (uint32_t)(((size_t)F * MMA_M * 4 + 1023) & ~(size_t)1023);
+  uint8_t* A = smem + a_off;                                   // [K/16][128 rows][16 B]
+  const uint32_t buf0 = a_off + (uint32_t)K * MMA_M;
+  const uint32_t blob_bytes = (uint32_t)a.tree_bytes;
+
+  // ---- rows -> shared memory (feature-major), dense-selector poisoning ---
+  {
+    const float* src = a.x + row * a.ldx;
+    for (int f = 0; f < F; ++f) xs[f * MMA_M + tid] = valid ? __ldg(src + f) : 0.0f;
+    if (a.dense_sel && valid) poison_row(xs, MMA_M, F, tid);
+  }
+  if (tid == 0) {
+    mbar_init(&blob_bar[0], 1);
+    mbar_init(&blob_bar[1], 1);
+    mbar_init(&mma_bar, 1);
+    mbar_fence_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n"
+                 ::"r"(smem_u32(&tmem_slot)), "r"(256) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = tmem_slot;
+
+  auto issue_blob = [&](int t) {  // thread 0
+    uint8_t* dst = smem + buf0 + (uint32_t)(t & 1) * blob_bytes;
+    const uint8_t* src = a.blob + (size_t)t * blob_bytes;
+    fence_proxy_async();
+    mbar_expect_tx(&blob_bar[t & 1], blob_bytes);
+    for (uint32_t off = 0; off < blob_bytes; off += 32768u)
+      bulk_g2s(dst + off, src + off, min(32768u, blob_bytes - off), &blob_bar[t & 1]);
+  };
+  if (tid == 0) issue_blob(0);
+
+  RowAcc<CT, PW> acc;
+  acc.init();
+  // instruction descriptor: D s32, A u8, B s8, both K-major, N = mma_n, M = 128
+  const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(MMA_M >> 4) << 24);
+  const uint32_t a_base = smem_u32(smem) + a_off;
+
+  auto tree_step = [&](auto jconst, int t) {
+    constexpr int J = decltype(jconst)::value;
+    const int b = t & 1;
+    if (tid == 0 && t + 1 < T) issue_blob(t + 1);  // buffer freed by the previous iteration's barrier
+    mbar_wait(&blob_bar[b], (uint32_t)(t >> 1) & 1u);
+    const uint8_t* blob = smem + buf0 + (uint32_t)b * blob_bytes;
+    const uint16_t* feat = reinterpret_cast<const uint16_t*>(blob + a.mma_feat_off);
+    const float* thr = reinterpret_cast<const float*>(blob + a.mma_thr_off);
+    // producer: this row's went_right bits, 16 per 16-byte core-matrix row
+    for (int c = 0; c < K / 16; ++c) {
+      uint32_t wds[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int i = c * 16 + j;
+        uint32_t bit;
+        if (i < K - 1) bit = xs[feat[i] * MMA_M + tid] > thr[i] ? 1u : 0u;
+        else bit = 1u;  // bias column
+        wds[j >> 2] |= bit << (8 * (j & 3));
+      }
+      *reinterpret_cast<uint4*>(A + (size_t)c * (MMA_M * 16) + tid * 16) = make_uint4(wds[0], wds[1], wds[2], wds[3]);
+    }
+    fence_proxy_async();  // generic-proxy A writes -> visible to the tensor core
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const uint32_t b_base = smem_u32(blob);
+      for (int s = 0; s < K / 32; ++s) {
+        const uint64_t ad = umma_desc(a_base + (uint32_t)s * 2 * (MMA_M * 16), MMA_M * 16, 128);
+        const uint64_t bd = umma_desc(b_base + (uint32_t)s * 2 * (N * 16), (uint32_t)N * 16, 128);
+        asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                     " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n"
+                     ::"r"(tmem), "l"(ad), "l"(bd), "r"(idesc), "r"(s) : "memory");
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+                   ::"r"(smem_u32(&mma_bar)) : "memory");
+    }
+    mbar_wait(&mma_bar, (uint32_t)t & 1u);
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    // epilogue: the selected leaf is the column whose score is zero
+    int leaf = 0;
+    const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+    for (int c0 = 0; c0 < N; c0 += 32) {
+      uint32_t r[32];
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                   "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+                   : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                     "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                     "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                     "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                     "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                   : "r"(lane_addr + (uint32_t)c0));
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (c0 + j < N && r[j] == 0u) leaf = c0 + j;
+    }
+    float v[CT];
+    load_payload<CT>(reinterpret_cast<const float*>(blob + a.mma_pay_off) + leaf * CT, v);
+    if (a.leaf_out && valid) a.leaf_out[row * T + t] = leaf;
+    const uint32_t code = PW ? __ldg(a.sched + t) : 0u;
+    accumulate<J, CT>(acc, v, a.C, code);
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();  // TMEM, A and this blob buffer are free again
+  };
+  for (int tg = 0; tg < T; tg += 8) {
+    tree_step(std::integral_constant<int, 0>{}, tg);
+    if (tg + 1 < T) tree_step(std::integral_constant<int, 1>{}, tg + 1);
+    if (tg + 2 < T) tree_step(std::integral_constant<int, 2>{}, tg + 2);
+    if (tg + 3 < T) tree_step(std::integral_constant<int, 3>{}, tg + 3);
+    if (tg + 4 < T) tree_step(std::integral_constant<int, 4>{}, tg + 4);
+    if (tg + 5 < T) tree_step(std::integral_constant<int, 5>{}, tg + 5);
+    if (tg + 6 < T) tree_step(std::integral_constant<int, 6>{}, tg + 6);
+    if (tg + 7 < T) tree_step(std::integral_constant<int, 7>{}, tg + 7);
+  }
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(256) : "memory");
+  float none[CT];
+#pragma unroll
+  for (int c = 0; c < CT; ++c) none[c] = 0.0f;
+  if (valid) finish_row<CT, PW>(a, row, acc, none);
+}
+
+// ---------------------------------------------------------------------------
 // host program
 // ---------------------------------------------------------------------------
 
@@ -813,6 +982,7 @@ struct cmlb_forest {
   uint16_t* umap = nullptr;
   int32_t* moff = nullptr;
   int ntt = 256, stage_cap = 0, node_off_bytes = 0, rcfg = 0, stage_off = 0, stage_bufs = 2;
+  int mma_k = 0, mma_n = 0, mma_feat_off = 0, mma_thr_off = 0, mma_pay_off = 0;
   ~cmlb_forest() {
     cudaFree(blob); cudaFree(slot_leaf); cudaFree(gnode); cudaFree(node_off);
     cudaFree(gpay); cudaFree(leaf_off); cudaFree(sched); cudaFree(classes);
@@ -893,8 +1063,20 @@ static KernelFn ranked_for(const cmlb_forest& f) {
   }
 }
 
+static KernelFn mma_for(const cmlb_forest& f) {
+  const bool pw = f.C == 1 && f.agg != CMLB_AGG_NONE;
+  switch (f.CT) {
+    case 1: return pw ? forest_mma_kernel<1, true> : forest_mma_kernel<1, false>;
+    case 2: return forest_mma_kernel<2, false>;
+    case 4: return forest_mma_kernel<4, false>;
+    case 8: return forest_mma_kernel<8, false>;
+    default: return nullptr;
+  }
+}
+
 static KernelFn kernel_for(const cmlb_forest& f) {
   if (f.variant == CMLB_FOREST_RANKED) return ranked_for(f);
+  if (f.variant == CMLB_FOREST_MMA) return mma_for(f);
   const bool perfect = f.variant == CMLB_FOREST_PERFECT;
   const bool pw = f.C == 1 && f.agg != CMLB_AGG_NONE;
   switch (f.CT) {
@@ -1028,6 +1210,40 @@ static void fill_ranked(const cmlb_forest_desc* d, int t, int D, int CT, int nod
   }
 }
 
+// Path-matrix blob of one tree for the MMA variant: [B: N x K s8, K-major
+// core-matrix layout][features u16 (K-1)][thresholds f32 (K-1)][payload N x CT].
+static void fill_mma(const cmlb_forest_desc* d, int t, int K, int N, int CT, int feat_off, int thr_off,
+                     int pay_off, uint8_t* blob) {
+  const int64_t nb = d->node_offset[t], lb = d->leaf_offset[t];
+  const int I = (int)(d->node_offset[t + 1] - nb), L = (int)(d->leaf_offset[t + 1] - lb);
+  int8_t* B = reinterpret_cast<int8_t*>(blob);
+  auto bidx = [&](int n, int k) { return (size_t)(k / 16) * (N * 16) + (size_t)n * 16 + (k % 16); };
+  // leaf ranges per internal node (children have larger level-order ids)
+  std::vector<int> size(I, 0), lo(I, 0), mid(I, 0);
+  auto nleaves = [&](int32_t ref) { return ref < 0 ? 1 : size[ref]; };
+  for (int j = I - 1; j >= 0; --j) size[j] = nleaves(d->left[nb + j]) + nleaves(d->right[nb + j]);
+  std::vector<int> D(L, 0);
+  for (int j = 0; j < I; ++j) {
+    const int32_t l = d->left[nb + j], r = d->right[nb + j];
+    mid[j] = lo[j] + nleaves(l);
+    if (l >= 0) lo[l] = lo[j];
+    if (r >= 0) lo[r] = mid[j];
+    const int hi = lo[j] + size[j];
+    for (int n = lo[j]; n < mid[j]; ++n) B[bidx(n, j)] = -1;
+    for (int n = mid[j]; n < hi; ++n) { B[bidx(n, j)] = 1; D[n] += 1; }
+  }
+  for (int n = 0; n < N; ++n) B[bidx(n, K - 1)] = n < L ? (int8_t)(-D[n]) : (int8_t)1;
+  uint16_t* feat = reinterpret_cast<uint16_t*>(blob + feat_off);
+  float* thr = reinterpret_cast<float*>(blob + thr_off);
+  for (int i = 0; i < K - 1; ++i) {
+    feat[i] = i < I ? (uint16_t)d->feature[nb + i] : 0;
+    thr[i] = i < I ? d->threshold[nb + i] : std::numeric_limits<float>::infinity();
+  }
+  float* pay = reinterpret_cast<float*>(blob + pay_off);
+  for (int n = 0; n < L; ++n)
+    for (int c = 0; c < d->n_outputs; ++c) pay[n * CT + c] = d->payload[(lb + n) * d->n_outputs + c];
+}
+
 static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out) {
   if (int s = validate(d)) return s;
   std::unique_ptr<cmlb_forest> f(new cmlb_forest());
@@ -1153,6 +1369,31 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
     return fail(CMLB_E_UNRESOLVED, "ranked layout does not fit (depth/outputs/thresholds)");
   f->variant = want;
 
+  if (f->variant == CMLB_FOREST_MMA) {
+    int maxI = 0, maxL = 1;
+    for (int t = 0; t < f->T; ++t) {
+      maxI = std::max<int>(maxI, (int)(d->node_offset[t + 1] - d->node_offset[t]));
+      maxL = std::max<int>(maxL, (int)(d->leaf_offset[t + 1] - d->leaf_offset[t]));
+    }
+    const int K = (maxI + 1 + 31) / 32 * 32, N = std::max(16, (maxL + 15) / 16 * 16);
+    if (N > 256 || f->CT > 8 || f->F > 65535 || f->agg == CMLB_AGG_NONE)
+      return fail(CMLB_E_UNRESOLVED, "MMA path-matrix variant needs <= 256 leaves, <= 8 outputs, an ensemble");
+    auto al = [](size_t v) { return (int)((v + 15) / 16 * 16); };
+    f->mma_k = K; f->mma_n = N;
+    f->mma_feat_off = al((size_t)N * K);
+    f->mma_thr_off = al((size_t)f->mma_feat_off + 2 * (size_t)(K - 1));
+    f->mma_pay_off = al((size_t)f->mma_thr_off + 4 * (size_t)(K - 1));
+    f->tree_bytes = al((size_t)f->mma_pay_off + 4 * (size_t)N * f->CT);
+    const size_t xs = ((size_t)f->F * MMA_M * 4 + 1023) / 1024 * 1024;
+    f->smem = xs + (size_t)K * MMA_M + 2 * (size_t)f->tree_bytes;
+    if (f->smem > SMEM_LIMIT) return fail(CMLB_E_UNRESOLVED, "MMA variant does not fit shared memory");
+    f->rpt = 1;
+    std::vector<uint8_t> blob((size_t)f->T * f->tree_bytes, 0);
+    for (int t = 0; t < f->T; ++t)
+      fill_mma(d, t, K, N, f->CT, f->mma_feat_off, f->mma_thr_off, f->mma_pay_off, blob.data() + (size_t)t * f->tree_bytes);
+    if (int st = upload(&f->blob, blob.data(), blob.size())) return st;
+  }
+
   if (f->variant == CMLB_FOREST_RANKED) {
     f->ntt = r_ntt; f->rpt = r_rpt; f->chunk_trees = r_chunk; f->tree_bytes = r_tree_bytes;
     f->node_off_bytes = r_node_off; f->stage_cap = r_stage; f->smem = r_smem; f->stage_off = r_stage_off; f->stage_bufs = r_stage_bufs;
@@ -1200,7 +1441,7 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
     if (int st = upload(&f->moff, moff.data(), moff.size())) return st;
   }
 
-  if (f->variant == CMLB_FOREST_RANKED) {
+  if (f->variant == CMLB_FOREST_RANKED || f->variant == CMLB_FOREST_MMA) {
     // built above
   } else if (f->variant == CMLB_FOREST_PERFECT) {
     std::vector<uint8_t> blob((size_t)f->T * f->tree_bytes, 0);
@@ -1244,7 +1485,9 @@ static int run_forest(const cmlb_forest* f, const float* x, int64_t n_rows, int6
   a.pay_off = f->pay_off; a.feat_off = f->feat_off;
   a.uthr = f->uthr; a.uoff = f->uoff; a.umap = f->umap; a.moff = f->moff; a.stage_cap = f->stage_cap; a.node_off_bytes = f->node_off_bytes; a.stage_off = f->stage_off; a.stage_bufs = f->stage_bufs;
   KernelFn k = kernel_for(*f);
-  const int threads = f->variant == CMLB_FOREST_RANKED ? f->ntt : NT;
+  a.mma_k = f->mma_k; a.mma_n = f->mma_n; a.mma_feat_off = f->mma_feat_off; a.mma_thr_off = f->mma_thr_off;
+  a.mma_pay_off = f->mma_pay_off;
+  const int threads = f->variant == CMLB_FOREST_RANKED ? f->ntt : (f->variant == CMLB_FOREST_MMA ? MMA_M : NT);
   const int64_t rows = (int64_t)threads * f->rpt;
   const int64_t grid = ceil_div(n_rows, rows);
   if (grid > 0x7fffffff) return fail(CMLB_E_INPUT, "too many rows for one launch");
@@ -1318,7 +1561,8 @@ int cmlb_forest_info(const cmlb_forest* f, int32_t* variant, int32_t* depth, int
   if (variant) *variant = f->variant;
   if (depth) *depth = f->depth;
   if (chunk_trees) *chunk_trees = f->chunk_trees;
-  if (rows_per_cta) *rows_per_cta = (f->variant == CMLB_FOREST_RANKED ? f->ntt : cmlb::NT) * f->rpt;
+  if (rows_per_cta)
+    *rows_per_cta = (f->variant == CMLB_FOREST_RANKED ? f->ntt : (f->variant == CMLB_FOREST_MMA ? cmlb::MMA_M : cmlb::NT)) * f->rpt;
   return CMLB_OK;
 }
 

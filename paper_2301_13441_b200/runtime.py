@@ -78,7 +78,7 @@ class _Forest:
     def info(self) -> dict:
         v, dep, ch, rows = (N.c_i32() for _ in range(4))
         N.check(N.lib().cmlb_forest_info(self.handle, C.byref(v), C.byref(dep), C.byref(ch), C.byref(rows)))
-        return {"variant": {1: "perfect", 2: "general", 3: "ranked"}[v.value], "depth": dep.value,
+        return {"variant": {1: "perfect", 2: "general", 3: "ranked", 4: "mma"}[v.value], "depth": dep.value,
                 "chunk_trees": ch.value, "rows_per_cta": rows.value}
 
     def run(self, x, y, n, ldx, stream, leaf_out=None):

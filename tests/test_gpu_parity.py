@@ -45,20 +45,20 @@ def test_execute_reference_plan(name):
     assert _same(got.astype(np.float64), case.want)
 
 
-@pytest.mark.parametrize("variant", [N.FOREST_PERFECT, N.FOREST_GENERAL, N.FOREST_RANKED])
+@pytest.mark.parametrize("variant", [N.FOREST_PERFECT, N.FOREST_GENERAL, N.FOREST_RANKED, N.FOREST_MMA])
 @pytest.mark.parametrize("name", [n for n in gc.case_names() if gc.get(n).leaves is not None])
 def test_leaf_indices_and_variants(name, variant):
     case = gc.get(name)
     spec = lower.lower_model(case.model, case.profile, case.passes)
     st = spec.stages[0]
-    if variant in (N.FOREST_PERFECT, N.FOREST_RANKED) and (max(t.depth() for t in st.trees) > 11
-                                                            or max(t.depth() for t in st.trees) == 0):
+    if variant in (N.FOREST_PERFECT, N.FOREST_RANKED, N.FOREST_MMA) and (max(t.depth() for t in st.trees) > 11
+                                                                          or max(t.depth() for t in st.trees) == 0):
         pytest.skip("too deep / no internal node for the perfect layout")
     try:
         prog = DeviceProgram(spec, 0, forest_variant=variant)
     except UnresolvedKernel:
-        assert variant in (N.FOREST_PERFECT, N.FOREST_RANKED)
-        pytest.skip("perfect/ranked layout does not fit this forest")
+        assert variant in (N.FOREST_PERFECT, N.FOREST_RANKED, N.FOREST_MMA)
+        pytest.skip("perfect/ranked/mma layout does not fit this forest")
     x = torch.from_numpy(case.x).cuda()
     leaves = torch.full((x.shape[0], len(st.trees)), -7, dtype=torch.int32, device="cuda")
     y = prog.run(x, leaf_out=leaves)
@@ -162,7 +162,7 @@ def test_large_synthetic_vs_c_oracle(T, depth, F, C, gbdt, n):
     spec = lower.lower_model(m)
     xd = torch.from_numpy(x).cuda()
     ran = 0
-    for variant in (N.FOREST_AUTO, N.FOREST_RANKED, N.FOREST_PERFECT, N.FOREST_GENERAL):
+    for variant in (N.FOREST_AUTO, N.FOREST_RANKED, N.FOREST_PERFECT, N.FOREST_GENERAL, N.FOREST_MMA):
         try:
             prog = DeviceProgram(spec, 0, forest_variant=variant)
         except UnresolvedKernel:
