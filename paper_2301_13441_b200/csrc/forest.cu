@@ -1361,8 +1361,14 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
   }
 
   f->rpt = saved_rpt;
-  if (want == CMLB_FOREST_AUTO)
-    want = ranked_ok ? CMLB_FOREST_RANKED : (perfect_ok ? CMLB_FOREST_PERFECT : CMLB_FOREST_GENERAL);
+  // AUTO: measured on B200 (tools/variant_table.py -> profiles/r1_variant_table.json):
+  // ranked wins from ~64 trees up (its per-row ranking pass amortizes over the
+  // trees), the f32 perfect layout below that, general for deep trees; the
+  // tcgen05 path-matrix form never wins (>= 10x slower at every shape).
+  if (want == CMLB_FOREST_AUTO) {
+    if (ranked_ok && (f->T >= 64 || !perfect_ok)) want = CMLB_FOREST_RANKED;
+    else want = perfect_ok ? CMLB_FOREST_PERFECT : CMLB_FOREST_GENERAL;
+  }
   if (want == CMLB_FOREST_PERFECT && !perfect_ok)
     return fail(CMLB_E_UNRESOLVED, "perfect layout does not fit (depth/outputs/features)");
   if (want == CMLB_FOREST_RANKED && !ranked_ok)
