@@ -21,7 +21,11 @@ except Exception:  # pragma: no cover - the GPU box has no reference
 
 def _bases(name: str, *own):
     ref = getattr(_ref_errors, name, None) if _ref_errors is not None else None
-    return own + ((ref,) if ref is not None else ())
+    if ref is None:
+        return own
+    # a base the reference class already derives from (Exception) must not
+    # precede it, or the MRO is inconsistent
+    return tuple(b for b in own if not issubclass(ref, b)) + (ref,)
 
 
 class MlowerError(*_bases("MlowerError", Exception)):
