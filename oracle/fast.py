@@ -23,10 +23,15 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(os.path.join(HERE, "cml_oracle.c")):
+        srcs = [os.path.join(HERE, f) for f in ("cml_oracle.c", "svm_oracle.c")]
+        if not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(s) for s in srcs):
             subprocess.run(["make", "-s", "-C", HERE], check=True)
         _lib = C.CDLL(LIB)
         _lib.oracle_forest.restype = C.c_int
+        _lib.oracle_svm.restype = C.c_int
+        _lib.oracle_svm.argtypes = [C.c_int32, C.c_double, C.c_double, C.c_int32, C.c_void_p, C.c_int32,
+                                    C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p,
+                                    C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_int32]
     return _lib
 
 

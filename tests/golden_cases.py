@@ -87,3 +87,50 @@ def agrees(case: Case, got: np.ndarray, tol: float = 1e-5) -> bool:
     same = (got == want) | both_nan
     close = np.abs(got - want) <= tol * np.maximum(np.abs(want), 1.0)
     return bool(np.all(same | close))
+
+
+# -- extended families (tools/make_golden_ext.py: scikit-learn + reference steps) --
+
+
+@functools.lru_cache(maxsize=1)
+def _ext_index():
+    with open(os.path.join(GOLDEN, "ext_index.json")) as fh:
+        return json.load(fh)
+
+
+@functools.lru_cache(maxsize=1)
+def _ext_arrays():
+    return dict(np.load(os.path.join(GOLDEN, "ext_arrays.npz")))
+
+
+class ExtCase:
+    def __init__(self, entry: dict):
+        self.entry = entry
+        self.name = entry["name"]
+        self.kind = entry["kind"]          # svm | transform | pipeline
+        arr = _ext_arrays()
+        self.x = arr[f"{self.name}__x"]
+        self.want = arr[f"{self.name}__want"]
+        self.dec = arr.get(f"{self.name}__dec")
+        self.sk_pred = arr.get(f"{self.name}__sk_pred")
+        self.model_json = bytes(arr[f"{self.name}__model"]).decode()
+        self.want_dtype = entry["want_dtype"]
+
+    @functools.cached_property
+    def model(self):
+        return parse_model(self.model_json)
+
+    @property
+    def is_classifier(self) -> bool:
+        return bool(getattr(self.model, "is_classifier", False))
+
+
+def ext_case_names():
+    return [e["name"] for e in _ext_index()]
+
+
+def ext_get(name: str) -> ExtCase:
+    for e in _ext_index():
+        if e["name"] == name:
+            return ExtCase(e)
+    raise KeyError(name)
