@@ -187,6 +187,46 @@ int cmlb_scaler_run(const cmlb_scaler* s, const float* x, int64_t n_rows, int64_
                     float* y, void* stream);
 void cmlb_scaler_destroy(cmlb_scaler* s);
 
+/* ------------------------------------------------------------------------ *
+ * Kernel SVMs (SVC / NuSVC / SVR / NuSVR).  Not in the reference:
+ * the semantics are libsvm's dense svm_predict_values as shipped in
+ * scikit-learn (see oracle/svm_oracle.c).  The Gram contraction X . SV^T runs
+ * on tcgen05 tensor cores as split-TF32 (3 products per K step, ~fp32
+ * accurate) with the kernel function and the one-vs-one decision sums fused
+ * into the TMEM epilogue (float64 accumulators); rows whose decision is within
+ * the epilogue's error bound of a vote flip are recomputed exactly in float64
+ * in libsvm's operation order by a second kernel.
+ * ------------------------------------------------------------------------ */
+
+enum cmlb_svm_kernel { CMLB_SVM_LINEAR = 0, CMLB_SVM_POLY = 1, CMLB_SVM_RBF = 2, CMLB_SVM_SIGMOID = 3 };
+
+typedef struct cmlb_svm_desc {
+  int32_t n_features;
+  int32_t n_sv;
+  int32_t kernel;              /* cmlb_svm_kernel */
+  int32_t degree;
+  double gamma;
+  double coef0;
+  const float* support_vectors; /* [n_sv][n_features], grouped by class for svc */
+  const float* dual_coef;      /* [n_classes - 1][n_sv] (svc) or [1][n_sv] (svr) */
+  const float* intercept;      /* [n_classes (n_classes - 1) / 2] (svc) or [1] (svr) */
+  const int32_t* n_support;    /* [n_classes] (svc); NULL for svr */
+  int32_t n_classes;           /* >= 2 for svc, 0 for svr */
+  const double* classes;       /* svc labels */
+  int32_t out_dtype;           /* svc: label dtype; svr: CMLB_OUT_F32 */
+} cmlb_svm_desc;
+
+typedef struct cmlb_svm cmlb_svm;
+int cmlb_svm_create(const cmlb_svm_desc* desc, int device, cmlb_svm** out);
+/* y: [n_rows][1] labels (svc) or float32 values (svr).  decision: optional
+ * device float64 [n_rows][max(1, pairs)] libsvm decision values (sum - rho).
+ * exact_rows: optional device int32, receives how many rows took the float64
+ * path.  Scratch is stream-ordered (cudaMallocAsync), so runs on different
+ * streams do not share state. */
+int cmlb_svm_run(const cmlb_svm* m, const float* x, int64_t n_rows, int64_t ldx, void* y, double* decision,
+                 int32_t* exact_rows, void* stream);
+void cmlb_svm_destroy(cmlb_svm* m);
+
 #ifdef __cplusplus
 }
 #endif

@@ -47,6 +47,15 @@ class ScalerDesc(C.Structure):
     ]
 
 
+class SVMDesc(C.Structure):
+    _fields_ = [
+        ("n_features", c_i32), ("n_sv", c_i32), ("kernel", c_i32), ("degree", c_i32),
+        ("gamma", c_f64), ("coef0", c_f64), ("support_vectors", P(c_f32)), ("dual_coef", P(c_f32)),
+        ("intercept", P(c_f32)), ("n_support", P(c_i32)), ("n_classes", c_i32), ("classes", P(c_f64)),
+        ("out_dtype", c_i32),
+    ]
+
+
 # enum values (cmlb.h)
 AGG_NONE, AGG_MEAN, AGG_SUM = 0, 1, 2
 TAIL_VALUES, TAIL_ARGMAX, TAIL_SIGMOID = 0, 1, 2
@@ -54,6 +63,7 @@ FOREST_AUTO, FOREST_PERFECT, FOREST_GENERAL, FOREST_RANKED, FOREST_MMA = 0, 1, 2
 LIN_VALUES, LIN_ARGMAX, LIN_SOFTMAX_ARGMAX, LIN_SIGMOID, LIN_SIGN = 0, 1, 2, 3, 4
 (SCALER_BINARIZER, SCALER_NORM_L1, SCALER_NORM_L2, SCALER_NORM_MAX, SCALER_MINMAX,
  SCALER_SUB_DIV, SCALER_DIV) = range(7)
+SVM_KERNEL = {"linear": 0, "poly": 1, "rbf": 2, "sigmoid": 3}
 
 _lock = threading.Lock()
 _lib = None
@@ -75,6 +85,10 @@ SIGNATURES = {
     "cmlb_scaler_create": (C.c_int, [P(ScalerDesc), C.c_int, P(c_vp)]),
     "cmlb_scaler_run": (C.c_int, [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp]),
     "cmlb_scaler_destroy": (None, [c_vp]),
+    "cmlb_svm_create": (C.c_int, [P(SVMDesc), C.c_int, P(c_vp)]),
+    "cmlb_svm_run": (C.c_int, [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "cmlb_svm_destroy": (None, [c_vp]),
+    "cmlb_svm_debug_fast": (C.c_int, [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "cmlb_debug_pairwise_schedule": (C.c_int, [c_i64, P(C.c_uint32)]),
 }
 

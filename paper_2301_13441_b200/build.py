@@ -16,7 +16,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libcmlb.so")
-SOURCES = ["capi.cu", "forest.cu", "linear.cu", "scaler.cu"]
+SOURCES = ["capi.cu", "forest.cu", "linear.cu", "scaler.cu", "svm.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
@@ -27,7 +27,7 @@ def _newest(paths):
 
 def build(force: bool = False, verbose: bool = False) -> str:
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    deps = srcs + [os.path.join(CSRC, "common.cuh"), os.path.join(ROOT, "include", "cmlb.h")]
+    deps = srcs + [os.path.join(CSRC, h) for h in ("common.cuh", "sm100.cuh")] + [os.path.join(ROOT, "include", "cmlb.h")]
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= _newest(deps):
         return LIB
     objdir = os.path.join(PKG, "build")

@@ -1,0 +1,765 @@
+// Kernel SVM operator (SVC / NuSVC / SVR / NuSVR) on sm_100a.
+//
+// Semantics (not in the reference): libsvm's dense
+// svm_predict_values as shipped in scikit-learn -- see oracle/svm_oracle.c,
+// which is pinned bit-exactly to scikit-learn.  Per row x:
+//   K_j = k(x, sv_j)                         (rbf / poly / sigmoid / linear)
+//   dec_p = sum_{j in class a} coef[b-1][j] K_j + sum_{j in class b} coef[a][j] K_j - rho_p
+//   for each class pair p = (a < b); vote a iff dec_p > 0; label = first max.
+//
+// Two kernels:
+//
+//  * svm_tc_kernel -- the Gram contraction G = X . SV^T (the only O(F) work
+//    per (row, SV)) on tcgen05 tensor cores, M = 128 rows x N = 256 support
+//    vectors per TMEM accumulator, K = 32 features per pipeline stage.
+//    TF32 keeps 10 mantissa bits, so each operand is split exactly,
+//    v = big + small (big = v with the low 13 mantissa bits cleared), and
+//    G += Xb.Sb + Xs.Sb + Xb.Ss: three tf32 MMAs per K step give ~fp32
+//    accuracy ("3xTF32").  SV splits are prepared once on the host in the
+//    UMMA core-matrix layout and streamed by TMA bulk copies; row tiles are
+//    split on the fly by four producer warps.  Warp roles: 0-3 A producers
+//    (load + split X), 4 B producer (cp.async.bulk), 5 MMA issuer (one
+//    thread) + TMEM owner, 6-9 epilogue.  TMEM holds two 128 x 256 f32
+//    accumulators so the epilogue of SV tile t overlaps the MMAs of t+1.
+//    Epilogue (thread = row = TMEM lane): kernel function of the Gram entry,
+//    float64 per-class decision sums, a running error bound E for the row;
+//    after the last tile: votes -> label.  A row whose decision values are
+//    within 4E of zero (a vote could flip) -- or any non-finite value -- is
+//    queued for the exact path instead of written.
+//
+//  * svm_exact_kernel -- persistent; recomputes queued rows in float64 in
+//    libsvm's exact operation order (OpenBLAS SkylakeX ddot order for every
+//    kernel dot product, sequential decision sums), 32 rows per CTA batch.
+//    Residual: CUDA's double exp/tanh may differ from glibc's by an ulp,
+//    which moves a decision by ~1e-16 relative.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace cmlb {
+namespace svm {
+
+using namespace sm100;
+
+constexpr int BM = 128;                       // rows per tile = TMEM lanes
+constexpr int BN = 256;                       // support vectors per tile = MMA N
+constexpr int BK = 32;                        // features per stage (128 B of fp32)
+constexpr int STAGES = 2;
+constexpr int A_BYTES = BM * BK * 4;          // 16 KB per split half
+constexpr int B_BYTES = BN * BK * 4;          // 32 KB per split half
+constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+constexpr int THREADS = 320;
+constexpr int EPI_WARP0 = 6;
+constexpr int MAXC = 16;                      // classes handled by the fused epilogue
+constexpr int XR = 32;                        // rows per exact-path batch
+constexpr int XCH = 256;                      // support vectors per exact-path chunk
+
+struct Args {
+  const float* x;
+  int64_t n_rows, ldx;
+  int F, KB, n_tiles, n_sv;
+  const uint8_t* bsplit;   // [n_tiles][KB][big | small][BN x BK core-matrix layout]
+  const float* ns;         // [n_tiles * BN] |sv|^2 (float64 rounded once)
+  const float* w;          // [n_tiles * BN][CP] coefficient of SV j toward class o (0 for its own class)
+  const float* wmax;       // [n_tiles * BN] max_o |w|
+  const int32_t* cls;      // [n_tiles * BN] class of SV j, -1 padding
+  const float* sv;         // [n_sv][F] (exact path)
+  const float* coef;       // [rows][n_sv] libsvm sv_coef (exact path)
+  const float* intercept;  // [pairs]
+  const double* classes;
+  int C, CP, pairs, kernel, degree, is_svr, out_dt, vec_x;
+  float gamma, coef0;
+  double gamma64, coef064;
+  void* y;
+  double* dec_out;
+  float* err_out;          // debug: per-row error bound E (nullable)
+  int no_exact;            // debug: write every row from the fast path
+  int32_t* queue;          // [n_rows] rows for the exact path
+  int32_t* queue_len;
+};
+
+__host__ __device__ inline int pair_index(int a, int b, int C) {  // a < b
+  return a * (2 * C - a - 1) / 2 + (b - a - 1);
+}
+
+// ---------------------------------------------------------------------------
+// fast path
+// ---------------------------------------------------------------------------
+
+// Kernel value of a Gram entry and its error bound.  de bounds the Gram
+// entry's error: the dropped small*small products are each below
+// 2^-20 |x_k s_k| (a tf32 "big" half keeps 11 significant bits), so they sum
+// to <= 2^-20 |x| |s| <= 2^-21 (|x|^2 + |s|^2) (Cauchy-Schwarz); the tf32
+// rounding of the small halves contributes the same order again, and the
+// caller's 4x safety factor on the accumulated bound covers both plus the
+// f32 accumulation.  Measured errors are 100-1000x below this bound
+// (tools/svm_error_probe.py, profiles/r1_svm_error_probe.jsonl).
+__device__ __forceinline__ float kvalue_fast(const Args& a, float g, float nx, float nsj, float& err) {
+  const float de = 4.76837158203125e-07f * (nx + nsj);  // 2^-21
+  if (a.kernel == CMLB_SVM_RBF) {
+    // d2 = nx + ns - 2g: error 2 de (Gram) + one f32 rounding of ~(nx + ns);
+    // exp2f: <= 2 ulp; the f32 argument product: 1 ulp
+    const float d2 = fmaxf(fmaf(-2.0f, g, nx + nsj), 0.0f);
+    const float k = exp2f(-a.gamma * 1.4426950408889634f * d2);
+    err = k * (a.gamma * (2.0f * de + 1.2e-7f * (nx + nsj)) + 6.0e-7f);
+    return k;
+  }
+  if (a.kernel == CMLB_SVM_LINEAR) {
+    err = de + 1.2e-7f * fabsf(g);
+    return g;
+  }
+  const float u = fmaf(a.gamma, g, a.coef0);
+  if (a.kernel == CMLB_SVM_POLY) {
+    float k = 1.0f, du = 1.0f;  // u^deg and u^(deg-1)
+    for (int i = 0; i < a.degree; ++i) {
+      if (i + 1 < a.degree) du *= u;
+      k *= u;
+    }
+    err = (float)a.degree * (fabsf(du) * (a.gamma * de + 1.2e-7f * fabsf(u)) + 2.4e-7f * fabsf(k)) + 1e-30f;
+    return k;
+  }
+  const float k = tanhf(u);
+  err = (1.0f - k * k) * (a.gamma * de + 1.2e-7f * fabsf(u)) + 4.0e-7f;
+  return k;
+}
+
+template <int CP>
+__device__ __forceinline__ void flush(const Args& a, int cur, const double (&acc)[CP], double* dec) {
+  if (cur < 0) return;
+  if (a.is_svr) {
+    dec[0] += acc[0];
+    return;
+  }
+#pragma unroll
+  for (int o = 0; o < CP; ++o) {
+    if (o < a.C && o != cur) {
+      const int p = o < cur ? pair_index(o, cur, a.C) : pair_index(cur, o, a.C);
+      dec[p] += acc[o];
+    }
+  }
+}
+
+template <int CP>
+__global__ void __launch_bounds__(THREADS, 1) svm_tc_kernel(const Args a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES], tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_slot;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t row0 = (int64_t)blockIdx.x * BM;
+  const int KB = a.KB, NT = a.n_tiles;
+  const int total = NT * KB;
+
+  // epilogue tables (after the stages)
+  float* w_s = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);   // [BN][CP]
+  float* ns_s = w_s + BN * CP;
+  float* wm_s = ns_s + BN;
+  int32_t* cls_s = reinterpret_cast<int32_t*>(wm_s + BN);
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      bar_init(&full_bar[s], BM + 1);
+      bar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      bar_init(&tfull_bar[b], 1);
+      bar_init(&tempty_bar[b], BM);
+    }
+    bar_fence_init();
+  }
+  if (warp == 5) tmem_alloc(&tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp < 4) {
+    // ---- A producers: thread r owns row r of the tile --------------------
+    const int r = tid;
+    const int64_t row = row0 + r;
+    const bool valid = row < a.n_rows;
+    const float* src = a.x + (valid ? row : 0) * a.ldx;
+    for (int it = 0; it < total; ++it) {
+      const int kb = it % KB, s = it % STAGES;
+      bar_wait(&empty_bar[s], ((it / STAGES) & 1) ^ 1);
+      uint8_t* abig = smem + s * STAGE_BYTES;
+      uint8_t* asmall = abig + A_BYTES;
+      const int k0 = kb * BK;
+#pragma unroll
+      for (int c = 0; c < BK / 4; ++c) {
+        const int k = k0 + 4 * c;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (valid) {
+          if (a.vec_x && k + 3 < a.F) {
+            v = __ldg(reinterpret_cast<const float4*>(src + k));
+          } else {
+            if (k < a.F) v.x = __ldg(src + k);
+            if (k + 1 < a.F) v.y = __ldg(src + k + 1);
+            if (k + 2 < a.F) v.z = __ldg(src + k + 2);
+            if (k + 3 < a.F) v.w = __ldg(src + k + 3);
+          }
+        }
+        float4 hi, lo;
+        hi.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u); lo.x = v.x - hi.x;
+        hi.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u); lo.y = v.y - hi.y;
+        hi.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u); lo.z = v.z - hi.z;
+        hi.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u); lo.w = v.w - hi.w;
+        *reinterpret_cast<float4*>(abig + c * (BM * 16) + r * 16) = hi;
+        *reinterpret_cast<float4*>(asmall + c * (BM * 16) + r * 16) = lo;
+      }
+      fence_async_smem();
+      bar_arrive(&full_bar[s]);
+    }
+  } else if (warp == 4) {
+    // ---- B producer: one bulk copy of the pre-split SV stage -------------
+    if (lane == 0) {
+      for (int it = 0; it < total; ++it) {
+        const int s = it % STAGES;
+        bar_wait(&empty_bar[s], ((it / STAGES) & 1) ^ 1);
+        uint8_t* dst = smem + s * STAGE_BYTES + 2 * A_BYTES;
+        const uint8_t* src = a.bsplit + (size_t)it * (2 * B_BYTES);
+        bar_arrive_tx(&full_bar[s], 2 * B_BYTES);
+        bulk_load(dst, src, B_BYTES, &full_bar[s]);
+        bulk_load(dst + B_BYTES, src + B_BYTES, B_BYTES, &full_bar[s]);
+      }
+    }
+  } else if (warp == 5) {
+    // ---- MMA issuer ------------------------------------------------------
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_tf32(BM, BN);
+      const uint32_t sbase = smem_addr(smem);
+      for (int t = 0; t < NT; ++t) {
+        const int b = t & 1;
+        bar_wait(&tempty_bar[b], ((t >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(b * BN);
+        for (int kb = 0; kb < KB; ++kb) {
+          const int it = t * KB + kb, s = it % STAGES;
+          bar_wait(&full_bar[s], (it / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t abig = sbase + s * STAGE_BYTES, asmall = abig + A_BYTES;
+          const uint32_t bbig = abig + 2 * A_BYTES, bsmall = bbig + B_BYTES;
+#pragma unroll
+          for (int k8 = 0; k8 < BK / 8; ++k8) {
+            const uint32_t ao = (uint32_t)k8 * 2 * (BM * 16), bo = (uint32_t)k8 * 2 * (BN * 16);
+            const uint64_t ab = desc_kmajor(abig + ao, BM * 16, 128), as = desc_kmajor(asmall + ao, BM * 16, 128);
+            const uint64_t bb = desc_kmajor(bbig + bo, BN * 16, 128), bs = desc_kmajor(bsmall + bo, BN * 16, 128);
+            mma_tf32(d, ab, bb, idesc, (kb | k8) != 0);
+            mma_tf32(d, as, bb, idesc, 1u);
+            mma_tf32(d, ab, bs, idesc, 1u);
+          }
+          mma_commit(&empty_bar[s]);  // stage s free once these MMAs retire
+        }
+        mma_commit(&tfull_bar[b]);    // accumulator b complete
+      }
+    }
+  } else {
+    // ---- epilogue: thread = row = TMEM lane -------------------------------
+    const int eg = warp & 3;                 // TMEM lane group this warp may access
+    const int r = eg * 32 + lane;
+    const int et = tid - EPI_WARP0 * 32;     // 0..127 (for cooperative table loads)
+    const int64_t row = row0 + r;
+    const bool valid = row < a.n_rows;
+    float nx = 0.0f;
+    if (valid) {
+      const float* src = a.x + row * a.ldx;
+      double s = 0.0;
+      for (int k = 0; k < a.F; ++k) {
+        const double v = (double)__ldg(src + k);
+        s = fma(v, v, s);
+      }
+      nx = (float)s;
+    }
+    double acc[CP];
+#pragma unroll
+    for (int o = 0; o < CP; ++o) acc[o] = 0.0;
+    double dec[MAXC * (MAXC - 1) / 2];
+    for (int p = 0; p < a.pairs; ++p) dec[p] = 0.0;
+    float err_sum = 0.0f;
+    int cur = -1;
+    for (int t = 0; t < NT; ++t) {
+      const int b = t & 1;
+      // this tile's SV tables -> shared memory (previous tile's readers are done)
+      named_bar_sync(1, BM);
+      {
+        const int j0 = t * BN;
+        for (int i = et; i < BN * CP; i += BM) w_s[i] = __ldg(a.w + (size_t)j0 * CP + i);
+        for (int i = et; i < BN; i += BM) {
+          ns_s[i] = __ldg(a.ns + j0 + i);
+          wm_s[i] = __ldg(a.wmax + j0 + i);
+          cls_s[i] = __ldg(a.cls + j0 + i);
+        }
+      }
+      named_bar_sync(1, BM);
+      bar_wait(&tfull_bar[b], (t >> 1) & 1);
+      tc_fence_after();
+      const uint32_t taddr = tmem + ((uint32_t)(eg * 32) << 16) + (uint32_t)(b * BN);
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t g[32];
+        tmem_ld32(taddr + (uint32_t)c0, g);
+#pragma unroll 4
+        for (int jj = 0; jj < 32; ++jj) {
+          const int j = c0 + jj;
+          const int c = cls_s[j];
+          if (c != cur) {  // uniform: classes are contiguous
+            flush<CP>(a, cur, acc, dec);
+#pragma unroll
+            for (int o = 0; o < CP; ++o) acc[o] = 0.0;
+            cur = c;
+          }
+          float e;
+          const float k = kvalue_fast(a, __uint_as_float(g[jj]), nx, ns_s[j], e);
+          err_sum = fmaf(wm_s[j], e, err_sum);
+          const double kd = (double)k;
+          const float* wj = w_s + j * CP;
+#pragma unroll
+          for (int o = 0; o < CP; ++o) acc[o] = fma((double)wj[o], kd, acc[o]);
+        }
+      }
+      tc_fence_before();
+      bar_arrive(&tempty_bar[b]);
+    }
+    flush<CP>(a, cur, acc, dec);
+    if (valid) {
+      const float tol = 4.0f * err_sum + 1e-30f;
+      if (a.err_out) a.err_out[row] = err_sum;
+      bool exact = !(tol < 3.0e38f);
+      if (a.is_svr) {
+        const double v = dec[0] + (double)a.intercept[0];
+        exact = exact || !(fabs(v) * 4.76837158203125e-07 > (double)tol);  // need rel. error < 2^-21
+        if (a.no_exact) exact = false;
+        if (!exact) {
+          store_out(a.y, row, a.out_dt, (double)(float)v);
+          if (a.dec_out) a.dec_out[row] = v;
+        }
+      } else {
+        int vote[MAXC];
+        for (int c = 0; c < a.C; ++c) vote[c] = 0;
+        int p = 0;
+        for (int i = 0; i < a.C; ++i) {
+          for (int j = i + 1; j < a.C; ++j, ++p) {
+            const double v = dec[p] + (double)a.intercept[p];
+            dec[p] = v;
+            exact = exact || !(fabs(v) > (double)tol);
+            if (v > 0) ++vote[i]; else ++vote[j];
+          }
+        }
+        if (a.no_exact) exact = false;
+        if (!exact) {
+          int best = 0;
+          for (int c = 1; c < a.C; ++c)
+            if (vote[c] > vote[best]) best = c;
+          store_out(a.y, row, a.out_dt, a.classes[best]);
+          if (a.dec_out)
+            for (int q = 0; q < a.pairs; ++q) a.dec_out[row * a.pairs + q] = dec[q];
+        }
+      }
+      if (exact) a.queue[atomicAdd(a.queue_len, 1)] = (int32_t)row;
+    }
+  }
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_free(tmem, 512);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// exact path: libsvm order in float64
+// ---------------------------------------------------------------------------
+
+// OpenBLAS SkylakeX ddot order (oracle/svm_oracle.c: ddot_skx) for one
+// (row, SV) pair; xs = the row's features in shared memory, column stride XR.
+// RBF: the vectors are d = x - s (ddot(d, d)); otherwise ddot(x, s).
+__device__ double exact_dot(const float* xs, const float* s, int F, bool rbf) {
+  const int n1 = F & -16, n32 = n1 & ~31;
+  auto term = [&](int k, double acc) {
+    const double xv = (double)xs[k * XR], sv = (double)__ldg(s + k);
+    if (rbf) {
+      const double d = __dsub_rn(xv, sv);
+      return fma(d, d, acc);
+    }
+    return fma(xv, sv, acc);
+  };
+  double a4[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int aa = q >> 2, l = q & 3;
+    double lo = 0.0, hi = 0.0;
+    for (int i = 0; i < n32; i += 32) {
+      lo = term(i + 8 * aa + l, lo);
+      hi = term(i + 8 * aa + l + 4, hi);
+    }
+    double v = __dadd_rn(lo, hi);
+    for (int i = n32; i < n1; i += 16) v = term(i + 4 * aa + l, v);
+    a4[q] = v;
+  }
+  double sl[4];
+#pragma unroll
+  for (int l = 0; l < 4; ++l) sl[l] = __dadd_rn(__dadd_rn(__dadd_rn(a4[l], a4[4 + l]), a4[8 + l]), a4[12 + l]);
+  double dot = n1 ? __dadd_rn(__dadd_rn(sl[0], sl[2]), __dadd_rn(sl[1], sl[3])) : 0.0;
+  for (int i = n1; i < F; ++i) dot = term(i, dot);
+  return dot;
+}
+
+__device__ double exact_k(const Args& a, const float* xs, const float* s) {
+  if (a.kernel == CMLB_SVM_RBF) return exp(__dmul_rn(-a.gamma64, exact_dot(xs, s, a.F, true)));
+  const double dot = exact_dot(xs, s, a.F, false);
+  if (a.kernel == CMLB_SVM_LINEAR) return dot;
+  const double u = __dadd_rn(__dmul_rn(a.gamma64, dot), a.coef064);
+  if (a.kernel == CMLB_SVM_SIGMOID) return tanh(u);
+  double tmp = u, ret = 1.0;  // libsvm powi
+  for (int t = a.degree; t > 0; t /= 2) {
+    if (t % 2 == 1) ret = __dmul_rn(ret, tmp);
+    tmp = __dmul_rn(tmp, tmp);
+  }
+  return ret;
+}
+
+constexpr int XTHREADS = 256;
+
+__global__ void __launch_bounds__(XTHREADS) svm_exact_kernel(const Args a, const int* n_sv_start) {
+  extern __shared__ __align__(16) uint8_t xsm[];
+  float* xs = reinterpret_cast<float*>(xsm);                         // [F][XR]
+  double* kv = reinterpret_cast<double*>(xsm + (((size_t)a.F * XR * 4 + 15) & ~(size_t)15));  // [XCH][XR]
+  double* decs = kv + XCH * XR;                                      // [XR][pairs]
+  __shared__ int32_t rows[XR];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nq = *a.queue_len;
+  const int npairs = a.is_svr ? 1 : a.pairs;
+  const int ntasks = XR * npairs;
+  const int TPT = (ntasks + XTHREADS - 1) / XTHREADS;  // (row, pair) tasks per thread, <= 15
+  for (int b0 = blockIdx.x * XR; b0 < nq; b0 += gridDim.x * XR) {
+    const int nb = min(XR, nq - b0);
+    if (tid < XR) rows[tid] = tid < nb ? a.queue[b0 + tid] : -1;
+    __syncthreads();
+    for (int i = tid; i < a.F * XR; i += XTHREADS) {
+      const int k = i / XR, r = i % XR;
+      xs[i] = rows[r] >= 0 ? __ldg(a.x + (int64_t)rows[r] * a.ldx + k) : 0.0f;
+    }
+    double sum[15];
+    for (int q = 0; q < 15; ++q) sum[q] = 0.0;
+    __syncthreads();
+    for (int j0 = 0; j0 < a.n_sv; j0 += XCH) {
+      const int nj = min(XCH, a.n_sv - j0);
+      // K values of this chunk: warp w takes SVs w, w+8, ..; lane = row
+      for (int jj = warp; jj < nj; jj += XTHREADS / 32)
+        kv[jj * XR + lane] = exact_k(a, xs + lane, a.sv + (size_t)(j0 + jj) * a.F);
+      __syncthreads();
+      // sequential decision sums in libsvm order, one (row, pair) per slot
+      for (int q = 0; q < TPT; ++q) {
+        const int task = tid + q * XTHREADS;
+        if (task >= ntasks) break;
+        const int r = task % XR, p = task / XR;
+        double s = sum[q];
+        if (a.is_svr) {
+          for (int jj = 0; jj < nj; ++jj)
+            s = __dadd_rn(s, __dmul_rn((double)__ldg(a.coef + j0 + jj), kv[jj * XR + r]));
+        } else {
+          // pair p -> (ca, cb)
+          int ca = 0, rem = p;
+          while (rem >= a.C - 1 - ca) { rem -= a.C - 1 - ca; ++ca; }
+          const int cb = ca + 1 + rem;
+          const int lo_a = n_sv_start[ca], hi_a = n_sv_start[ca + 1];
+          const int lo_b = n_sv_start[cb], hi_b = n_sv_start[cb + 1];
+          const float* c1 = a.coef + (size_t)(cb - 1) * a.n_sv;
+          const float* c2 = a.coef + (size_t)ca * a.n_sv;
+          for (int j = max(lo_a, j0); j < min(hi_a, j0 + nj); ++j)
+            s = __dadd_rn(s, __dmul_rn((double)__ldg(c1 + j), kv[(j - j0) * XR + r]));
+          for (int j = max(lo_b, j0); j < min(hi_b, j0 + nj); ++j)
+            s = __dadd_rn(s, __dmul_rn((double)__ldg(c2 + j), kv[(j - j0) * XR + r]));
+        }
+        sum[q] = s;
+      }
+      __syncthreads();
+    }
+    for (int q = 0; q < TPT; ++q) {
+      const int task = tid + q * XTHREADS;
+      if (task < ntasks) {
+        const int r = task % XR, p = task / XR;
+        decs[r * npairs + p] = __dsub_rn(sum[q], -(double)a.intercept[p]);
+      }
+    }
+    __syncthreads();
+    if (tid < nb) {
+      const int64_t row = rows[tid];
+      const double* d = decs + tid * npairs;
+      if (a.is_svr) {
+        store_out(a.y, row, a.out_dt, (double)(float)d[0]);
+        if (a.dec_out) a.dec_out[row] = d[0];
+      } else {
+        int vote[MAXC];
+        for (int c = 0; c < a.C; ++c) vote[c] = 0;
+        int p = 0;
+        for (int i = 0; i < a.C; ++i)
+          for (int j = i + 1; j < a.C; ++j, ++p) {
+            if (d[p] > 0) ++vote[i]; else ++vote[j];
+          }
+        int best = 0;
+        for (int c = 1; c < a.C; ++c)
+          if (vote[c] > vote[best]) best = c;
+        store_out(a.y, row, a.out_dt, a.classes[best]);
+        if (a.dec_out)
+          for (int q = 0; q < npairs; ++q) a.dec_out[row * npairs + q] = d[q];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace svm
+
+// ---------------------------------------------------------------------------
+// host program
+// ---------------------------------------------------------------------------
+
+struct cmlb_svm_impl {
+  int device;
+  svm::Args a;
+  int CP;
+  std::vector<void*> bufs;
+  int32_t* sv_start;   // device [C + 1]
+  size_t tc_smem, x_smem;
+};
+
+}  // namespace cmlb
+
+struct cmlb_svm : cmlb::cmlb_svm_impl {};
+
+namespace cmlb {
+
+template <typename T>
+static int upload(cmlb_svm* m, const std::vector<T>& h, const T** out) {
+  void* d = nullptr;
+  const size_t bytes = std::max<size_t>(h.size() * sizeof(T), 16);
+  CMLB_CUDA(cudaMalloc(&d, bytes));
+  m->bufs.push_back(d);
+  if (!h.empty()) CMLB_CUDA(cudaMemcpy(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+  *out = static_cast<const T*>(d);
+  return CMLB_OK;
+}
+
+static void destroy_svm(cmlb_svm* m) {
+  if (!m) return;
+  DeviceGuard g(m->device);
+  for (void* p : m->bufs) cudaFree(p);
+  delete m;
+}
+
+static int make_svm(const cmlb_svm_desc* d, int device, cmlb_svm** out) {
+  using namespace svm;
+  if (!d || !out) return fail(CMLB_E_VALIDATION, "null svm descriptor");
+  const int F = d->n_features, NSV = d->n_sv;
+  if (F <= 0 || NSV <= 0) return fail(CMLB_E_VALIDATION, "svm needs n_features > 0 and n_sv > 0");
+  if (d->kernel < CMLB_SVM_LINEAR || d->kernel > CMLB_SVM_SIGMOID) return fail(CMLB_E_VALIDATION, "unknown svm kernel");
+  const bool svr = d->n_classes == 0;
+  const int C = svr ? 1 : d->n_classes;
+  if (!svr && (C < 2 || C > MAXC)) return fail(CMLB_E_UNRESOLVED, "svc supports 2..16 classes");
+  if (!svr && !d->n_support) return fail(CMLB_E_VALIDATION, "svc needs n_support");
+  if (!out_dtype_ok(d->out_dtype)) return fail(CMLB_E_VALIDATION, "bad out_dtype");
+  const int pairs = svr ? 1 : C * (C - 1) / 2;
+  const int CP = C <= 2 ? 2 : C <= 4 ? 4 : C <= 8 ? 8 : 16;
+  const int KB = (F + BK - 1) / BK, NT = (NSV + BN - 1) / BN, NP = NT * BN;
+
+  cmlb_svm* m = new (std::nothrow) cmlb_svm();
+  if (!m) return fail(CMLB_E_DEVICE, "out of host memory");
+  m->device = device;
+  DeviceGuard g(device);
+  int st = CMLB_OK;
+
+  std::vector<int32_t> start(C + 1, 0);
+  std::vector<int32_t> cls(NP, -1);
+  if (svr) {
+    start[1] = NSV;
+  } else {
+    for (int c = 0; c < C; ++c) start[c + 1] = start[c] + d->n_support[c];
+    if (start[C] != NSV) {
+      destroy_svm(m);
+      return fail(CMLB_E_VALIDATION, "n_support does not sum to n_sv");
+    }
+  }
+  for (int c = 0; c < C; ++c)
+    for (int j = start[c]; j < start[c + 1]; ++j) cls[j] = c;
+  // per-SV coefficient toward each other class (libsvm: SV of class c in
+  // pair (c, o) uses coef[o-1] if c < o, else coef[o])
+  std::vector<float> w((size_t)NP * CP, 0.0f), wmax(NP, 0.0f), ns(NP, 0.0f);
+  for (int j = 0; j < NSV; ++j) {
+    const int c = cls[j];
+    for (int o = 0; o < C; ++o) {
+      float v;
+      if (svr) v = d->dual_coef[j];
+      else if (o == c) continue;
+      else v = d->dual_coef[(size_t)(c < o ? o - 1 : o) * NSV + j];
+      w[(size_t)j * CP + o] = v;
+      wmax[j] = std::max(wmax[j], std::fabs(v));
+    }
+    double s = 0.0;
+    for (int k = 0; k < F; ++k) {
+      const double v = d->support_vectors[(size_t)j * F + k];
+      s += v * v;
+    }
+    ns[j] = (float)s;
+  }
+  // SV splits in the UMMA core-matrix layout: [tile][kb][big|small][c][row][4]
+  std::vector<uint8_t> bsplit((size_t)NT * KB * 2 * B_BYTES, 0);
+  for (int t = 0; t < NT; ++t)
+    for (int kb = 0; kb < KB; ++kb) {
+      uint8_t* base = bsplit.data() + ((size_t)t * KB + kb) * 2 * B_BYTES;
+      for (int r = 0; r < BN; ++r) {
+        const int j = t * BN + r;
+        if (j >= NSV) continue;
+        for (int e = 0; e < BK; ++e) {
+          const int k = kb * BK + e;
+          if (k >= F) continue;
+          const float v = d->support_vectors[(size_t)j * F + k];
+          uint32_t u;
+          std::memcpy(&u, &v, 4);
+          u &= 0xFFFFE000u;
+          float hi;
+          std::memcpy(&hi, &u, 4);
+          const float lo = v - hi;
+          const size_t off = (size_t)(e / 4) * (BN * 16) + (size_t)r * 16 + (size_t)(e % 4) * 4;
+          std::memcpy(base + off, &hi, 4);
+          std::memcpy(base + B_BYTES + off, &lo, 4);
+        }
+      }
+    }
+  std::vector<float> svv(d->support_vectors, d->support_vectors + (size_t)NSV * F);
+  std::vector<float> coef(d->dual_coef, d->dual_coef + (size_t)(svr ? 1 : C - 1) * NSV);
+  std::vector<float> ic(d->intercept, d->intercept + pairs);
+  std::vector<double> classes(svr ? 1 : C, 0.0);
+  if (!svr)
+    for (int c = 0; c < C; ++c) classes[c] = d->classes[c];
+
+  Args& a = m->a;
+  std::memset(&a, 0, sizeof(a));
+  const uint8_t* bs = nullptr;
+  const int32_t* ss = nullptr;
+  if ((st = upload(m, bsplit, &bs)) || (st = upload(m, ns, &a.ns)) || (st = upload(m, w, &a.w)) ||
+      (st = upload(m, wmax, &a.wmax)) || (st = upload(m, cls, &a.cls)) || (st = upload(m, svv, &a.sv)) ||
+      (st = upload(m, coef, &a.coef)) || (st = upload(m, ic, &a.intercept)) ||
+      (st = upload(m, classes, &a.classes)) || (st = upload(m, start, &ss))) {
+    destroy_svm(m);
+    return st;
+  }
+  a.bsplit = bs;
+  m->sv_start = const_cast<int32_t*>(ss);
+  a.F = F; a.KB = KB; a.n_tiles = NT; a.n_sv = NSV;
+  a.C = C; a.CP = CP; a.pairs = pairs; a.kernel = d->kernel; a.degree = d->degree; a.is_svr = svr;
+  a.out_dt = d->out_dtype;
+  a.gamma = (float)d->gamma; a.coef0 = (float)d->coef0; a.gamma64 = d->gamma; a.coef064 = d->coef0;
+  m->CP = CP;
+  m->tc_smem = (size_t)STAGES * STAGE_BYTES + (size_t)BN * CP * 4 + BN * 4 * 3;
+  m->x_smem = (((size_t)F * XR * 4 + 15) & ~(size_t)15) + (size_t)XCH * XR * 8 + (size_t)XR * pairs * 8;
+  if (m->x_smem > 227 * 1024) {
+    destroy_svm(m);
+    return fail(CMLB_E_UNRESOLVED, "svm exact path: features x classes exceed shared memory");
+  }
+  *out = m;
+  return CMLB_OK;
+}
+
+template <int CP>
+static int launch_tc(const svm::Args& a, int64_t n, size_t smem, cudaStream_t s) {
+  auto fn = svm::svm_tc_kernel<CP>;
+  CMLB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  fn<<<(unsigned)ceil_div(n, svm::BM), svm::THREADS, smem, s>>>(a);
+  CMLB_CUDA(cudaGetLastError());
+  note_launch();
+  return CMLB_OK;
+}
+
+}  // namespace cmlb
+
+extern "C" {
+
+int cmlb_svm_create(const cmlb_svm_desc* desc, int device, cmlb_svm** out) {
+  try {
+    return cmlb::make_svm(desc, device, out);
+  } catch (const std::exception& e) {
+    return cmlb::fail(CMLB_E_DEVICE, e.what());
+  }
+}
+
+int cmlb_svm_run(const cmlb_svm* m, const float* x, int64_t n_rows, int64_t ldx, void* y, double* decision,
+                 int32_t* exact_rows, void* stream) {
+  using namespace cmlb;
+  if (!m) return fail(CMLB_E_VALIDATION, "null svm");
+  if (n_rows < 0 || ldx < m->a.F) return fail(CMLB_E_INPUT, "bad svm input shape");
+  if (n_rows > INT32_MAX) return fail(CMLB_E_INPUT, "svm batch exceeds 2^31 rows");
+  if (n_rows == 0) return CMLB_OK;
+  DeviceGuard g(m->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  svm::Args a = m->a;
+  a.x = x; a.n_rows = n_rows; a.ldx = ldx; a.y = y; a.dec_out = decision;
+  a.vec_x = ((reinterpret_cast<uintptr_t>(x) & 15) == 0 && (ldx & 3) == 0) ? 1 : 0;
+  void* scratch = nullptr;
+  CMLB_CUDA(cudaMallocAsync(&scratch, (size_t)(n_rows + 4) * sizeof(int32_t), s));
+  a.queue_len = static_cast<int32_t*>(scratch);
+  a.queue = a.queue_len + 4;
+  int st = CMLB_OK;
+  if (cudaMemsetAsync(a.queue_len, 0, sizeof(int32_t), s) != cudaSuccess) st = fail(CMLB_E_DEVICE, "memset");
+  if (!st) {
+    switch (m->CP) {
+      case 2: st = launch_tc<2>(a, n_rows, m->tc_smem, s); break;
+      case 4: st = launch_tc<4>(a, n_rows, m->tc_smem, s); break;
+      case 8: st = launch_tc<8>(a, n_rows, m->tc_smem, s); break;
+      default: st = launch_tc<16>(a, n_rows, m->tc_smem, s); break;
+    }
+  }
+  if (!st) {
+    cudaError_t e = cudaFuncSetAttribute(svm::svm_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)m->x_smem);
+    if (e != cudaSuccess) st = cuda_fail(e, "svm_exact smem");
+  }
+  if (!st) {
+    const int grid = std::max(1, std::min<int>(num_sms(m->device), (int)ceil_div(n_rows, svm::XR)));
+    svm::svm_exact_kernel<<<grid, svm::XTHREADS, m->x_smem, s>>>(a, m->sv_start);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) st = cuda_fail(e, "svm_exact_kernel");
+    else note_launch();
+  }
+  if (!st && exact_rows) {
+    cudaError_t e = cudaMemcpyAsync(exact_rows, a.queue_len, sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) st = cuda_fail(e, "exact_rows");
+  }
+  cudaFreeAsync(scratch, s);
+  return st;
+}
+
+void cmlb_svm_destroy(cmlb_svm* m) { cmlb::destroy_svm(m); }
+
+/* Diagnostics (tests/tools only): fast path for every row, with the
+ * epilogue's per-row error bound E written to err (device float32 [n]). */
+int cmlb_svm_debug_fast(const cmlb_svm* m, const float* x, int64_t n_rows, int64_t ldx, void* y, double* decision,
+                        float* err, void* stream) {
+  using namespace cmlb;
+  if (!m || n_rows <= 0) return fail(CMLB_E_VALIDATION, "debug_fast: bad arguments");
+  DeviceGuard g(m->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  svm::Args a = m->a;
+  a.x = x; a.n_rows = n_rows; a.ldx = ldx; a.y = y; a.dec_out = decision; a.err_out = err; a.no_exact = 1;
+  a.vec_x = ((reinterpret_cast<uintptr_t>(x) & 15) == 0 && (ldx & 3) == 0) ? 1 : 0;
+  void* scratch = nullptr;
+  CMLB_CUDA(cudaMallocAsync(&scratch, (size_t)(n_rows + 4) * sizeof(int32_t), s));
+  a.queue_len = static_cast<int32_t*>(scratch);
+  a.queue = a.queue_len + 4;
+  CMLB_CUDA(cudaMemsetAsync(a.queue_len, 0, sizeof(int32_t), s));
+  int st;
+  switch (m->CP) {
+    case 2: st = launch_tc<2>(a, n_rows, m->tc_smem, s); break;
+    case 4: st = launch_tc<4>(a, n_rows, m->tc_smem, s); break;
+    case 8: st = launch_tc<8>(a, n_rows, m->tc_smem, s); break;
+    default: st = launch_tc<16>(a, n_rows, m->tc_smem, s); break;
+  }
+  cudaFreeAsync(scratch, s);
+  return st;
+}
+
+}  // extern "C"

@@ -119,6 +119,22 @@ class ScalerSpec:
 
 
 @dataclass(eq=False)
+class SVMSpec:
+    """Kernel SVM (extmodels.SVMModel): libsvm decision + votes (svc) or value (svr)."""
+
+    model: object
+    out_dtype: str = "float32"
+
+    @property
+    def n_features(self) -> int:
+        return self.model.n_features
+
+    @property
+    def out_cols(self) -> int:
+        return 1
+
+
+@dataclass(eq=False)
 class ProgramSpec:
     """Stages run back to back; stage i's output feeds stage i+1."""
 
@@ -240,6 +256,11 @@ def lower_model(model, profile=None, passes=DEFAULT_PASSES) -> ProgramSpec:
         st = lower_forest_model(model, profile, passes)
     elif fam == "linear":
         st = lower_linear_model(model, profile, passes)
+    elif fam == "svm":
+        st = SVMSpec(model, _class_out(model.classes) if model.classes is not None else "float32")
+    elif fam in ("columns", "pipeline"):
+        from .fuse import lower_composite
+        return lower_composite(model, profile, passes)
     else:
         st = lower_scaler_model(model)
     return ProgramSpec([st], model.n_features)

@@ -21,7 +21,7 @@ import torch
 from . import _native as N
 from .dtypes import OUT_CODE
 from .errors import DeviceError, InputMismatch
-from .lower import ForestSpec, LinearSpec, ProgramSpec, ScalerSpec
+from .lower import ForestSpec, LinearSpec, ProgramSpec, ScalerSpec, SVMSpec
 
 TORCH_DTYPE = {
     "bool": torch.uint8, "int8": torch.int8, "int16": torch.int16, "int32": torch.int32,
@@ -141,7 +141,41 @@ class _Scaler:
             self.handle = None
 
 
-_BUILDERS = {ForestSpec: _Forest, LinearSpec: _Linear, ScalerSpec: _Scaler}
+class _SVM:
+    def __init__(self, spec: SVMSpec, device: int):
+        self.spec = spec
+        m = spec.model
+        sv = np.ascontiguousarray(m.support_vectors, np.float32)
+        coef = np.ascontiguousarray(m.dual_coef, np.float32)
+        ic = np.ascontiguousarray(m.intercept, np.float32)
+        svr = m.model_type == "svr"
+        ns = np.ascontiguousarray(np.asarray(m.n_support if not svr else (0,), np.int32))
+        classes = np.ascontiguousarray(np.asarray(m.classes if not svr else (0.0,), np.float64))
+        d = N.SVMDesc()
+        d.n_features, d.n_sv, d.kernel, d.degree = m.n_features, sv.shape[0], N.SVM_KERNEL[m.kernel], int(m.degree)
+        d.gamma, d.coef0 = float(m.gamma), float(m.coef0)
+        d.support_vectors, d.dual_coef, d.intercept = N.ptr(sv, N.c_f32), N.ptr(coef, N.c_f32), N.ptr(ic, N.c_f32)
+        d.n_support = N.ptr(ns, N.c_i32) if not svr else None
+        d.n_classes = 0 if svr else len(m.classes)
+        d.classes = N.ptr(classes, N.c_f64)
+        d.out_dtype = OUT_CODE[spec.out_dtype]
+        h = N.c_vp()
+        N.check(N.lib().cmlb_svm_create(C.byref(d), device, C.byref(h)))
+        self.handle = h
+        self.pairs = 1 if svr else len(m.classes) * (len(m.classes) - 1) // 2
+
+    def run(self, x, y, n, ldx, stream, leaf_out=None, decision=None, exact_rows=None):
+        dp = decision.data_ptr() if decision is not None else None
+        ep = exact_rows.data_ptr() if exact_rows is not None else None
+        N.check(N.lib().cmlb_svm_run(self.handle, x.data_ptr(), n, ldx, y.data_ptr(), dp, ep, stream))
+
+    def close(self):
+        if self.handle:
+            N.lib().cmlb_svm_destroy(self.handle)
+            self.handle = None
+
+
+_BUILDERS = {ForestSpec: _Forest, LinearSpec: _Linear, ScalerSpec: _Scaler, SVMSpec: _SVM}
 
 
 class DeviceProgram:
