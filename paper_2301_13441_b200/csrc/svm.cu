@@ -55,10 +55,11 @@ constexpr int STAGES = 2;
 constexpr int A_BYTES = BM * BK * 4;          // 16 KB per split half
 constexpr int B_BYTES = BN * BK * 4;          // 32 KB per split half
 constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-constexpr int THREADS = 320;
 constexpr int EPI_WARP0 = 6;
+constexpr int EPI_THREADS = 256;              // 8 warps: 2 per TMEM lane group, one column half each
+constexpr int THREADS = EPI_WARP0 * 32 + EPI_THREADS;
 constexpr int MAXC = 16;                      // classes handled by the fused epilogue
-constexpr int XR = 32;                        // rows per exact-path batch
+constexpr int XR = 8;                         // rows per exact-path batch (3 CTAs per SM)
 constexpr int XCH = 256;                      // support vectors per exact-path chunk
 
 struct Args {
@@ -67,10 +68,10 @@ struct Args {
   int F, KB, n_tiles, n_sv;
   const uint8_t* bsplit;   // [n_tiles][KB][big | small][BN x BK core-matrix layout]
   const float* ns;         // [n_tiles * BN] |sv|^2 (float64 rounded once)
-  const float* w;          // [n_tiles * BN][CP] coefficient of SV j toward class o (0 for its own class)
+  const float* w;          // [n_tiles * BN][CPS] coefficient of SV j toward class o (0 for its own class)
   const float* wmax;       // [n_tiles * BN] max_o |w|
   const int32_t* cls;      // [n_tiles * BN] class of SV j, -1 padding
-  const float* sv;         // [n_sv][F] (exact path)
+  const double* sv;        // [n_sv][F] float64 copy (exact path)
   const float* coef;       // [rows][n_sv] libsvm sv_coef (exact path)
   const float* intercept;  // [pairs]
   const double* classes;
@@ -105,9 +106,10 @@ __device__ __forceinline__ float kvalue_fast(const Args& a, float g, float nx, f
   const float de = 4.76837158203125e-07f * (nx + nsj);  // 2^-21
   if (a.kernel == CMLB_SVM_RBF) {
     // d2 = nx + ns - 2g: error 2 de (Gram) + one f32 rounding of ~(nx + ns);
-    // exp2f: <= 2 ulp; the f32 argument product: 1 ulp
+    // ex2.approx: ~2 ulp; the f32 argument product: 1 ulp of ~3
     const float d2 = fmaxf(fmaf(-2.0f, g, nx + nsj), 0.0f);
-    const float k = exp2f(-a.gamma * 1.4426950408889634f * d2);
+    float k;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(k) : "f"(-a.gamma * 1.4426950408889634f * d2));
     err = k * (a.gamma * (2.0f * de + 1.2e-7f * (nx + nsj)) + 6.0e-7f);
     return k;
   }
@@ -148,6 +150,7 @@ __device__ __forceinline__ void flush(const Args& a, int cur, const double (&acc
 
 template <int CP>
 __global__ void __launch_bounds__(THREADS, 1) svm_tc_kernel(const Args a) {
+  constexpr int CPS = (CP + 3) & ~3;  // w row stride (16-byte aligned rows)
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES], tfull_bar[2], tempty_bar[2];
   __shared__ uint32_t tmem_slot;
@@ -157,8 +160,8 @@ __global__ void __launch_bounds__(THREADS, 1) svm_tc_kernel(const Args a) {
   const int total = NT * KB;
 
   // epilogue tables (after the stages)
-  float* w_s = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);   // [BN][CP]
-  float* ns_s = w_s + BN * CP;
+  float* w_s = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);   // [BN][CPS]
+  float* ns_s = w_s + BN * CPS;
   float* wm_s = ns_s + BN;
   int32_t* cls_s = reinterpret_cast<int32_t*>(wm_s + BN);
 
@@ -169,7 +172,7 @@ __global__ void __launch_bounds__(THREADS, 1) svm_tc_kernel(const Args a) {
     }
     for (int b = 0; b < 2; ++b) {
       bar_init(&tfull_bar[b], 1);
-      bar_init(&tempty_bar[b], BM);
+      bar_init(&tempty_bar[b], EPI_THREADS);
     }
     bar_fence_init();
   }
@@ -260,10 +263,12 @@ __global__ void __launch_bounds__(THREADS, 1) svm_tc_kernel(const Args a) {
       }
     }
   } else {
-    // ---- epilogue: thread = row = TMEM lane -------------------------------
+    // ---- epilogue: thread = row = TMEM lane; two warps per lane group ---
+    const int e = warp - EPI_WARP0;          // 0..7
     const int eg = warp & 3;                 // TMEM lane group this warp may access
+    const int half = e >> 2;                 // which 128 columns of each tile
     const int r = eg * 32 + lane;
-    const int et = tid - EPI_WARP0 * 32;     // 0..127 (for cooperative table loads)
+    const int et = tid - EPI_WARP0 * 32;     // 0..255 (cooperative table loads)
     const int64_t row = row0 + r;
     const bool valid = row < a.n_rows;
     float nx = 0.0f;
@@ -277,58 +282,96 @@ __global__ void __launch_bounds__(THREADS, 1) svm_tc_kernel(const Args a) {
       nx = (float)s;
     }
     double acc[CP];
+    float pacc[CP];
 #pragma unroll
-    for (int o = 0; o < CP; ++o) acc[o] = 0.0;
+    for (int o = 0; o < CP; ++o) acc[o] = 0.0, pacc[o] = 0.0f;
     double dec[MAXC * (MAXC - 1) / 2];
     for (int p = 0; p < a.pairs; ++p) dec[p] = 0.0;
-    float err_sum = 0.0f;
+    float err_sum = 0.0f, err_sq = 0.0f;
     int cur = -1;
+    // fp32 partial sums over <= 8 columns, folded into the fp64 class sums:
+    // each adds at most 2^-21 sum|w K| of error, charged to the bound below
+    auto fold = [&]() {
+#pragma unroll
+      for (int o = 0; o < CP; ++o) {
+        acc[o] += (double)pacc[o];
+        pacc[o] = 0.0f;
+      }
+    };
     for (int t = 0; t < NT; ++t) {
       const int b = t & 1;
       // this tile's SV tables -> shared memory (previous tile's readers are done)
-      named_bar_sync(1, BM);
+      named_bar_sync(1, EPI_THREADS);
       {
         const int j0 = t * BN;
-        for (int i = et; i < BN * CP; i += BM) w_s[i] = __ldg(a.w + (size_t)j0 * CP + i);
-        for (int i = et; i < BN; i += BM) {
+        for (int i = et; i < BN * CPS; i += EPI_THREADS) w_s[i] = __ldg(a.w + (size_t)j0 * CPS + i);
+        for (int i = et; i < BN; i += EPI_THREADS) {
           ns_s[i] = __ldg(a.ns + j0 + i);
           wm_s[i] = __ldg(a.wmax + j0 + i);
           cls_s[i] = __ldg(a.cls + j0 + i);
         }
       }
-      named_bar_sync(1, BM);
+      named_bar_sync(1, EPI_THREADS);
       bar_wait(&tfull_bar[b], (t >> 1) & 1);
       tc_fence_after();
       const uint32_t taddr = tmem + ((uint32_t)(eg * 32) << 16) + (uint32_t)(b * BN);
-      for (int c0 = 0; c0 < BN; c0 += 32) {
+      for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 32) {
         uint32_t g[32];
         tmem_ld32(taddr + (uint32_t)c0, g);
-#pragma unroll 4
-        for (int jj = 0; jj < 32; ++jj) {
-          const int j = c0 + jj;
-          const int c = cls_s[j];
-          if (c != cur) {  // uniform: classes are contiguous
-            flush<CP>(a, cur, acc, dec);
 #pragma unroll
-            for (int o = 0; o < CP; ++o) acc[o] = 0.0;
-            cur = c;
+        for (int grp = 0; grp < 4; ++grp) {
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            const int j = c0 + grp * 8 + jj;
+            const int c = cls_s[j];
+            if (c != cur) {  // uniform: classes are contiguous
+              fold();
+              flush<CP>(a, cur, acc, dec);
+#pragma unroll
+              for (int o = 0; o < CP; ++o) acc[o] = 0.0;
+              cur = c;
+            }
+            float ek;
+            const float k = kvalue_fast(a, __uint_as_float(g[grp * 8 + jj]), nx, ns_s[j], ek);
+            const float we = wm_s[j] * (ek + 4.76837158203125e-07f * fabsf(k));
+            err_sum += we;
+            err_sq = fmaf(we, we, err_sq);
+            const float* wj = w_s + j * CPS;
+#pragma unroll
+            for (int o = 0; o < CP; ++o) pacc[o] = fmaf(wj[o], k, pacc[o]);
           }
-          float e;
-          const float k = kvalue_fast(a, __uint_as_float(g[jj]), nx, ns_s[j], e);
-          err_sum = fmaf(wm_s[j], e, err_sum);
-          const double kd = (double)k;
-          const float* wj = w_s + j * CP;
-#pragma unroll
-          for (int o = 0; o < CP; ++o) acc[o] = fma((double)wj[o], kd, acc[o]);
+          fold();
         }
       }
       tc_fence_before();
       bar_arrive(&tempty_bar[b]);
     }
     flush<CP>(a, cur, acc, dec);
+    // combine the two column halves of each row: half 1 hands its sums over
+    float* xch = reinterpret_cast<float*>(smem);  // the stages are idle now
+    double* xd = reinterpret_cast<double*>(xch);
+    named_bar_sync(1, EPI_THREADS);               // every epilogue thread is past its last tile
+    const int stride = a.pairs + 1;
+    if (half == 1) {
+      for (int p = 0; p < a.pairs; ++p) xd[r * stride + p] = dec[p];
+      xd[r * stride + a.pairs] = (double)err_sum;
+      xch[2 * BM * stride + r] = err_sq;
+    }
+    named_bar_sync(1, EPI_THREADS);
+    if (half == 1) return;
+    for (int p = 0; p < a.pairs; ++p) dec[p] += xd[r * stride + p];
+    err_sum += (float)xd[r * stride + a.pairs];
+    err_sq += xch[2 * BM * stride + r];
     if (valid) {
-      const float tol = 4.0f * err_sum + 1e-30f;
-      if (a.err_out) a.err_out[row] = err_sum;
+      // b_j = per-SV error bound.  E = sum b_j assumes every error aligned;
+      // the per-SV errors (dropped small*small products, tf32 roundings,
+      // fp32 partial sums) have data-dependent signs, so by Hoeffding
+      // P(|sum| >= 8 sigma) <= 2 exp(-32) with sigma^2 = sum b_j^2.  The
+      // vote threshold is tol = min(4 E, 8 sigma); measured errors stay
+      // below 0.2 sigma (tools/svm_error_probe.py).
+      const float bound = fminf(err_sum, 2.0f * sqrtf(err_sq));
+      const float tol = 4.0f * bound + 1e-30f;
+      if (a.err_out) a.err_out[row] = bound;
       bool exact = !(tol < 3.0e38f);
       if (a.is_svr) {
         const double v = dec[0] + (double)a.intercept[0];
@@ -362,9 +405,12 @@ __global__ void __launch_bounds__(THREADS, 1) svm_tc_kernel(const Args a) {
       }
       if (exact) a.queue[atomicAdd(a.queue_len, 1)] = (int32_t)row;
     }
+    return;
   }
-  __syncthreads();
+  // producers and the MMA warp: TMEM is released once the epilogue has
+  // drained the last accumulator (its final tempty arrival)
   if (warp == 5) {
+    if (NT >= 1) bar_wait(&tempty_bar[(NT - 1) & 1], ((NT - 1) >> 1) & 1);
     tc_fence_after();
     tmem_free(tmem, 512);
   }
@@ -375,30 +421,38 @@ __global__ void __launch_bounds__(THREADS, 1) svm_tc_kernel(const Args a) {
 // ---------------------------------------------------------------------------
 
 // OpenBLAS SkylakeX ddot order (oracle/svm_oracle.c: ddot_skx) for one
-// (row, SV) pair; xs = the row's features in shared memory, column stride XR.
-// RBF: the vectors are d = x - s (ddot(d, d)); otherwise ddot(x, s).
-__device__ double exact_dot(const float* xs, const float* s, int F, bool rbf) {
+// (row, SV) pair; xs = the row's features in shared memory (float64, column
+// stride XR), s = the SV in float64.  RBF: the vectors are d = x - s
+// (ddot(d, d)); otherwise ddot(x, s).
+__device__ double exact_dot(const double* xs, const double* s, int F, bool rbf) {
   const int n1 = F & -16, n32 = n1 & ~31;
   auto term = [&](int k, double acc) {
-    const double xv = (double)xs[k * XR], sv = (double)__ldg(s + k);
+    const double xv = xs[k * XR], sv = __ldg(s + k);
     if (rbf) {
       const double d = __dsub_rn(xv, sv);
       return fma(d, d, acc);
     }
     return fma(xv, sv, acc);
   };
+  // stream k in order: element k feeds lane k % 32 of the 4 x 8 AVX-512
+  // accumulators (32 independent FMA chains), then lane k % 16 of the
+  // 4 x 4 AVX2 ones
+  double a8[32];
+#pragma unroll
+  for (int u = 0; u < 32; ++u) a8[u] = 0.0;
+  int k = 0;
+  for (; k < n32; k += 32) {
+#pragma unroll
+    for (int u = 0; u < 32; ++u) a8[u] = term(k + u, a8[u]);
+  }
   double a4[16];
 #pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    const int aa = q >> 2, l = q & 3;
-    double lo = 0.0, hi = 0.0;
-    for (int i = 0; i < n32; i += 32) {
-      lo = term(i + 8 * aa + l, lo);
-      hi = term(i + 8 * aa + l + 4, hi);
-    }
-    double v = __dadd_rn(lo, hi);
-    for (int i = n32; i < n1; i += 16) v = term(i + 4 * aa + l, v);
-    a4[q] = v;
+  for (int aa = 0; aa < 4; ++aa)
+#pragma unroll
+    for (int l = 0; l < 4; ++l) a4[aa * 4 + l] = __dadd_rn(a8[aa * 8 + l], a8[aa * 8 + l + 4]);
+  for (; k < n1; k += 16) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) a4[u] = term(k + u, a4[u]);
   }
   double sl[4];
 #pragma unroll
@@ -408,7 +462,7 @@ __device__ double exact_dot(const float* xs, const float* s, int F, bool rbf) {
   return dot;
 }
 
-__device__ double exact_k(const Args& a, const float* xs, const float* s) {
+__device__ double exact_k(const Args& a, const double* xs, const double* s) {
   if (a.kernel == CMLB_SVM_RBF) return exp(__dmul_rn(-a.gamma64, exact_dot(xs, s, a.F, true)));
   const double dot = exact_dot(xs, s, a.F, false);
   if (a.kernel == CMLB_SVM_LINEAR) return dot;
@@ -426,31 +480,33 @@ constexpr int XTHREADS = 256;
 
 __global__ void __launch_bounds__(XTHREADS) svm_exact_kernel(const Args a, const int* n_sv_start) {
   extern __shared__ __align__(16) uint8_t xsm[];
-  float* xs = reinterpret_cast<float*>(xsm);                         // [F][XR]
-  double* kv = reinterpret_cast<double*>(xsm + (((size_t)a.F * XR * 4 + 15) & ~(size_t)15));  // [XCH][XR]
+  double* xs = reinterpret_cast<double*>(xsm);                       // [F][XR]
+  double* kv = xs + (size_t)a.F * XR;                                 // [XCH][XR]
   double* decs = kv + XCH * XR;                                      // [XR][pairs]
   __shared__ int32_t rows[XR];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nq = *a.queue_len;
   const int npairs = a.is_svr ? 1 : a.pairs;
   const int ntasks = XR * npairs;
-  const int TPT = (ntasks + XTHREADS - 1) / XTHREADS;  // (row, pair) tasks per thread, <= 15
+  const int TPT = (ntasks + XTHREADS - 1) / XTHREADS;  // (row, pair) tasks per thread, <= 4
   for (int b0 = blockIdx.x * XR; b0 < nq; b0 += gridDim.x * XR) {
     const int nb = min(XR, nq - b0);
     if (tid < XR) rows[tid] = tid < nb ? a.queue[b0 + tid] : -1;
     __syncthreads();
     for (int i = tid; i < a.F * XR; i += XTHREADS) {
       const int k = i / XR, r = i % XR;
-      xs[i] = rows[r] >= 0 ? __ldg(a.x + (int64_t)rows[r] * a.ldx + k) : 0.0f;
+      xs[i] = rows[r] >= 0 ? (double)__ldg(a.x + (int64_t)rows[r] * a.ldx + k) : 0.0;
     }
-    double sum[15];
-    for (int q = 0; q < 15; ++q) sum[q] = 0.0;
+    double sum[4];
+    for (int q = 0; q < 4; ++q) sum[q] = 0.0;
     __syncthreads();
     for (int j0 = 0; j0 < a.n_sv; j0 += XCH) {
       const int nj = min(XCH, a.n_sv - j0);
-      // K values of this chunk: warp w takes SVs w, w+8, ..; lane = row
-      for (int jj = warp; jj < nj; jj += XTHREADS / 32)
-        kv[jj * XR + lane] = exact_k(a, xs + lane, a.sv + (size_t)(j0 + jj) * a.F);
+      // K values of this chunk: each warp takes 32 / XR SVs at a time;
+      // lane % XR = row
+      constexpr int SPW = 32 / XR;
+      for (int jj = SPW * warp + lane / XR; jj < nj; jj += SPW * (XTHREADS / 32))
+        kv[jj * XR + (lane % XR)] = exact_k(a, xs + (lane % XR), a.sv + (size_t)(j0 + jj) * a.F);
       __syncthreads();
       // sequential decision sums in libsvm order, one (row, pair) per slot
       for (int q = 0; q < TPT; ++q) {
@@ -470,8 +526,10 @@ __global__ void __launch_bounds__(XTHREADS) svm_exact_kernel(const Args a, const
           const int lo_b = n_sv_start[cb], hi_b = n_sv_start[cb + 1];
           const float* c1 = a.coef + (size_t)(cb - 1) * a.n_sv;
           const float* c2 = a.coef + (size_t)ca * a.n_sv;
+#pragma unroll 8
           for (int j = max(lo_a, j0); j < min(hi_a, j0 + nj); ++j)
             s = __dadd_rn(s, __dmul_rn((double)__ldg(c1 + j), kv[(j - j0) * XR + r]));
+#pragma unroll 8
           for (int j = max(lo_b, j0); j < min(hi_b, j0 + nj); ++j)
             s = __dadd_rn(s, __dmul_rn((double)__ldg(c2 + j), kv[(j - j0) * XR + r]));
         }
@@ -564,7 +622,9 @@ static int make_svm(const cmlb_svm_desc* d, int device, cmlb_svm** out) {
   if (!svr && !d->n_support) return fail(CMLB_E_VALIDATION, "svc needs n_support");
   if (!out_dtype_ok(d->out_dtype)) return fail(CMLB_E_VALIDATION, "bad out_dtype");
   const int pairs = svr ? 1 : C * (C - 1) / 2;
-  const int CP = C <= 2 ? 2 : C <= 4 ? 4 : C <= 8 ? 8 : 16;
+  // accumulators per row: the smallest instantiated width >= C
+  const int CP = C <= 2 ? 2 : C <= 3 ? 3 : C <= 4 ? 4 : C <= 6 ? 6 : C <= 8 ? 8 : C <= 10 ? 10 : C <= 12 ? 12 : 16;
+  const int CPS = (CP + 3) & ~3;
   const int KB = (F + BK - 1) / BK, NT = (NSV + BN - 1) / BN, NP = NT * BN;
 
   cmlb_svm* m = new (std::nothrow) cmlb_svm();
@@ -588,7 +648,7 @@ static int make_svm(const cmlb_svm_desc* d, int device, cmlb_svm** out) {
     for (int j = start[c]; j < start[c + 1]; ++j) cls[j] = c;
   // per-SV coefficient toward each other class (libsvm: SV of class c in
   // pair (c, o) uses coef[o-1] if c < o, else coef[o])
-  std::vector<float> w((size_t)NP * CP, 0.0f), wmax(NP, 0.0f), ns(NP, 0.0f);
+  std::vector<float> w((size_t)NP * CPS, 0.0f), wmax(NP, 0.0f), ns(NP, 0.0f);
   for (int j = 0; j < NSV; ++j) {
     const int c = cls[j];
     for (int o = 0; o < C; ++o) {
@@ -596,7 +656,7 @@ static int make_svm(const cmlb_svm_desc* d, int device, cmlb_svm** out) {
       if (svr) v = d->dual_coef[j];
       else if (o == c) continue;
       else v = d->dual_coef[(size_t)(c < o ? o - 1 : o) * NSV + j];
-      w[(size_t)j * CP + o] = v;
+      w[(size_t)j * CPS + o] = v;
       wmax[j] = std::max(wmax[j], std::fabs(v));
     }
     double s = 0.0;
@@ -630,7 +690,7 @@ static int make_svm(const cmlb_svm_desc* d, int device, cmlb_svm** out) {
         }
       }
     }
-  std::vector<float> svv(d->support_vectors, d->support_vectors + (size_t)NSV * F);
+  std::vector<double> svv(d->support_vectors, d->support_vectors + (size_t)NSV * F);
   std::vector<float> coef(d->dual_coef, d->dual_coef + (size_t)(svr ? 1 : C - 1) * NSV);
   std::vector<float> ic(d->intercept, d->intercept + pairs);
   std::vector<double> classes(svr ? 1 : C, 0.0);
@@ -655,8 +715,8 @@ static int make_svm(const cmlb_svm_desc* d, int device, cmlb_svm** out) {
   a.out_dt = d->out_dtype;
   a.gamma = (float)d->gamma; a.coef0 = (float)d->coef0; a.gamma64 = d->gamma; a.coef064 = d->coef0;
   m->CP = CP;
-  m->tc_smem = (size_t)STAGES * STAGE_BYTES + (size_t)BN * CP * 4 + BN * 4 * 3;
-  m->x_smem = (((size_t)F * XR * 4 + 15) & ~(size_t)15) + (size_t)XCH * XR * 8 + (size_t)XR * pairs * 8;
+  m->tc_smem = (size_t)STAGES * STAGE_BYTES + (size_t)BN * CPS * 4 + BN * 4 * 3;
+  m->x_smem = (size_t)F * XR * 8 + (size_t)XCH * XR * 8 + (size_t)XR * pairs * 8;
   if (m->x_smem > 227 * 1024) {
     destroy_svm(m);
     return fail(CMLB_E_UNRESOLVED, "svm exact path: features x classes exceed shared memory");
@@ -673,6 +733,19 @@ static int launch_tc(const svm::Args& a, int64_t n, size_t smem, cudaStream_t s)
   CMLB_CUDA(cudaGetLastError());
   note_launch();
   return CMLB_OK;
+}
+
+static int launch_any(int CP, const svm::Args& a, int64_t n, size_t smem, cudaStream_t s) {
+  switch (CP) {
+    case 2: return launch_tc<2>(a, n, smem, s);
+    case 3: return launch_tc<3>(a, n, smem, s);
+    case 4: return launch_tc<4>(a, n, smem, s);
+    case 6: return launch_tc<6>(a, n, smem, s);
+    case 8: return launch_tc<8>(a, n, smem, s);
+    case 10: return launch_tc<10>(a, n, smem, s);
+    case 12: return launch_tc<12>(a, n, smem, s);
+    default: return launch_tc<16>(a, n, smem, s);
+  }
 }
 
 }  // namespace cmlb
@@ -706,12 +779,7 @@ int cmlb_svm_run(const cmlb_svm* m, const float* x, int64_t n_rows, int64_t ldx,
   int st = CMLB_OK;
   if (cudaMemsetAsync(a.queue_len, 0, sizeof(int32_t), s) != cudaSuccess) st = fail(CMLB_E_DEVICE, "memset");
   if (!st) {
-    switch (m->CP) {
-      case 2: st = launch_tc<2>(a, n_rows, m->tc_smem, s); break;
-      case 4: st = launch_tc<4>(a, n_rows, m->tc_smem, s); break;
-      case 8: st = launch_tc<8>(a, n_rows, m->tc_smem, s); break;
-      default: st = launch_tc<16>(a, n_rows, m->tc_smem, s); break;
-    }
+    st = launch_any(m->CP, a, n_rows, m->tc_smem, s);
   }
   if (!st) {
     cudaError_t e = cudaFuncSetAttribute(svm::svm_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -719,7 +787,7 @@ int cmlb_svm_run(const cmlb_svm* m, const float* x, int64_t n_rows, int64_t ldx,
     if (e != cudaSuccess) st = cuda_fail(e, "svm_exact smem");
   }
   if (!st) {
-    const int grid = std::max(1, std::min<int>(num_sms(m->device), (int)ceil_div(n_rows, svm::XR)));
+    const int grid = std::max(1, std::min<int>(3 * num_sms(m->device), (int)ceil_div(n_rows, svm::XR)));
     svm::svm_exact_kernel<<<grid, svm::XTHREADS, m->x_smem, s>>>(a, m->sv_start);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) st = cuda_fail(e, "svm_exact_kernel");
@@ -752,12 +820,7 @@ int cmlb_svm_debug_fast(const cmlb_svm* m, const float* x, int64_t n_rows, int64
   a.queue = a.queue_len + 4;
   CMLB_CUDA(cudaMemsetAsync(a.queue_len, 0, sizeof(int32_t), s));
   int st;
-  switch (m->CP) {
-    case 2: st = launch_tc<2>(a, n_rows, m->tc_smem, s); break;
-    case 4: st = launch_tc<4>(a, n_rows, m->tc_smem, s); break;
-    case 8: st = launch_tc<8>(a, n_rows, m->tc_smem, s); break;
-    default: st = launch_tc<16>(a, n_rows, m->tc_smem, s); break;
-  }
+  st = launch_any(m->CP, a, n_rows, m->tc_smem, s);
   cudaFreeAsync(scratch, s);
   return st;
 }
