@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define CMLB_ABI_VERSION 1
+#define CMLB_ABI_VERSION 2
 
 enum cmlb_status {
   CMLB_OK = 0,
@@ -73,6 +73,28 @@ enum cmlb_tail {
   CMLB_TAIL_SIGMOID = 2   /* float64 sigmoid -> float32 > 0.5 -> label (convert.py:217-222) */
 };
 
+/* Fused preprocessing ("prologue"): model input column f is computed from a
+ * raw input column as the reference scaler / scikit-learn one-hot encoder
+ * would (float32, pinned rounding: convert.py:255-284), so a pipeline
+ * scaler -> one-hot -> model runs as ONE kernel reading the raw rows.  Used
+ * by the forest, linear and SVM programs (optional) and by the standalone
+ * column program below. */
+enum cmlb_col_op {
+  CMLB_COL_COPY = 0,      /* x                                                  */
+  CMLB_COL_SUB_DIV = 1,   /* (x - a) / b       StandardScaler, RobustScaler     */
+  CMLB_COL_DIV = 2,       /* x / a             MaxAbsScaler                     */
+  CMLB_COL_MUL_ADD = 3,   /* x * a + b, two roundings   MinMaxScaler            */
+  CMLB_COL_GREATER = 4,   /* x > a ? 1 : 0     Binarizer                        */
+  CMLB_COL_EQUAL = 5      /* x == a ? 1 : 0    OneHotEncoder indicator column   */
+};
+
+typedef struct cmlb_column_op {
+  int32_t src;            /* raw input column */
+  int32_t op;             /* cmlb_col_op */
+  float a;
+  float b;
+} cmlb_column_op;
+
 enum cmlb_forest_variant {
   CMLB_FOREST_AUTO = 0,        /* pick by (depth, trees, features) from the measured table */
   CMLB_FOREST_PERFECT = 1,     /* perfect-padded trees staged in shared memory */
@@ -101,6 +123,8 @@ typedef struct cmlb_forest_desc {
   int32_t out_dtype;            /* cmlb_out_dtype */
   int32_t dense_selector;       /* 1: replicate dense W1 (0*inf = NaN) semantics */
   int32_t variant;              /* cmlb_forest_variant */
+  const cmlb_column_op* prologue; /* optional [n_features]: feature f = op(x[src]) (ABI 2) */
+  int32_t n_inputs;             /* raw input columns when prologue != NULL */
 } cmlb_forest_desc;
 
 typedef struct cmlb_forest cmlb_forest;
@@ -152,6 +176,8 @@ typedef struct cmlb_linear_desc {
   int32_t n_classes;
   int32_t out_dtype;
   int32_t sparse_coef;      /* 1: CSR weight semantics (skip zero weights, kernels.py:115-123) */
+  const cmlb_column_op* prologue; /* optional [n_features] (ABI 2) */
+  int32_t n_inputs;
 } cmlb_linear_desc;
 
 typedef struct cmlb_linear cmlb_linear;
@@ -214,6 +240,8 @@ typedef struct cmlb_svm_desc {
   int32_t n_classes;           /* >= 2 for svc, 0 for svr */
   const double* classes;       /* svc labels */
   int32_t out_dtype;           /* svc: label dtype; svr: CMLB_OUT_F32 */
+  const cmlb_column_op* prologue; /* optional [n_features] */
+  int32_t n_inputs;
 } cmlb_svm_desc;
 
 typedef struct cmlb_svm cmlb_svm;
@@ -226,6 +254,32 @@ int cmlb_svm_create(const cmlb_svm_desc* desc, int device, cmlb_svm** out);
 int cmlb_svm_run(const cmlb_svm* m, const float* x, int64_t n_rows, int64_t ldx, void* y, double* decision,
                  int32_t* exact_rows, void* stream);
 void cmlb_svm_destroy(cmlb_svm* m);
+
+/* ------------------------------------------------------------------------ *
+ * Column transform: OneHotEncoder / ColumnTransformer / elementwise scalers
+ * as one gather-transform kernel (y[:, f] = op_f(x[:, src_f])), plus the
+ * OneHotEncoder(handle_unknown='error') membership check: `checks` lists raw
+ * columns whose value must be one of its sorted category list.
+ * ------------------------------------------------------------------------ */
+
+typedef struct cmlb_columns_desc {
+  int32_t n_inputs;
+  int32_t n_outputs;
+  const cmlb_column_op* ops;     /* [n_outputs] */
+  int32_t n_checks;
+  const int32_t* check_col;      /* [n_checks] raw column */
+  const int64_t* check_offset;   /* [n_checks + 1] into check_values */
+  const float* check_values;     /* ascending categories per checked column */
+} cmlb_columns_desc;
+
+typedef struct cmlb_columns cmlb_columns;
+int cmlb_columns_create(const cmlb_columns_desc* desc, int device, cmlb_columns** out);
+/* y: device float32 [n_rows][n_outputs] (NULL: check only).  bad_row:
+ * optional device int64, receives the first row holding an unknown category
+ * or -1 (the caller raises, as OneHotEncoder.transform does). */
+int cmlb_columns_run(const cmlb_columns* c, const float* x, int64_t n_rows, int64_t ldx, float* y,
+                     int64_t* bad_row, void* stream);
+void cmlb_columns_destroy(cmlb_columns* c);
 
 #ifdef __cplusplus
 }

@@ -21,6 +21,10 @@ c_i32, c_i64, c_f32, c_f64, c_vp = C.c_int32, C.c_int64, C.c_float, C.c_double, 
 P = C.POINTER
 
 
+class ColumnOp(C.Structure):
+    _fields_ = [("src", c_i32), ("op", c_i32), ("a", c_f32), ("b", c_f32)]
+
+
 class ForestDesc(C.Structure):
     _fields_ = [
         ("n_trees", c_i32), ("n_features", c_i32), ("n_outputs", c_i32),
@@ -30,6 +34,7 @@ class ForestDesc(C.Structure):
         ("aggregation", c_i32), ("tail", c_i32), ("learning_rate", c_f32), ("base_score", c_f32),
         ("classes", P(c_f64)), ("n_classes", c_i32), ("out_dtype", c_i32),
         ("dense_selector", c_i32), ("variant", c_i32),
+        ("prologue", c_vp), ("n_inputs", c_i32),
     ]
 
 
@@ -37,7 +42,7 @@ class LinearDesc(C.Structure):
     _fields_ = [
         ("n_features", c_i32), ("n_outputs", c_i32), ("coef", P(c_f32)), ("intercept", P(c_f32)),
         ("tail", c_i32), ("classes", P(c_f64)), ("n_classes", c_i32), ("out_dtype", c_i32),
-        ("sparse_coef", c_i32),
+        ("sparse_coef", c_i32), ("prologue", c_vp), ("n_inputs", c_i32),
     ]
 
 
@@ -52,7 +57,14 @@ class SVMDesc(C.Structure):
         ("n_features", c_i32), ("n_sv", c_i32), ("kernel", c_i32), ("degree", c_i32),
         ("gamma", c_f64), ("coef0", c_f64), ("support_vectors", P(c_f32)), ("dual_coef", P(c_f32)),
         ("intercept", P(c_f32)), ("n_support", P(c_i32)), ("n_classes", c_i32), ("classes", P(c_f64)),
-        ("out_dtype", c_i32),
+        ("out_dtype", c_i32), ("prologue", c_vp), ("n_inputs", c_i32),
+    ]
+
+
+class ColumnsDesc(C.Structure):
+    _fields_ = [
+        ("n_inputs", c_i32), ("n_outputs", c_i32), ("ops", c_vp), ("n_checks", c_i32),
+        ("check_col", P(c_i32)), ("check_offset", P(c_i64)), ("check_values", P(c_f32)),
     ]
 
 
@@ -89,6 +101,9 @@ SIGNATURES = {
     "cmlb_svm_run": (C.c_int, [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "cmlb_svm_destroy": (None, [c_vp]),
     "cmlb_svm_debug_fast": (C.c_int, [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "cmlb_columns_create": (C.c_int, [P(ColumnsDesc), C.c_int, P(c_vp)]),
+    "cmlb_columns_run": (C.c_int, [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp]),
+    "cmlb_columns_destroy": (None, [c_vp]),
     "cmlb_debug_pairwise_schedule": (C.c_int, [c_i64, P(C.c_uint32)]),
 }
 

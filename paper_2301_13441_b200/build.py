@@ -16,7 +16,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libcmlb.so")
-SOURCES = ["capi.cu", "forest.cu", "linear.cu", "scaler.cu", "svm.cu"]
+SOURCES = ["capi.cu", "forest.cu", "linear.cu", "scaler.cu", "svm.cu", "cols.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

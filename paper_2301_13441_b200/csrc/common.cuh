@@ -77,6 +77,25 @@ __device__ __forceinline__ void store_out(void* y, int64_t i, int dt, double v) 
   }
 }
 
+// Fused preprocessing: model feature f = op(x[src]) with the reference
+// scalers' float32 rounding (convert.py:255-284) and OneHotEncoder's
+// indicator (cmlb.h: cmlb_column_op).  A null prologue reads x[f].
+__device__ __forceinline__ float col_apply(int op, float v, float a, float b) {
+  switch (op) {
+    case CMLB_COL_COPY: return v;
+    case CMLB_COL_SUB_DIV: return __fdiv_rn(__fsub_rn(v, a), b);
+    case CMLB_COL_DIV: return __fdiv_rn(v, a);
+    case CMLB_COL_MUL_ADD: return __fadd_rn(__fmul_rn(v, a), b);
+    case CMLB_COL_GREATER: return v > a ? 1.0f : 0.0f;
+    default: return v == a ? 1.0f : 0.0f;  // CMLB_COL_EQUAL
+  }
+}
+__device__ __forceinline__ float load_col(const cmlb_column_op* pro, const float* row, int f) {
+  if (pro == nullptr) return __ldg(row + f);
+  const int4 w = __ldg(reinterpret_cast<const int4*>(pro) + f);
+  return col_apply(w.y, __ldg(row + w.x), __int_as_float(w.z), __int_as_float(w.w));
+}
+
 inline int out_dtype_ok(int dt) { return dt >= CMLB_OUT_BOOL && dt <= CMLB_OUT_F32; }
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -117,6 +117,7 @@ constexpr int SMAX = 10;  // register stack slots for the pairwise replay
 
 struct ForestArgs {
   const float* x;
+  const cmlb_column_op* pro;  // fused preprocessing (nullable)
   int64_t n_rows;
   int64_t ldx;
   void* y;
@@ -334,7 +335,7 @@ __global__ void __launch_bounds__(NT) forest_kernel(const ForestArgs a) {
       const int64_t row = tile + r;
       const float* src = a.x + row * a.ldx;
       if (row < a.n_rows) {
-        for (int f = 0; f < F; ++f) xs[f * ROWS + r] = __ldg(src + f);
+        for (int f = 0; f < F; ++f) xs[f * ROWS + r] = load_col(a.pro, src, f);
         if (a.dense_sel) poison_row(xs, ROWS, F, r);
       } else {
         for (int f = 0; f < F; ++f) xs[f * ROWS + r] = 0.0f;
@@ -361,14 +362,14 @@ __global__ void __launch_bounds__(NT) forest_kernel(const ForestArgs a) {
     nbad[k] = 0;
     if (!XS && a.dense_sel && rowk[k] < a.n_rows) {
       const float* src = a.x + rowk[k] * a.ldx;
-      for (int f = 0; f < F; ++f) nbad[k] += !isfinite(__ldg(src + f));
+      for (int f = 0; f < F; ++f) nbad[k] += !isfinite(load_col(a.pro, src, f));
     }
   }
 
   auto xval = [&](int k, int f) -> float {
     if (XS) return xs[f * ROWS + tid + k * NT];
     if (rowk[k] >= a.n_rows) return 0.0f;
-    float v = __ldg(a.x + rowk[k] * a.ldx + f);
+    float v = load_col(a.pro, a.x + rowk[k] * a.ldx, f);
     if (nbad[k] && (nbad[k] >= 2 || isfinite(v))) v = __int_as_float(0x7fc00000);
     return v;
   };
@@ -616,7 +617,7 @@ __global__ void __launch_bounds__(NTT, 1) forest_ranked_kernel(const ForestArgs 
     nbad[k] = 0;
     if (a.dense_sel && rowk[k] < a.n_rows) {
       const float* src = a.x + rowk[k] * a.ldx;
-      for (int f = 0; f < F; ++f) nbad[k] += !isfinite(__ldg(src + f));
+      for (int f = 0; f < F; ++f) nbad[k] += !isfinite(load_col(a.pro, src, f));
     }
   }
 
@@ -651,7 +652,7 @@ __global__ void __launch_bounds__(NTT, 1) forest_ranked_kernel(const ForestArgs 
       for (int j = 0; j < 8; ++j) {
         float v = 0.0f;
         if (rowk[k] < a.n_rows && g0 + j < F) {
-          v = __ldg(src + g0 + j);
+          v = load_col(a.pro, src, g0 + j);
           if (nbad[k] && (nbad[k] >= 2 || isfinite(v))) v = __int_as_float(0x7fc00000);
         }
         xv[k][j] = v;
@@ -835,7 +836,7 @@ __global__ void __launch_bounds__(MMA_M, 1) forest_mma_kernel(const ForestArgs a
   // ---- rows -> shared memory (feature-major), dense-selector poisoning ---
   {
     const float* src = a.x + row * a.ldx;
-    for (int f = 0; f < F; ++f) xs[f * MMA_M + tid] = valid ? __ldg(src + f) : 0.0f;
+    for (int f = 0; f < F; ++f) xs[f * MMA_M + tid] = valid ? load_col(a.pro, src, f) : 0.0f;
     if (a.dense_sel && valid) poison_row(xs, MMA_M, F, tid);
   }
   if (tid == 0) {
@@ -983,7 +984,10 @@ struct cmlb_forest {
   int32_t* moff = nullptr;
   int ntt = 256, stage_cap = 0, node_off_bytes = 0, rcfg = 0, stage_off = 0, stage_bufs = 2;
   int mma_k = 0, mma_n = 0, mma_feat_off = 0, mma_thr_off = 0, mma_pay_off = 0;
+  cmlb_column_op* pro = nullptr;  // fused preprocessing
+  int n_inputs = 0;
   ~cmlb_forest() {
+    cudaFree(pro);
     cudaFree(blob); cudaFree(slot_leaf); cudaFree(gnode); cudaFree(node_off);
     cudaFree(gpay); cudaFree(leaf_off); cudaFree(sched); cudaFree(classes);
     cudaFree(uthr); cudaFree(uoff); cudaFree(umap); cudaFree(moff);
@@ -1257,6 +1261,17 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
   f->n_classes = d->n_classes;
   const bool pairwise = f->C == 1 && f->agg != CMLB_AGG_NONE;
   f->rpt = rows_per_thread(f->CT, pairwise);
+  f->n_inputs = f->F;
+  if (d->prologue) {
+    if (d->n_inputs <= 0) return fail(CMLB_E_VALIDATION, "prologue needs n_inputs > 0");
+    for (int k = 0; k < f->F; ++k) {
+      const cmlb_column_op& o = d->prologue[k];
+      if (o.src < 0 || o.src >= d->n_inputs || o.op < CMLB_COL_COPY || o.op > CMLB_COL_EQUAL)
+        return fail(CMLB_E_VALIDATION, "bad prologue column op");
+    }
+    f->n_inputs = d->n_inputs;
+    if (int s = upload(&f->pro, d->prologue, (size_t)f->F)) return s;
+  }
 
   int D = 0;
   for (int t = 0; t < f->T; ++t) D = std::max(D, tree_depth(d, t));
@@ -1476,12 +1491,13 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
 static int run_forest(const cmlb_forest* f, const float* x, int64_t n_rows, int64_t ldx, void* y,
                       int32_t* leaf_out, double* partial, void* stream) {
   if (!f) return fail(CMLB_E_VALIDATION, "null forest");
-  if (n_rows < 0 || ldx < f->F) return fail(CMLB_E_INPUT, "bad input extents");
+  if (n_rows < 0 || ldx < f->n_inputs) return fail(CMLB_E_INPUT, "bad input extents");
   if (n_rows == 0) return CMLB_OK;
   if (!x || (!y && !partial)) return fail(CMLB_E_VALIDATION, "null input/output pointer");
   DeviceGuard guard(f->device);
   ForestArgs a{};
   a.x = x; a.n_rows = n_rows; a.ldx = ldx; a.y = y; a.leaf_out = leaf_out; a.partial = partial;
+  a.pro = f->pro;
   a.T = f->T; a.F = f->F; a.C = f->C; a.depth = f->depth; a.ni = f->ni; a.ns = f->ns;
   a.tree_bytes = f->tree_bytes; a.chunk_trees = f->chunk_trees; a.rows_per_cta = NT * f->rpt;
   a.blob = f->blob; a.slot_leaf = f->slot_leaf; a.gnode = f->gnode; a.node_off = f->node_off;

@@ -30,6 +30,7 @@ struct LinearArgs {
   const float* w;        // [C][F]
   const float* b;        // [C]
   const double* classes;
+  const cmlb_column_op* pro;  // fused preprocessing (nullable)
   int F, C, tail, out_dt, sparse;
 };
 
@@ -96,7 +97,13 @@ __global__ void __launch_bounds__(LNT) linear_kernel(const LinearArgs a) {
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
       if (row < a.n_rows) {
         const float* src = a.x + row * a.ldx + k;
-        if (vec && k + 4 <= F) {
+        if (a.pro) {
+          const float* rp = a.x + row * a.ldx;
+          if (k < F) v.x = load_col(a.pro, rp, k);
+          if (k + 1 < F) v.y = load_col(a.pro, rp, k + 1);
+          if (k + 2 < F) v.z = load_col(a.pro, rp, k + 2);
+          if (k + 3 < F) v.w = load_col(a.pro, rp, k + 3);
+        } else if (vec && k + 4 <= F) {
           v = __ldg(reinterpret_cast<const float4*>(src));
         } else {
           if (k < F) v.x = __ldg(src);
@@ -224,11 +231,12 @@ static LinFn linear_for(int C, int* rows) {
 }  // namespace cmlb
 
 struct cmlb_linear {
-  int device = 0, F = 0, C = 0, tail = 0, out_dt = 4, sparse = 0;
+  int device = 0, F = 0, C = 0, tail = 0, out_dt = 4, sparse = 0, n_inputs = 0;
   float* w = nullptr;
   float* b = nullptr;
   double* classes = nullptr;
-  ~cmlb_linear() { cudaFree(w); cudaFree(b); cudaFree(classes); }
+  cmlb_column_op* pro = nullptr;
+  ~cmlb_linear() { cudaFree(w); cudaFree(b); cudaFree(classes); cudaFree(pro); }
 };
 
 extern "C" {
@@ -256,6 +264,18 @@ int cmlb_linear_create(const cmlb_linear_desc* d, int device, cmlb_linear** out)
   CMLB_CUDA(cudaMalloc(&m->classes, nc * sizeof(double)));
   if (d->n_classes > 0)
     CMLB_CUDA(cudaMemcpy(m->classes, d->classes, nc * sizeof(double), cudaMemcpyHostToDevice));
+  m->n_inputs = m->F;
+  if (d->prologue) {
+    if (d->n_inputs <= 0) return fail(CMLB_E_VALIDATION, "prologue needs n_inputs > 0");
+    for (int k = 0; k < m->F; ++k) {
+      const cmlb_column_op& o = d->prologue[k];
+      if (o.src < 0 || o.src >= d->n_inputs || o.op < CMLB_COL_COPY || o.op > CMLB_COL_EQUAL)
+        return fail(CMLB_E_VALIDATION, "bad prologue column op");
+    }
+    m->n_inputs = d->n_inputs;
+    CMLB_CUDA(cudaMalloc(&m->pro, (size_t)m->F * sizeof(cmlb_column_op)));
+    CMLB_CUDA(cudaMemcpy(m->pro, d->prologue, (size_t)m->F * sizeof(cmlb_column_op), cudaMemcpyHostToDevice));
+  }
   *out = m.release();
   return CMLB_OK;
 }
@@ -264,10 +284,11 @@ int cmlb_linear_run(const cmlb_linear* m, const float* x, int64_t n_rows, int64_
                     void* stream) {
   using namespace cmlb;
   if (!m) return fail(CMLB_E_VALIDATION, "null linear model");
-  if (n_rows < 0 || ldx < m->F) return fail(CMLB_E_INPUT, "bad input extents");
+  if (n_rows < 0 || ldx < m->n_inputs) return fail(CMLB_E_INPUT, "bad input extents");
   if (n_rows == 0) return CMLB_OK;
   DeviceGuard guard(m->device);
   LinearArgs a{};
+  a.pro = m->pro;
   a.x = x; a.n_rows = n_rows; a.ldx = ldx; a.y = y; a.w = m->w; a.b = m->b; a.classes = m->classes;
   a.F = m->F; a.C = m->C; a.tail = m->tail; a.out_dt = m->out_dt; a.sparse = m->sparse;
   int rows = 0;

@@ -82,6 +82,7 @@ struct Args {
   double* dec_out;
   float* err_out;          // debug: per-row error bound E (nullable)
   int no_exact;            // debug: write every row from the fast path
+  const cmlb_column_op* pro;  // fused preprocessing (nullable)
   int32_t* queue;          // [n_rows] rows for the exact path
   int32_t* queue_len;
 };
@@ -199,7 +200,12 @@ __global__ void __launch_bounds__(THREADS, 1) svm_tc_kernel(const Args a) {
         const int k = k0 + 4 * c;
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
         if (valid) {
-          if (a.vec_x && k + 3 < a.F) {
+          if (a.pro) {
+            if (k < a.F) v.x = load_col(a.pro, src, k);
+            if (k + 1 < a.F) v.y = load_col(a.pro, src, k + 1);
+            if (k + 2 < a.F) v.z = load_col(a.pro, src, k + 2);
+            if (k + 3 < a.F) v.w = load_col(a.pro, src, k + 3);
+          } else if (a.vec_x && k + 3 < a.F) {
             v = __ldg(reinterpret_cast<const float4*>(src + k));
           } else {
             if (k < a.F) v.x = __ldg(src + k);
@@ -276,7 +282,7 @@ __global__ void __launch_bounds__(THREADS, 1) svm_tc_kernel(const Args a) {
       const float* src = a.x + row * a.ldx;
       double s = 0.0;
       for (int k = 0; k < a.F; ++k) {
-        const double v = (double)__ldg(src + k);
+        const double v = (double)load_col(a.pro, src, k);
         s = fma(v, v, s);
       }
       nx = (float)s;
@@ -495,7 +501,7 @@ __global__ void __launch_bounds__(XTHREADS) svm_exact_kernel(const Args a, const
     __syncthreads();
     for (int i = tid; i < a.F * XR; i += XTHREADS) {
       const int k = i / XR, r = i % XR;
-      xs[i] = rows[r] >= 0 ? (double)__ldg(a.x + (int64_t)rows[r] * a.ldx + k) : 0.0;
+      xs[i] = rows[r] >= 0 ? (double)load_col(a.pro, a.x + (int64_t)rows[r] * a.ldx, k) : 0.0;
     }
     double sum[4];
     for (int q = 0; q < 4; ++q) sum[q] = 0.0;
@@ -579,6 +585,7 @@ __global__ void __launch_bounds__(XTHREADS) svm_exact_kernel(const Args a, const
 
 struct cmlb_svm_impl {
   int device;
+  int n_inputs;
   svm::Args a;
   int CP;
   std::vector<void*> bufs;
@@ -715,6 +722,24 @@ static int make_svm(const cmlb_svm_desc* d, int device, cmlb_svm** out) {
   a.out_dt = d->out_dtype;
   a.gamma = (float)d->gamma; a.coef0 = (float)d->coef0; a.gamma64 = d->gamma; a.coef064 = d->coef0;
   m->CP = CP;
+  m->n_inputs = F;
+  if (d->prologue) {
+    if (d->n_inputs <= 0) {
+      destroy_svm(m);
+      return fail(CMLB_E_VALIDATION, "prologue needs n_inputs > 0");
+    }
+    std::vector<cmlb_column_op> pro(d->prologue, d->prologue + F);
+    for (const auto& o : pro)
+      if (o.src < 0 || o.src >= d->n_inputs || o.op < CMLB_COL_COPY || o.op > CMLB_COL_EQUAL) {
+        destroy_svm(m);
+        return fail(CMLB_E_VALIDATION, "bad prologue column op");
+      }
+    if ((st = upload(m, pro, &a.pro))) {
+      destroy_svm(m);
+      return st;
+    }
+    m->n_inputs = d->n_inputs;
+  }
   m->tc_smem = (size_t)STAGES * STAGE_BYTES + (size_t)BN * CPS * 4 + BN * 4 * 3;
   m->x_smem = (size_t)F * XR * 8 + (size_t)XCH * XR * 8 + (size_t)XR * pairs * 8;
   if (m->x_smem > 227 * 1024) {
@@ -764,7 +789,7 @@ int cmlb_svm_run(const cmlb_svm* m, const float* x, int64_t n_rows, int64_t ldx,
                  int32_t* exact_rows, void* stream) {
   using namespace cmlb;
   if (!m) return fail(CMLB_E_VALIDATION, "null svm");
-  if (n_rows < 0 || ldx < m->a.F) return fail(CMLB_E_INPUT, "bad svm input shape");
+  if (n_rows < 0 || ldx < m->n_inputs) return fail(CMLB_E_INPUT, "bad svm input shape");
   if (n_rows > INT32_MAX) return fail(CMLB_E_INPUT, "svm batch exceeds 2^31 rows");
   if (n_rows == 0) return CMLB_OK;
   DeviceGuard g(m->device);

@@ -67,6 +67,12 @@ class ForestSpec:
     classes: tuple = ()
     out_dtype: str = "float32"
     dense_selector: bool = False
+    prologue: object = None        # fuse.COL_DTYPE ops over the raw input (fused preprocessing)
+    n_inputs: int = 0
+
+    @property
+    def in_cols(self) -> int:
+        return self.n_inputs if self.prologue is not None else self.n_features
 
     @property
     def out_cols(self) -> int:
@@ -94,10 +100,16 @@ class LinearSpec:
     classes: tuple = ()
     out_dtype: str = "float32"
     sparse_coef: bool = False
+    prologue: object = None
+    n_inputs: int = 0
 
     @property
     def n_features(self) -> int:
         return int(self.coef.shape[1])
+
+    @property
+    def in_cols(self) -> int:
+        return self.n_inputs if self.prologue is not None else self.n_features
 
     @property
     def out_cols(self) -> int:
@@ -124,10 +136,16 @@ class SVMSpec:
 
     model: object
     out_dtype: str = "float32"
+    prologue: object = None
+    n_inputs: int = 0
 
     @property
     def n_features(self) -> int:
         return self.model.n_features
+
+    @property
+    def in_cols(self) -> int:
+        return self.n_inputs if self.prologue is not None else self.n_features
 
     @property
     def out_cols(self) -> int:

@@ -20,8 +20,20 @@ import torch
 
 from . import _native as N
 from .dtypes import OUT_CODE
-from .errors import DeviceError, InputMismatch
+from .errors import DeviceError, InputMismatch, ValidationError
+from .fuse import ColumnsSpec
 from .lower import ForestSpec, LinearSpec, ProgramSpec, ScalerSpec, SVMSpec
+
+
+def _prologue(spec, desc):
+    """Attach a stage's fused-preprocessing ops to its descriptor; returns the
+    buffer the caller keeps alive until create() returns."""
+    if getattr(spec, "prologue", None) is None:
+        desc.prologue, desc.n_inputs = None, 0
+        return None
+    ops = np.ascontiguousarray(spec.prologue)
+    desc.prologue, desc.n_inputs = ops.ctypes.data, int(spec.n_inputs)
+    return ops
 
 TORCH_DTYPE = {
     "bool": torch.uint8, "int8": torch.int8, "int16": torch.int16, "int32": torch.int32,
@@ -69,9 +81,10 @@ class _Forest:
         d.out_dtype = OUT_CODE[spec.out_dtype]
         d.dense_selector = int(spec.dense_selector)
         d.variant = variant
+        pro = _prologue(spec, d)
         h = N.c_vp()
         N.check(N.lib().cmlb_forest_create(C.byref(d), device, C.byref(h)))
-        del keep
+        del keep, pro
         self.handle = h
         self.n_trees = T
 
@@ -107,8 +120,10 @@ class _Linear:
         d.classes, d.n_classes = N.ptr(classes, N.c_f64), len(spec.classes)
         d.out_dtype = OUT_CODE[spec.out_dtype]
         d.sparse_coef = int(spec.sparse_coef)
+        pro = _prologue(spec, d)
         h = N.c_vp()
         N.check(N.lib().cmlb_linear_create(C.byref(d), device, C.byref(h)))
+        del pro
         self.handle = h
 
     def run(self, x, y, n, ldx, stream, leaf_out=None):
@@ -159,8 +174,10 @@ class _SVM:
         d.n_classes = 0 if svr else len(m.classes)
         d.classes = N.ptr(classes, N.c_f64)
         d.out_dtype = OUT_CODE[spec.out_dtype]
+        pro = _prologue(spec, d)
         h = N.c_vp()
         N.check(N.lib().cmlb_svm_create(C.byref(d), device, C.byref(h)))
+        del pro
         self.handle = h
         self.pairs = 1 if svr else len(m.classes) * (len(m.classes) - 1) // 2
 
@@ -175,7 +192,47 @@ class _SVM:
             self.handle = None
 
 
-_BUILDERS = {ForestSpec: _Forest, LinearSpec: _Linear, ScalerSpec: _Scaler, SVMSpec: _SVM}
+class _Columns:
+    """One-hot / column-transformer / scaler column map; check-only when its ops
+    run fused inside the next stage."""
+
+    def __init__(self, spec: ColumnsSpec, device: int):
+        self.spec = spec
+        ops = np.ascontiguousarray(spec.ops)
+        cols = np.ascontiguousarray([c for c, _ in spec.checks] or [0], np.int32)
+        off = np.zeros(len(spec.checks) + 1, np.int64)
+        for i, (_, v) in enumerate(spec.checks):
+            off[i + 1] = off[i] + len(v)
+        vals = np.ascontiguousarray(np.concatenate([v for _, v in spec.checks]) if spec.checks else np.zeros(1),
+                                    np.float32)
+        d = N.ColumnsDesc()
+        d.n_inputs, d.n_outputs, d.ops = spec.n_inputs, int(ops.shape[0]), ops.ctypes.data
+        d.n_checks = len(spec.checks)
+        d.check_col, d.check_offset, d.check_values = N.ptr(cols, N.c_i32), N.ptr(off, N.c_i64), N.ptr(vals, N.c_f32)
+        h = N.c_vp()
+        N.check(N.lib().cmlb_columns_create(C.byref(d), device, C.byref(h)))
+        self.handle = h
+
+    def run(self, x, y, n, ldx, stream, leaf_out=None, bad=None):
+        yp = y.data_ptr() if y is not None else None
+        bp = bad.data_ptr() if bad is not None else None
+        N.check(N.lib().cmlb_columns_run(self.handle, x.data_ptr(), n, ldx, yp, bp, stream))
+
+    def close(self):
+        if self.handle:
+            N.lib().cmlb_columns_destroy(self.handle)
+            self.handle = None
+
+
+def raise_unknown_category(bad: torch.Tensor, x_rows_offset: int = 0) -> None:
+    """Raise as OneHotEncoder.transform does when a checked row held an unknown value."""
+    r = int(bad.item())
+    if r >= 0:
+        raise ValidationError(f"Found unknown categories in row {r + x_rows_offset} during transform "
+                              "(OneHotEncoder handle_unknown='error')")
+
+
+_BUILDERS = {ForestSpec: _Forest, LinearSpec: _Linear, ScalerSpec: _Scaler, SVMSpec: _SVM, ColumnsSpec: _Columns}
 
 
 class DeviceProgram:
@@ -206,8 +263,12 @@ class DeviceProgram:
             raise InputMismatch(f"input dtype {x.dtype} != float32")
 
     def run(self, x: torch.Tensor, out: torch.Tensor | None = None, stream=None,
-            leaf_out: torch.Tensor | None = None) -> torch.Tensor:
-        """Run on a CUDA tensor (N, F) float32 with unit column stride."""
+            leaf_out: torch.Tensor | None = None, bad: torch.Tensor | None = None) -> torch.Tensor:
+        """Run on a CUDA tensor (N, F) float32 with unit column stride.
+
+        One-hot membership checks write the first offending row into ``bad``
+        (device int64) when given -- the caller raises after its own sync;
+        otherwise this call synchronises and raises ``ValidationError``."""
         self.check_input(x)
         if not x.is_cuda or x.device.index != self.device:
             raise InputMismatch(f"input on {x.device}, program on cuda:{self.device}")
@@ -215,20 +276,34 @@ class DeviceProgram:
             x = x.contiguous()
         n = int(x.shape[0])
         sh = _stream_handle(stream)
+        own_bad = None
         with torch.cuda.device(self.device):
+            if self.has_checks and bad is None:
+                bad = own_bad = torch.empty(1, dtype=torch.int64, device=x.device)
             cur, ld = x, int(x.stride(0)) if n > 0 else self.n_features
             for i, st in enumerate(self.stages):
                 last = i == len(self.stages) - 1
-                cols = st.spec.out_cols
-                dt = TORCH_DTYPE[st.spec.out_dtype]
-                if last and out is not None:
-                    y = out
-                else:
-                    y = torch.empty((n, cols), dtype=dt, device=x.device)
-                if n > 0:
+                spec = st.spec
+                if isinstance(spec, ColumnsSpec) and not spec.emit:
+                    st.run(cur, None, n, max(ld, 1), sh, bad=bad)  # membership check only
+                    continue
+                cols = spec.out_cols
+                dt = TORCH_DTYPE[spec.out_dtype]
+                y = out if last and out is not None else torch.empty((n, cols), dtype=dt, device=x.device)
+                if isinstance(spec, ColumnsSpec):
+                    st.run(cur, y if n > 0 else None, n, max(ld, 1), sh, bad=bad if spec.checks else None)
+                elif n > 0:
                     st.run(cur, y, n, max(ld, 1), sh, leaf_out if last else None)
                 cur, ld = y, cols
+            if own_bad is not None:
+                if stream is not None:
+                    stream.synchronize()
+                raise_unknown_category(own_bad)
         return cur
+
+    @property
+    def has_checks(self) -> bool:
+        return any(isinstance(st.spec, ColumnsSpec) and st.spec.checks for st in self.stages)
 
     def forest(self) -> _Forest:
         if len(self.stages) != 1 or not isinstance(self.stages[0], _Forest):
@@ -264,6 +339,8 @@ def run_host(program: DeviceProgram, x_host: torch.Tensor, chunk_rows: int = 1 <
         rows = min(chunk_rows, n)
         xbuf = [torch.empty((rows, program.n_features), dtype=torch.float32, device=dev) for _ in streams]
         ybuf = [torch.empty((rows, program.out_cols), dtype=dt, device=dev) for _ in streams]
+        nchunks = (n + rows - 1) // rows
+        bads = torch.full((nchunks,), -1, dtype=torch.int64, device=dev) if program.has_checks else None
         cur = torch.cuda.current_stream(dev)
         for s in streams:
             s.wait_stream(cur)
@@ -274,10 +351,16 @@ def run_host(program: DeviceProgram, x_host: torch.Tensor, chunk_rows: int = 1 <
             with torch.cuda.stream(s):
                 xb = xbuf[k][: r1 - r0]
                 xb.copy_(x_host[r0:r1], non_blocking=True)
-                program.run(xb, out=ybuf[k][: r1 - r0], stream=s)
+                program.run(xb, out=ybuf[k][: r1 - r0], stream=s,
+                            bad=bads[i:i + 1] if bads is not None else None)
                 out_host[r0:r1].copy_(ybuf[k][: r1 - r0], non_blocking=True)
         for s in streams:
             cur.wait_stream(s)
         for s in streams:
             s.synchronize()
+        if bads is not None:
+            b = bads.cpu().numpy()
+            hit = np.flatnonzero(b >= 0)
+            if hit.size:
+                raise_unknown_category(torch.tensor(int(b[hit[0]]) + int(hit[0]) * rows))
     return out_host

@@ -222,33 +222,35 @@ def config4b(out, dev, scale):
 
 
 def config5(out, dev, scale, rng):
-    import bench
-    rf, mu, sigma = bench.load_model()
-    F = 64
-    # the same trees, re-indexed onto 64 features (scaled inputs), so the forest shape is the north star's
-    trees = []
-    for t in rf.trees:
-        a = t.arrays
-        trees.append(TreeModel("decision_tree_regressor", F, TreeArrays(a.is_leaf, (a.feature * 2 + 1) % F,
-                                                                        a.threshold / 3.0, a.left, a.right, a.value), None))
-    rf64 = ForestModel("random_forest_classifier", F, tuple(trees), "mean_probability", 1.0, 0.0, rf.classes)
-    ss = ScalerModel("standard_scaler", F, vectors=(("mean", tuple(float(v) for v in rng.standard_normal(F).astype(np.float32))),
-                                                     ("scale", tuple(float(v) for v in rng.uniform(0.5, 2, F).astype(np.float32)))))
+    """Config 5: ColumnTransformer(StandardScaler 56 + OneHotEncoder 8 x 16) -> RF500 d8
+    on 5M x 64, fused (one forest kernel with the column prologue + the one-hot
+    membership check) vs materialised (column kernel writes the 184 model
+    columns, then the forest)."""
+    from oracle import ext_semantics as ext
+    from paper_2301_13441_b200.fuse import ColumnsSpec
+    from paper_2301_13441_b200.lower import ProgramSpec
+    from paper_2301_13441_b200.runtime import DeviceProgram
+    from workloads import config5_pipeline
     n = 5_000_000 // scale
-    x = torch.randn((n, F), generator=torch.Generator(device=dev).manual_seed(4), device=dev) * 2
-    p_ss = api.compile_model(ss).program(0)
-    p_rf = api.compile_model(rf64).program(0)
-    ms_ss = time_launch(lambda: p_ss.run(x))
-    xs = p_ss.run(x)
-    ms_rf = time_launch(lambda: p_rf.run(xs), reps=5)
-    sub = x[:3000].cpu().numpy()
-    want_s, _ = sem.predict(ss, sub)
-    want, _ = sem.predict(rf64, want_s.astype(np.float32))
-    got = p_rf.run(p_ss.run(x[:3000])).cpu().numpy().astype(np.float64)
-    out.append(line("5: StandardScaler(64) -> RF500 d8, 5M x 64", ms_ss + ms_rf, n, 64 * 4 + 1,
-                    bool(np.array_equal(got, want)),
-                    {"scaler_ms": ms_ss, "forest_ms": ms_rf, "scaler_hbm_gbs": n * 64 * 8 / (ms_ss / 1e3) / 1e9,
-                     "variant": p_rf.forest().info()}))
+    m, xh = config5_pipeline(rows=n)
+    x = torch.from_numpy(xh).to(dev)
+    compiled = api.compile_model(m)
+    prog = compiled.program(0)
+    bad = torch.empty(1, dtype=torch.int64, device=dev)
+    ms = time_launch(lambda: prog.run(x, bad=bad), reps=5)
+    assert int(bad.item()) == -1
+    cs, fs = prog.spec.stages
+    unfused = DeviceProgram(ProgramSpec([ColumnsSpec(fs.prologue, cs.n_inputs, cs.checks),
+                                         type(fs)(**{**fs.__dict__, "prologue": None, "n_inputs": 0})], 64), 0)
+    ms_unfused = time_launch(lambda: unfused.run(x, bad=bad), reps=5)
+    sub = 3000
+    want, _ = ext.predict(m, xh[:sub])
+    got = prog.run(x[:sub]).cpu().numpy().astype(np.float64)
+    got_u = unfused.run(x[:sub]).cpu().numpy().astype(np.float64)
+    out.append(line("5: ColumnTransformer(StandardScaler 56 + OneHot 8x16) -> RF500 d8, 5M x 64 (fused)", ms, n,
+                    64 * 4 + 1, bool(np.array_equal(got, want) and np.array_equal(got_u, want)),
+                    {"unfused_ms": ms_unfused, "fusion_speedup": ms_unfused / ms, "model_columns": 184,
+                     "variant": prog.stages[-1].info(), "launches_per_step": 4}))
 
 
 if __name__ == "__main__":
