@@ -28,6 +28,7 @@ kernel per operator representation runs on the GPU.  Inputs may be
 from __future__ import annotations
 
 import threading
+import warnings
 import weakref
 from dataclasses import dataclass
 
@@ -162,7 +163,10 @@ def _run(owner, spec_getter, x, device=None):
     prog = _program_for(owner, device, spec_getter())
     if arr.shape[1] != prog.n_features:
         raise InputMismatch(f"input shape {arr.shape} does not match (batch, {prog.n_features})")
-    out = run_host(prog, torch.from_numpy(np.ascontiguousarray(arr)))
+    with warnings.catch_warnings():  # read-only host arrays are only read
+        warnings.simplefilter("ignore", UserWarning)
+        xt = torch.from_numpy(np.ascontiguousarray(arr))
+    out = run_host(prog, xt)
     values = out.numpy()
     if prog.out_dtype == "bool":
         values = values.astype(np.uint8)

@@ -47,6 +47,28 @@ def _stream_handle(stream) -> int:
     return int(stream.cuda_stream)
 
 
+def compact_features(spec: ForestSpec, feature: np.ndarray):
+    """Rank / stage only the features the trees test.
+
+    A one-hot-widened input (config 5: 184 model columns, 28 tested) would
+    otherwise make every kernel variant stage and rank 156 dead columns per
+    row.  The used columns become the forest's features through a prologue
+    (a COPY gather of the raw column, or the subset of the fused
+    preprocessing ops).  Not with a dense selector: there a non-finite value
+    in ANY column poisons the row.  Returns (n_features,
+    prologue ops or None, n_inputs)."""
+    from .fuse import identity_ops
+    F = spec.n_features
+    if spec.dense_selector or feature.size == 0:
+        return F, spec.prologue, spec.n_inputs
+    used = np.unique(feature)
+    if used.size == F or (spec.prologue is None and used.size > 0.75 * F):
+        return F, spec.prologue, spec.n_inputs
+    base = spec.prologue if spec.prologue is not None else identity_ops(F)
+    n_in = spec.n_inputs if spec.prologue is not None else F
+    return int(used.size), np.ascontiguousarray(base[used]), n_in
+
+
 class _Forest:
     def __init__(self, spec: ForestSpec, device: int, variant: int = N.FOREST_AUTO):
         self.spec = spec
@@ -64,9 +86,12 @@ class _Forest:
         right = cat([t.right for t in trees], np.int32)
         payload = np.ascontiguousarray(np.concatenate([t.payload for t in trees]).astype(np.float32))
         classes = np.ascontiguousarray(np.asarray(spec.classes, np.float64))
+        n_features, prologue, n_inputs = compact_features(spec, feature)
+        if prologue is not spec.prologue:
+            feature = np.ascontiguousarray(np.searchsorted(np.unique(feature), feature).astype(np.int32))
         keep = (node_off, leaf_off, feature, threshold, left, right, payload, classes)
         d = N.ForestDesc()
-        d.n_trees, d.n_features, d.n_outputs = T, spec.n_features, spec.n_outputs
+        d.n_trees, d.n_features, d.n_outputs = T, n_features, spec.n_outputs
         d.node_offset = N.ptr(node_off, N.c_i64)
         d.leaf_offset = N.ptr(leaf_off, N.c_i64)
         d.feature = N.ptr(feature, N.c_i32)
@@ -81,7 +106,10 @@ class _Forest:
         d.out_dtype = OUT_CODE[spec.out_dtype]
         d.dense_selector = int(spec.dense_selector)
         d.variant = variant
-        pro = _prologue(spec, d)
+        pro = None
+        if prologue is not None:
+            pro = np.ascontiguousarray(prologue)
+            d.prologue, d.n_inputs = pro.ctypes.data, int(n_inputs)
         h = N.c_vp()
         N.check(N.lib().cmlb_forest_create(C.byref(d), device, C.byref(h)))
         del keep, pro
