@@ -26,6 +26,23 @@ int cuda_fail(cudaError_t e, const char* what) {
 
 void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+// Stream-ordered scratch (cudaMallocAsync) comes from the device's default
+// pool; keep freed blocks cached there instead of returning them to the
+// driver at every synchronisation (the default threshold of 0 turns each
+// run's scratch into a fresh mapping).
+void keep_pool(int device) {
+  static std::mutex mu;
+  static std::unordered_map<int, bool> done;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done[device]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done[device] = true;
+}
+
 int num_sms(int device) {
   static std::mutex mu;
   static std::unordered_map<int, int> cache;

@@ -143,6 +143,7 @@ int cmlb_columns_run(const cmlb_columns* m, const float* x, int64_t n_rows, int6
     note_launch();
   }
   if (bad_row) {
+    keep_pool(m->device);
     void* scratch = nullptr;
     CMLB_CUDA(cudaMallocAsync(&scratch, sizeof(unsigned long long), s));
     a.bad = static_cast<unsigned long long*>(scratch);

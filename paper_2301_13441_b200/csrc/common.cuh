@@ -101,5 +101,6 @@ inline int out_dtype_ok(int dt) { return dt >= CMLB_OUT_BOOL && dt <= CMLB_OUT_F
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 int num_sms(int device);
+void keep_pool(int device);
 
 }  // namespace cmlb

@@ -14,12 +14,16 @@
 // for both the coalesced fill and the per-row reads); the weight chunk as
 // float64 ws[k][c], read as warp-wide broadcasts.
 
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <memory>
 #include <string>
 #include <vector>
 
 #include "common.cuh"
+#include "sm100.cuh"
 
 namespace cmlb {
 
@@ -31,7 +35,10 @@ struct LinearArgs {
   const float* b;        // [C]
   const double* classes;
   const cmlb_column_op* pro;  // fused preprocessing (nullable)
+  const float* wnorm;         // [C] |w_c|_2 rounded up (certified path)
   int F, C, tail, out_dt, sparse;
+  int32_t* queue;             // certified path: rows left to the float64 recompute
+  int32_t* queue_len;
 };
 
 constexpr int LNT = 128;
@@ -213,6 +220,7 @@ __global__ void __launch_bounds__(LNT) linear_kernel(const LinearArgs a) {
 
 using LinFn = void (*)(const LinearArgs);
 
+
 // (kernel, rows per CTA) by output count
 static LinFn linear_for(int C, int* rows) {
   *rows = LNT * 2;
@@ -228,15 +236,382 @@ static LinFn linear_for(int C, int* rows) {
   return nullptr;
 }
 
+
+// ---------------------------------------------------------------------------
+// Certified float32 path for the class tails (ARGMAX / SIGMOID / SIGN).
+//
+// The class needs only the ORDER of the reference's float32 logits (or the
+// sign of one), not their bits.  Logits are accumulated in float32 FFMA
+// chains (half the bytes of ws, full-rate FP32) with a rigorous bound: a
+// sequential chain of n fused multiply-adds errs by at most n u sum|x_k w_k|
+// <= n u |x| |w_c| (u = 2^-24, Cauchy-Schwarz), plus the reference's two
+// float32 roundings (logit, + b).  When the top logit beats every other by
+// more than twice that bound (or the sign is clear of the sigmoid's rounding
+// window), the reference class is certain.  Otherwise -- or on any
+// non-finite value -- the thread recomputes its row in float64 exactly as the
+// reference does (ascending k, kernels.py:95-100, CSR zero-skip) and takes the
+// reference tail.  X is read once from HBM either way.
+// ---------------------------------------------------------------------------
+
+template <int CM>
+__device__ void exact_row_tail(const LinearArgs& a, int64_t row) {
+  double acc[CM];
+#pragma unroll
+  for (int c = 0; c < CM; ++c) acc[c] = 0.0;
+  const float* src = a.x + row * a.ldx;
+  for (int k = 0; k < a.F; ++k) {
+    const double xv = (double)load_col(a.pro, src, k);
+#pragma unroll
+    for (int c = 0; c < CM; ++c) {
+      if (c < a.C) {
+        const double wc = (double)__ldg(a.w + (int64_t)c * a.F + k);
+        if (!(a.sparse && wc == 0.0)) acc[c] = fma(xv, wc, acc[c]);
+      }
+    }
+  }
+  float z[CM];
+#pragma unroll
+  for (int c = 0; c < CM; ++c) z[c] = c < a.C ? __fadd_rn(__double2float_rn(acc[c]), __ldg(a.b + c)) : 0.0f;
+  if (a.tail == CMLB_LIN_ARGMAX) {
+    store_out(a.y, row, a.out_dt, a.classes[first_max<CM>(z, a.C)]);
+  } else if (a.tail == CMLB_LIN_SIGMOID) {
+    const float p = __double2float_rn(ref_sigmoid((double)z[0]));
+    store_out(a.y, row, a.out_dt, a.classes[p > 0.5f ? 1 : 0]);
+  } else {
+    store_out(a.y, row, a.out_dt, a.classes[z[0] > 0.0f ? 1 : 0]);
+  }
+}
+
+template <int CM, int LRPT, int LKC>
+__global__ void __launch_bounds__(LNT) linear_cert_kernel(const LinearArgs a) {
+  constexpr int LROWS = LNT * LRPT;
+  constexpr int LXS = LROWS + 1;
+  constexpr int CE = (CM + 3) / 4 * 4;
+  constexpr int NV = LROWS * LKC / 4 / LNT;
+  static_assert(LKC == 16 && NV * LNT * 4 == LROWS * LKC, "chunk shape");
+  __shared__ float xs[LKC * LXS];
+  __shared__ __align__(16) float ws[LKC * CE];
+  const int tid = threadIdx.x;
+  const int64_t tile = (int64_t)blockIdx.x * LROWS;
+  const int F = a.F, C = a.C;
+  const bool vec = (a.ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
+
+  float acc[LRPT][CM], nx[LRPT];
+#pragma unroll
+  for (int k = 0; k < LRPT; ++k) {
+    nx[k] = 0.0f;
+#pragma unroll
+    for (int c = 0; c < CM; ++c) acc[k][c] = 0.0f;
+  }
+
+  float4 pre[NV];
+  auto load_chunk = [&](int k0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int idx = tid + LNT * i;
+      const int r = idx >> 2, part = idx & 3;
+      const int64_t row = tile + r;
+      const int k = k0 + part * 4;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (row < a.n_rows) {
+        const float* rp = a.x + row * a.ldx;
+        if (a.pro) {
+          if (k < F) v.x = load_col(a.pro, rp, k);
+          if (k + 1 < F) v.y = load_col(a.pro, rp, k + 1);
+          if (k + 2 < F) v.z = load_col(a.pro, rp, k + 2);
+          if (k + 3 < F) v.w = load_col(a.pro, rp, k + 3);
+        } else if (vec && k + 4 <= F) {
+          v = __ldg(reinterpret_cast<const float4*>(rp + k));
+        } else {
+          if (k < F) v.x = __ldg(rp + k);
+          if (k + 1 < F) v.y = __ldg(rp + k + 1);
+          if (k + 2 < F) v.z = __ldg(rp + k + 2);
+          if (k + 3 < F) v.w = __ldg(rp + k + 3);
+        }
+      }
+      pre[i] = v;
+    }
+  };
+  auto store_chunk = [&](int k0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int idx = tid + LNT * i;
+      const int r = idx >> 2, part = idx & 3;
+      float* dst = xs + (part * 4) * LXS + r;
+      dst[0] = pre[i].x;
+      dst[LXS] = pre[i].y;
+      dst[2 * LXS] = pre[i].z;
+      dst[3 * LXS] = pre[i].w;
+    }
+    for (int i = tid; i < LKC * CE; i += LNT) {
+      const int kk = i / CE, c = i % CE;
+      ws[i] = (k0 + kk < F && c < C) ? __ldg(a.w + (int64_t)c * F + k0 + kk) : 0.0f;
+    }
+  };
+
+  load_chunk(0);
+  for (int k0 = 0; k0 < F; k0 += LKC) {
+    __syncthreads();
+    store_chunk(k0);
+    __syncthreads();
+    if (k0 + LKC < F) load_chunk(k0 + LKC);
+    const int kc = min(LKC, F - k0);
+    for (int kk = 0; kk < kc; ++kk) {
+      float xv[LRPT];
+#pragma unroll
+      for (int k = 0; k < LRPT; ++k) {
+        xv[k] = xs[kk * LXS + tid + k * LNT];
+        nx[k] = fmaf(xv[k], xv[k], nx[k]);
+      }
+      const float4* w4 = reinterpret_cast<const float4*>(ws + kk * CE);
+#pragma unroll
+      for (int c4 = 0; c4 < CE / 4; ++c4) {
+        const float4 wv = w4[c4];
+        const float wq[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const int c = 4 * c4 + h;
+          if (c < CM) {
+#pragma unroll
+            for (int k = 0; k < LRPT; ++k) acc[k][c] = fmaf(xv[k], wq[h], acc[k][c]);
+          }
+        }
+      }
+    }
+  }
+
+  // n u |x| |w|: |x| from its own float32 chain (relative error <= F u,
+  // covered by the 1.0625 factor for F < 2^20)
+  const float nu = (float)(F + 2) * 5.9604644775390625e-08f;
+#pragma unroll
+  for (int k = 0; k < LRPT; ++k) {
+    const int64_t row = tile + tid + k * LNT;
+    if (row >= a.n_rows) continue;
+    const float xn = sqrtf(nx[k]) * 1.0625f;
+    float z[CM], e[CM];
+    bool ok = true;
+#pragma unroll
+    for (int c = 0; c < CM; ++c) {
+      if (c < C) {
+        z[c] = __fadd_rn(acc[k][c], __ldg(a.b + c));
+        // chain bound + the reference's rounding of the logit and of + b
+        e[c] = nu * xn * __ldg(a.wnorm + c) + 2.4e-7f * (fabsf(acc[k][c]) + fabsf(z[c]));
+        ok = ok && (z[c] - z[c] == 0.0f) && (e[c] < 3.0e38f);  // finite
+      } else {
+        z[c] = 0.0f;
+        e[c] = 0.0f;
+      }
+    }
+    if (ok) {
+      if (a.tail == CMLB_LIN_ARGMAX) {
+        const int t = first_max<CM>(z, C);
+#pragma unroll
+        for (int c = 0; c < CM; ++c)
+          if (c < C && c != t) ok = ok && (z[t] - z[c] > 2.0f * (e[t] + e[c]));
+        if (ok) store_out(a.y, row, a.out_dt, a.classes[t]);
+      } else if (a.tail == CMLB_LIN_SIGMOID) {
+        // sigmoid(z) rounds above 0.5 for z > 2^-23: demand 2^-21
+        if (z[0] - 2.0f * e[0] > 4.76837158203125e-07f) store_out(a.y, row, a.out_dt, a.classes[1]);
+        else if (z[0] + 2.0f * e[0] < 0.0f) store_out(a.y, row, a.out_dt, a.classes[0]);
+        else ok = false;
+      } else {  // SIGN
+        if (z[0] - 2.0f * e[0] > 0.0f) store_out(a.y, row, a.out_dt, a.classes[1]);
+        else if (z[0] + 2.0f * e[0] < 0.0f) store_out(a.y, row, a.out_dt, a.classes[0]);
+        else ok = false;
+      }
+    }
+    if (!ok) a.queue[atomicAdd(a.queue_len, 1)] = (int32_t)row;
+  }
+}
+
+// Persistent: one warp per queued row, float64 in the reference's order --
+// lane c runs output c's ascending-k FMA chain (kernels.py:95-100), x
+// arrives 32 features at a time by one coalesced load and shuffles.
+template <int CM>
+__global__ void __launch_bounds__(LNT) linear_exact_rows_kernel(const LinearArgs a) {
+  const int nq = *a.queue_len;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * LNT + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * LNT) >> 5;
+  const int F = a.F, C = a.C;
+  for (int64_t i = gw; i < nq; i += nw) {
+    const int64_t row = a.queue[i];
+    const float* src = a.x + row * a.ldx;
+    double acc = 0.0;
+    const int c = lane;
+    const float* wr = a.w + (int64_t)(c < C ? c : 0) * F;
+    for (int k0 = 0; k0 < F; k0 += 32) {
+      const int kn = min(32, F - k0);
+      const float xl = lane < kn ? load_col(a.pro, src, k0 + lane) : 0.0f;
+      float wv[32];  // this lane's coefficients for the 32 features, loaded up front
+#pragma unroll
+      for (int j = 0; j < 32; ++j) wv[j] = (j < kn && c < C) ? __ldg(wr + k0 + j) : 0.0f;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const double xv = (double)__shfl_sync(0xffffffffu, xl, j);
+        if (j < kn && c < C && !(a.sparse && wv[j] == 0.0f)) acc = fma(xv, (double)wv[j], acc);
+      }
+    }
+    float zl = c < C ? __fadd_rn(__double2float_rn(acc), __ldg(a.b + c)) : 0.0f;
+    float z[CM];
+#pragma unroll
+    for (int q = 0; q < CM; ++q) z[q] = __shfl_sync(0xffffffffu, zl, q & 31);
+    if (lane == 0) {
+      if (a.tail == CMLB_LIN_ARGMAX) {
+        store_out(a.y, row, a.out_dt, a.classes[first_max<CM>(z, C)]);
+      } else if (a.tail == CMLB_LIN_SIGMOID) {
+        const float p = __double2float_rn(ref_sigmoid((double)z[0]));
+        store_out(a.y, row, a.out_dt, a.classes[p > 0.5f ? 1 : 0]);
+      } else {
+        store_out(a.y, row, a.out_dt, a.classes[z[0] > 0.0f ? 1 : 0]);
+      }
+    }
+  }
+}
+
+
+
+// Thread-per-row certified kernel (the default for class tails, F % 4 == 0):
+// each thread streams its rows' features straight from HBM with float4 loads
+// (16 features in flight per row, double-buffered in registers; a warp's 32
+// rows share their cache lines through L1) and multiplies them against W,
+// which sits in shared memory k-major so the CM coefficients of feature k are
+// one broadcast read for the whole warp.  Every logit is a sequential float32
+// FMA chain (the n u |x| |w| bound of linear_cert_kernel applies verbatim);
+// FP32 work is 7,840 FMA per 784-feature row against 3,136 B of HBM reads, so
+// the kernel is HBM-bound.
+template <int CM, int RPT>
+__global__ void __launch_bounds__(LNT) linear_rows_kernel(const LinearArgs a) {
+  constexpr int CE = (CM + 3) & ~3;
+  extern __shared__ __align__(16) float wkm[];   // [F][CE]
+  const int F = a.F, C = a.C;
+  for (int i = threadIdx.x; i < F * CE; i += LNT) {
+    const int k = i / CE, c = i - k * CE;
+    wkm[i] = c < C ? __ldg(a.w + (int64_t)c * F + k) : 0.0f;
+  }
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * LNT * RPT + threadIdx.x;
+  const float* rp[RPT];
+  bool live[RPT];
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const int64_t row = base + r * LNT;
+    live[r] = row < a.n_rows;
+    rp[r] = a.x + (live[r] ? row : 0) * a.ldx;
+  }
+  float acc[RPT][CM], nx[RPT];
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    nx[r] = 0.0f;
+#pragma unroll
+    for (int c = 0; c < CM; ++c) acc[r][c] = 0.0f;
+  }
+  constexpr int U = 4;  // float4 per row per step (16 features)
+  float4 cur[RPT][U], nxt[RPT][U];
+  auto load = [&](float4 (&dst)[RPT][U], int k0) {
+#pragma unroll
+    for (int r = 0; r < RPT; ++r)
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = k0 + 4 * u;
+        dst[r][u] = (k < F) ? __ldg(reinterpret_cast<const float4*>(rp[r] + k)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+  };
+  load(cur, 0);
+  for (int k0 = 0; k0 < F; k0 += 4 * U) {
+    if (k0 + 4 * U < F) load(nxt, k0 + 4 * U);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = k0 + 4 * u;
+      if (k >= F) break;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float4* w4 = reinterpret_cast<const float4*>(wkm + (k + e) * CE);
+        float xv[RPT];
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+          xv[r] = e == 0 ? cur[r][u].x : e == 1 ? cur[r][u].y : e == 2 ? cur[r][u].z : cur[r][u].w;
+          nx[r] = fmaf(xv[r], xv[r], nx[r]);
+        }
+#pragma unroll
+        for (int c4 = 0; c4 < CE / 4; ++c4) {
+          const float4 w = w4[c4];
+#pragma unroll
+          for (int r = 0; r < RPT; ++r) {
+            if (4 * c4 + 0 < CM) acc[r][4 * c4 + 0] = fmaf(xv[r], w.x, acc[r][4 * c4 + 0]);
+            if (4 * c4 + 1 < CM) acc[r][4 * c4 + 1] = fmaf(xv[r], w.y, acc[r][4 * c4 + 1]);
+            if (4 * c4 + 2 < CM) acc[r][4 * c4 + 2] = fmaf(xv[r], w.z, acc[r][4 * c4 + 2]);
+            if (4 * c4 + 3 < CM) acc[r][4 * c4 + 3] = fmaf(xv[r], w.w, acc[r][4 * c4 + 3]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RPT; ++r)
+#pragma unroll
+      for (int u = 0; u < U; ++u) cur[r][u] = nxt[r][u];
+  }
+  const float nu = (float)(F + 2) * 5.9604644775390625e-08f;
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    if (!live[r]) continue;
+    const int64_t row = base + r * LNT;
+    const float xn = sqrtf(nx[r]) * 1.0625f;
+    float z[CM], e[CM];
+    bool ok = true;
+#pragma unroll
+    for (int c = 0; c < CM; ++c) {
+      if (c < C) {
+        z[c] = __fadd_rn(acc[r][c], __ldg(a.b + c));
+        e[c] = nu * xn * __ldg(a.wnorm + c) + 2.4e-7f * (fabsf(acc[r][c]) + fabsf(z[c]));
+        ok = ok && (z[c] - z[c] == 0.0f) && (e[c] < 3.0e38f);
+      } else {
+        z[c] = 0.0f;
+        e[c] = 0.0f;
+      }
+    }
+    if (ok) {
+      if (a.tail == CMLB_LIN_ARGMAX) {
+        const int t = first_max<CM>(z, C);
+#pragma unroll
+        for (int c = 0; c < CM; ++c)
+          if (c < C && c != t) ok = ok && (z[t] - z[c] > 2.0f * (e[t] + e[c]));
+        if (ok) store_out(a.y, row, a.out_dt, a.classes[t]);
+      } else if (a.tail == CMLB_LIN_SIGMOID) {
+        if (z[0] - 2.0f * e[0] > 4.76837158203125e-07f) store_out(a.y, row, a.out_dt, a.classes[1]);
+        else if (z[0] + 2.0f * e[0] < 0.0f) store_out(a.y, row, a.out_dt, a.classes[0]);
+        else ok = false;
+      } else {
+        if (z[0] - 2.0f * e[0] > 0.0f) store_out(a.y, row, a.out_dt, a.classes[1]);
+        else if (z[0] + 2.0f * e[0] < 0.0f) store_out(a.y, row, a.out_dt, a.classes[0]);
+        else ok = false;
+      }
+    }
+    if (!ok) a.queue[atomicAdd(a.queue_len, 1)] = (int32_t)row;
+  }
+}
+
+static LinFn linear_cert_for(int C, LinFn* fixup) {
+  if (C <= 1) { *fixup = linear_exact_rows_kernel<1>; return linear_cert_kernel<1, 2, 16>; }
+  if (C <= 2) { *fixup = linear_exact_rows_kernel<2>; return linear_cert_kernel<2, 2, 16>; }
+  if (C <= 4) { *fixup = linear_exact_rows_kernel<4>; return linear_cert_kernel<4, 2, 16>; }
+  if (C <= 8) { *fixup = linear_exact_rows_kernel<8>; return linear_cert_kernel<8, 2, 16>; }
+  if (C <= 12) { *fixup = linear_exact_rows_kernel<12>; return linear_cert_kernel<12, 2, 16>; }
+  if (C <= 16) { *fixup = linear_exact_rows_kernel<16>; return linear_cert_kernel<16, 2, 16>; }
+  if (C <= 32) { *fixup = linear_exact_rows_kernel<32>; return linear_cert_kernel<32, 1, 16>; }
+  return nullptr;
+}
+
 }  // namespace cmlb
 
 struct cmlb_linear {
   int device = 0, F = 0, C = 0, tail = 0, out_dt = 4, sparse = 0, n_inputs = 0;
+  float* wnorm = nullptr;
   float* w = nullptr;
   float* b = nullptr;
   double* classes = nullptr;
   cmlb_column_op* pro = nullptr;
-  ~cmlb_linear() { cudaFree(w); cudaFree(b); cudaFree(classes); cudaFree(pro); }
+  ~cmlb_linear() { cudaFree(w); cudaFree(b); cudaFree(classes); cudaFree(pro); cudaFree(wnorm); }
 };
 
 extern "C" {
@@ -264,6 +639,16 @@ int cmlb_linear_create(const cmlb_linear_desc* d, int device, cmlb_linear** out)
   CMLB_CUDA(cudaMalloc(&m->classes, nc * sizeof(double)));
   if (d->n_classes > 0)
     CMLB_CUDA(cudaMemcpy(m->classes, d->classes, nc * sizeof(double), cudaMemcpyHostToDevice));
+  {
+    std::vector<float> wn(m->C);
+    for (int c = 0; c < m->C; ++c) {
+      double s2 = 0.0;
+      for (int k = 0; k < m->F; ++k) s2 += (double)d->coef[(size_t)c * m->F + k] * d->coef[(size_t)c * m->F + k];
+      wn[c] = (float)(std::sqrt(s2) * (1.0 + 1e-6));
+    }
+    CMLB_CUDA(cudaMalloc(&m->wnorm, m->C * sizeof(float)));
+    CMLB_CUDA(cudaMemcpy(m->wnorm, wn.data(), m->C * sizeof(float), cudaMemcpyHostToDevice));
+  }
   m->n_inputs = m->F;
   if (d->prologue) {
     if (d->n_inputs <= 0) return fail(CMLB_E_VALIDATION, "prologue needs n_inputs > 0");
@@ -291,12 +676,56 @@ int cmlb_linear_run(const cmlb_linear* m, const float* x, int64_t n_rows, int64_
   a.pro = m->pro;
   a.x = x; a.n_rows = n_rows; a.ldx = ldx; a.y = y; a.w = m->w; a.b = m->b; a.classes = m->classes;
   a.F = m->F; a.C = m->C; a.tail = m->tail; a.out_dt = m->out_dt; a.sparse = m->sparse;
+  a.wnorm = m->wnorm;
+  keep_pool(m->device);
   int rows = 0;
   LinFn k = linear_for(m->C, &rows);
-  const int64_t grid = ceil_div(n_rows, rows);
-  k<<<(unsigned)grid, LNT, 0, (cudaStream_t)stream>>>(a);
+  // class tails: certified float32 logits (exact float64 recompute of the
+  // rare rows whose class the bound cannot settle); CMLB_LINEAR_EXACT=1 forces
+  // the float64 kernel everywhere
+  static const bool force_exact = [] {
+    const char* e = std::getenv("CMLB_LINEAR_EXACT");
+    return e && e[0] == '1';
+  }();
+  LinFn fixup = nullptr;
+  if (!force_exact && m->tail != CMLB_LIN_VALUES && m->tail != CMLB_LIN_SOFTMAX_ARGMAX) {
+    if (LinFn kc = linear_cert_for(m->C, &fixup)) {
+      k = kc;
+      rows = m->C <= 16 ? 2 * LNT : LNT;
+    }
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  void* scratch = nullptr;
+  if (fixup) {
+    if (n_rows > INT32_MAX) return fail(CMLB_E_INPUT, "linear batch exceeds 2^31 rows");
+    CMLB_CUDA(cudaMallocAsync(&scratch, (size_t)(n_rows + 4) * sizeof(int32_t), s));
+    a.queue_len = static_cast<int32_t*>(scratch);
+    a.queue = a.queue_len + 4;
+    CMLB_CUDA(cudaMemsetAsync(a.queue_len, 0, sizeof(int32_t), s));
+  }
+  // thread-per-row certified kernel when rows are float4-aligned and W fits
+  const int cm = m->C <= 2 ? 2 : m->C <= 4 ? 4 : m->C <= 8 ? 8 : m->C <= 12 ? 12 : 16;
+  const size_t wbytes = (size_t)m->F * ((cm + 3) & ~3) * 4;
+  const bool aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (ldx % 4) == 0 && (m->F % 4) == 0;
+  if (fixup && !m->pro && m->C <= 16 && aligned && wbytes <= 100 * 1024) {
+    LinFn kr = cm == 2 ? linear_rows_kernel<2, 2> : cm == 4 ? linear_rows_kernel<4, 2> : cm == 8 ? linear_rows_kernel<8, 2>
+             : cm == 12 ? linear_rows_kernel<12, 2> : linear_rows_kernel<16, 2>;
+    const int rpt = 2;
+    CMLB_CUDA(cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wbytes));
+    kr<<<(unsigned)ceil_div(n_rows, (int64_t)LNT * rpt), LNT, wbytes, s>>>(a);
+  } else {
+    const int64_t grid = ceil_div(n_rows, rows);
+    k<<<(unsigned)grid, LNT, 0, s>>>(a);
+  }
   note_launch();
   CMLB_CUDA(cudaGetLastError());
+  if (fixup) {
+    const int g = (int)std::min<int64_t>(ceil_div(n_rows, LNT), (int64_t)num_sms(m->device) * 4);
+    fixup<<<g, LNT, 0, s>>>(a);
+    note_launch();
+    CMLB_CUDA(cudaGetLastError());
+    CMLB_CUDA(cudaFreeAsync(scratch, s));
+  }
   return CMLB_OK;
 }
 

@@ -797,6 +797,7 @@ int cmlb_svm_run(const cmlb_svm* m, const float* x, int64_t n_rows, int64_t ldx,
   svm::Args a = m->a;
   a.x = x; a.n_rows = n_rows; a.ldx = ldx; a.y = y; a.dec_out = decision;
   a.vec_x = ((reinterpret_cast<uintptr_t>(x) & 15) == 0 && (ldx & 3) == 0) ? 1 : 0;
+  keep_pool(m->device);
   void* scratch = nullptr;
   CMLB_CUDA(cudaMallocAsync(&scratch, (size_t)(n_rows + 4) * sizeof(int32_t), s));
   a.queue_len = static_cast<int32_t*>(scratch);
