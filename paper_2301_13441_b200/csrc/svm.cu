@@ -17,9 +17,9 @@
 //    G += Xb.Sb + Xs.Sb + Xb.Ss: three tf32 MMAs per K step give ~fp32
 //    accuracy ("3xTF32").  SV splits are prepared once on the host in the
 //    UMMA core-matrix layout and streamed by TMA bulk copies; row tiles are
-//    split on the fly by four producer warps.  Warp roles: 0-3 A producers
-//    (load + split X), 4 B producer (cp.async.bulk), 5 MMA issuer (one
-//    thread) + TMEM owner, 6-9 epilogue.  TMEM holds two 128 x 256 f32
+//    split on the fly by eight producer warps.  Warp roles: 0-7 A producers
+//    (load + split X, two threads per row), 8 B producer (cp.async.bulk),
+//    9 MMA issuer (one thread) + TMEM owner, 10-17 epilogue.  TMEM holds two 128 x 256 f32
 //    accumulators so the epilogue of SV tile t overlaps the MMAs of t+1.
 //    Epilogue (thread = row = TMEM lane): kernel function of the Gram entry,
 //    float64 per-class decision sums, a running error bound E for the row;
@@ -36,6 +36,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -55,7 +56,10 @@ constexpr int STAGES = 2;
 constexpr int A_BYTES = BM * BK * 4;          // 16 KB per split half
 constexpr int B_BYTES = BN * BK * 4;          // 32 KB per split half
 constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-constexpr int EPI_WARP0 = 6;
+constexpr int A_THREADS = 2 * BM;             // 8 warps: two threads per row, one half of each K chunk
+constexpr int B_WARP = A_THREADS / 32;        // TMA producer
+constexpr int MMA_WARP = B_WARP + 1;          // MMA issuer + TMEM owner
+constexpr int EPI_WARP0 = MMA_WARP + 1;
 constexpr int EPI_THREADS = 256;              // 8 warps: 2 per TMEM lane group, one column half each
 constexpr int THREADS = EPI_WARP0 * 32 + EPI_THREADS;
 constexpr int MAXC = 16;                      // classes handled by the fused epilogue
@@ -70,6 +74,7 @@ struct Args {
   const float* ns;         // [n_tiles * BN] |sv|^2 (float64 rounded once)
   const float* w;          // [n_tiles * BN][CPS] coefficient of SV j toward class o (0 for its own class)
   const float* wmax;       // [n_tiles * BN] max_o |w|
+  const float* qerr;       // [n_tiles * BN] RBF bound term wmax_j * gamma * 1.075e-6 * |sv_j|^2
   const int32_t* cls;      // [n_tiles * BN] class of SV j, -1 padding
   const double* sv;        // [n_sv][F] float64 copy (exact path)
   const float* coef;       // [rows][n_sv] libsvm sv_coef (exact path)
@@ -82,6 +87,7 @@ struct Args {
   double* dec_out;
   float* err_out;          // debug: per-row error bound E (nullable)
   int no_exact;            // debug: write every row from the fast path
+  int probe;               // debug: bit 0 skip X loads, bit 1 skip B copies, bit 2 skip epilogue math
   const cmlb_column_op* pro;  // fused preprocessing (nullable)
   int32_t* queue;          // [n_rows] rows for the exact path
   int32_t* queue_len;
@@ -165,10 +171,11 @@ __global__ void __launch_bounds__(THREADS, 1) svm_tc_kernel(const Args a) {
   float* ns_s = w_s + BN * CPS;
   float* wm_s = ns_s + BN;
   int32_t* cls_s = reinterpret_cast<int32_t*>(wm_s + BN);
+  float* q_s = reinterpret_cast<float*>(cls_s + BN);
 
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      bar_init(&full_bar[s], BM + 1);
+      bar_init(&full_bar[s], A_THREADS + 1);
       bar_init(&empty_bar[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -177,55 +184,69 @@ __global__ void __launch_bounds__(THREADS, 1) svm_tc_kernel(const Args a) {
     }
     bar_fence_init();
   }
-  if (warp == 5) tmem_alloc(&tmem_slot, 512);
+  if (warp == MMA_WARP) tmem_alloc(&tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
 
-  if (warp < 4) {
+  if (tid < A_THREADS) {
     // ---- A producers: thread r owns row r of the tile --------------------
-    const int r = tid;
+    // The row's next 32 features are loaded into registers BEFORE waiting for
+    // their stage to drain, so the L2 latency overlaps the MMAs in flight.
+    constexpr int CH = BK / 8;               // float4 chunks per thread per stage
+    const int r = tid & (BM - 1), c0 = (tid / BM) * CH;
     const int64_t row = row0 + r;
     const bool valid = row < a.n_rows;
     const float* src = a.x + (valid ? row : 0) * a.ldx;
+    float4 v[CH];
+    auto load_k = [&](int kb) {
+      const int k0 = kb * BK;
+#pragma unroll
+      for (int cc = 0; cc < CH; ++cc) {
+        const int c = c0 + cc;
+        const int k = k0 + 4 * c;
+        float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (valid && !(a.probe & 1)) {
+          if (a.pro) {
+            if (k < a.F) q.x = load_col(a.pro, src, k);
+            if (k + 1 < a.F) q.y = load_col(a.pro, src, k + 1);
+            if (k + 2 < a.F) q.z = load_col(a.pro, src, k + 2);
+            if (k + 3 < a.F) q.w = load_col(a.pro, src, k + 3);
+          } else if (a.vec_x && k + 3 < a.F) {
+            q = __ldg(reinterpret_cast<const float4*>(src + k));
+          } else {
+            if (k < a.F) q.x = __ldg(src + k);
+            if (k + 1 < a.F) q.y = __ldg(src + k + 1);
+            if (k + 2 < a.F) q.z = __ldg(src + k + 2);
+            if (k + 3 < a.F) q.w = __ldg(src + k + 3);
+          }
+        }
+        v[cc] = q;
+      }
+    };
+    load_k(0);
     for (int it = 0; it < total; ++it) {
-      const int kb = it % KB, s = it % STAGES;
+      const int s = it % STAGES;
       bar_wait(&empty_bar[s], ((it / STAGES) & 1) ^ 1);
       uint8_t* abig = smem + s * STAGE_BYTES;
       uint8_t* asmall = abig + A_BYTES;
-      const int k0 = kb * BK;
 #pragma unroll
-      for (int c = 0; c < BK / 4; ++c) {
-        const int k = k0 + 4 * c;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (valid) {
-          if (a.pro) {
-            if (k < a.F) v.x = load_col(a.pro, src, k);
-            if (k + 1 < a.F) v.y = load_col(a.pro, src, k + 1);
-            if (k + 2 < a.F) v.z = load_col(a.pro, src, k + 2);
-            if (k + 3 < a.F) v.w = load_col(a.pro, src, k + 3);
-          } else if (a.vec_x && k + 3 < a.F) {
-            v = __ldg(reinterpret_cast<const float4*>(src + k));
-          } else {
-            if (k < a.F) v.x = __ldg(src + k);
-            if (k + 1 < a.F) v.y = __ldg(src + k + 1);
-            if (k + 2 < a.F) v.z = __ldg(src + k + 2);
-            if (k + 3 < a.F) v.w = __ldg(src + k + 3);
-          }
-        }
+      for (int cc = 0; cc < CH; ++cc) {
+        const int c = c0 + cc;
         float4 hi, lo;
-        hi.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u); lo.x = v.x - hi.x;
-        hi.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u); lo.y = v.y - hi.y;
-        hi.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u); lo.z = v.z - hi.z;
-        hi.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u); lo.w = v.w - hi.w;
+        hi.x = __uint_as_float(__float_as_uint(v[cc].x) & 0xFFFFE000u); lo.x = v[cc].x - hi.x;
+        hi.y = __uint_as_float(__float_as_uint(v[cc].y) & 0xFFFFE000u); lo.y = v[cc].y - hi.y;
+        hi.z = __uint_as_float(__float_as_uint(v[cc].z) & 0xFFFFE000u); lo.z = v[cc].z - hi.z;
+        hi.w = __uint_as_float(__float_as_uint(v[cc].w) & 0xFFFFE000u); lo.w = v[cc].w - hi.w;
         *reinterpret_cast<float4*>(abig + c * (BM * 16) + r * 16) = hi;
         *reinterpret_cast<float4*>(asmall + c * (BM * 16) + r * 16) = lo;
       }
       fence_async_smem();
       bar_arrive(&full_bar[s]);
+      if (it + 1 < total) load_k((it + 1) % KB);
     }
-  } else if (warp == 4) {
+  } else if (warp == B_WARP) {
     // ---- B producer: one bulk copy of the pre-split SV stage -------------
     if (lane == 0) {
       for (int it = 0; it < total; ++it) {
@@ -233,12 +254,16 @@ __global__ void __launch_bounds__(THREADS, 1) svm_tc_kernel(const Args a) {
         bar_wait(&empty_bar[s], ((it / STAGES) & 1) ^ 1);
         uint8_t* dst = smem + s * STAGE_BYTES + 2 * A_BYTES;
         const uint8_t* src = a.bsplit + (size_t)it * (2 * B_BYTES);
-        bar_arrive_tx(&full_bar[s], 2 * B_BYTES);
-        bulk_load(dst, src, B_BYTES, &full_bar[s]);
-        bulk_load(dst + B_BYTES, src + B_BYTES, B_BYTES, &full_bar[s]);
+        if (a.probe & 2) {
+          bar_arrive(&full_bar[s]);
+        } else {
+          bar_arrive_tx(&full_bar[s], 2 * B_BYTES);
+          bulk_load(dst, src, B_BYTES, &full_bar[s]);
+          bulk_load(dst + B_BYTES, src + B_BYTES, B_BYTES, &full_bar[s]);
+        }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == MMA_WARP) {
     // ---- MMA issuer ------------------------------------------------------
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_tf32(BM, BN);
@@ -295,6 +320,9 @@ __global__ void __launch_bounds__(THREADS, 1) svm_tc_kernel(const Args a) {
     for (int p = 0; p < a.pairs; ++p) dec[p] = 0.0;
     float err_sum = 0.0f, err_sq = 0.0f;
     int cur = -1;
+    const bool rbf = a.kernel == CMLB_SVM_RBF;
+    const float neg_gl2 = -a.gamma * 1.4426950408889634f;
+    const float alpha = a.gamma * 1.075e-6f * nx + 1.077e-6f;
     // fp32 partial sums over <= 8 columns, folded into the fp64 class sums:
     // each adds at most 2^-21 sum|w K| of error, charged to the bound below
     auto fold = [&]() {
@@ -315,6 +343,7 @@ __global__ void __launch_bounds__(THREADS, 1) svm_tc_kernel(const Args a) {
           ns_s[i] = __ldg(a.ns + j0 + i);
           wm_s[i] = __ldg(a.wmax + j0 + i);
           cls_s[i] = __ldg(a.cls + j0 + i);
+          q_s[i] = __ldg(a.qerr + j0 + i);
         }
       }
       named_bar_sync(1, EPI_THREADS);
@@ -324,27 +353,48 @@ __global__ void __launch_bounds__(THREADS, 1) svm_tc_kernel(const Args a) {
       for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 32) {
         uint32_t g[32];
         tmem_ld32(taddr + (uint32_t)c0, g);
+        if (a.probe & 4) continue;
 #pragma unroll
         for (int grp = 0; grp < 4; ++grp) {
+          const int jg = c0 + grp * 8;
+          if (rbf && cls_s[jg] == cur && cls_s[jg + 7] == cur) {
+            // common case: 8 SVs of the current class, RBF -- branch-free.
+            // b_j = K_j * (wmax_j * alpha + q_j) is the per-SV bound of
+            // kvalue_fast (Gram error, d2 rounding, ex2, fp32 partials)
 #pragma unroll
-          for (int jj = 0; jj < 8; ++jj) {
-            const int j = c0 + grp * 8 + jj;
-            const int c = cls_s[j];
-            if (c != cur) {  // uniform: classes are contiguous
-              fold();
-              flush<CP>(a, cur, acc, dec);
+            for (int jj = 0; jj < 8; ++jj) {
+              const int j = jg + jj;
+              const float d2 = fmaxf(fmaf(-2.0f, __uint_as_float(g[grp * 8 + jj]), nx + ns_s[j]), 0.0f);
+              float k;
+              asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(k) : "f"(neg_gl2 * d2));
+              const float bj = k * fmaf(wm_s[j], alpha, q_s[j]);
+              err_sum += bj;
+              err_sq = fmaf(bj, bj, err_sq);
+              const float* wj = w_s + j * CPS;
 #pragma unroll
-              for (int o = 0; o < CP; ++o) acc[o] = 0.0;
-              cur = c;
+              for (int o = 0; o < CP; ++o) pacc[o] = fmaf(wj[o], k, pacc[o]);
             }
-            float ek;
-            const float k = kvalue_fast(a, __uint_as_float(g[grp * 8 + jj]), nx, ns_s[j], ek);
-            const float we = wm_s[j] * (ek + 4.76837158203125e-07f * fabsf(k));
-            err_sum += we;
-            err_sq = fmaf(we, we, err_sq);
-            const float* wj = w_s + j * CPS;
+          } else {
 #pragma unroll
-            for (int o = 0; o < CP; ++o) pacc[o] = fmaf(wj[o], k, pacc[o]);
+            for (int jj = 0; jj < 8; ++jj) {
+              const int j = jg + jj;
+              const int c = cls_s[j];
+              if (c != cur) {  // uniform: classes are contiguous
+                fold();
+                flush<CP>(a, cur, acc, dec);
+#pragma unroll
+                for (int o = 0; o < CP; ++o) acc[o] = 0.0;
+                cur = c;
+              }
+              float ek;
+              const float k = kvalue_fast(a, __uint_as_float(g[grp * 8 + jj]), nx, ns_s[j], ek);
+              const float we = wm_s[j] * (ek + 4.76837158203125e-07f * fabsf(k));
+              err_sum += we;
+              err_sq = fmaf(we, we, err_sq);
+              const float* wj = w_s + j * CPS;
+#pragma unroll
+              for (int o = 0; o < CP; ++o) pacc[o] = fmaf(wj[o], k, pacc[o]);
+            }
           }
           fold();
         }
@@ -415,7 +465,7 @@ __global__ void __launch_bounds__(THREADS, 1) svm_tc_kernel(const Args a) {
   }
   // producers and the MMA warp: TMEM is released once the epilogue has
   // drained the last accumulator (its final tempty arrival)
-  if (warp == 5) {
+  if (warp == MMA_WARP) {
     if (NT >= 1) bar_wait(&tempty_bar[(NT - 1) & 1], ((NT - 1) >> 1) & 1);
     tc_fence_after();
     tmem_free(tmem, 512);
@@ -655,7 +705,7 @@ static int make_svm(const cmlb_svm_desc* d, int device, cmlb_svm** out) {
     for (int j = start[c]; j < start[c + 1]; ++j) cls[j] = c;
   // per-SV coefficient toward each other class (libsvm: SV of class c in
   // pair (c, o) uses coef[o-1] if c < o, else coef[o])
-  std::vector<float> w((size_t)NP * CPS, 0.0f), wmax(NP, 0.0f), ns(NP, 0.0f);
+  std::vector<float> w((size_t)NP * CPS, 0.0f), wmax(NP, 0.0f), ns(NP, 0.0f), qerr(NP, 0.0f);
   for (int j = 0; j < NSV; ++j) {
     const int c = cls[j];
     for (int o = 0; o < C; ++o) {
@@ -672,6 +722,7 @@ static int make_svm(const cmlb_svm_desc* d, int device, cmlb_svm** out) {
       s += v * v;
     }
     ns[j] = (float)s;
+    qerr[j] = (float)((double)wmax[j] * d->gamma * 1.075e-6 * s * (1.0 + 1e-6));
   }
   // SV splits in the UMMA core-matrix layout: [tile][kb][big|small][c][row][4]
   std::vector<uint8_t> bsplit((size_t)NT * KB * 2 * B_BYTES, 0);
@@ -709,7 +760,7 @@ static int make_svm(const cmlb_svm_desc* d, int device, cmlb_svm** out) {
   const uint8_t* bs = nullptr;
   const int32_t* ss = nullptr;
   if ((st = upload(m, bsplit, &bs)) || (st = upload(m, ns, &a.ns)) || (st = upload(m, w, &a.w)) ||
-      (st = upload(m, wmax, &a.wmax)) || (st = upload(m, cls, &a.cls)) || (st = upload(m, svv, &a.sv)) ||
+      (st = upload(m, wmax, &a.wmax)) || (st = upload(m, qerr, &a.qerr)) || (st = upload(m, cls, &a.cls)) || (st = upload(m, svv, &a.sv)) ||
       (st = upload(m, coef, &a.coef)) || (st = upload(m, ic, &a.intercept)) ||
       (st = upload(m, classes, &a.classes)) || (st = upload(m, start, &ss))) {
     destroy_svm(m);
@@ -740,7 +791,7 @@ static int make_svm(const cmlb_svm_desc* d, int device, cmlb_svm** out) {
     }
     m->n_inputs = d->n_inputs;
   }
-  m->tc_smem = (size_t)STAGES * STAGE_BYTES + (size_t)BN * CPS * 4 + BN * 4 * 3;
+  m->tc_smem = (size_t)STAGES * STAGE_BYTES + (size_t)BN * CPS * 4 + BN * 4 * 4;
   m->x_smem = (size_t)F * XR * 8 + (size_t)XCH * XR * 8 + (size_t)XR * pairs * 8;
   if (m->x_smem > 227 * 1024) {
     destroy_svm(m);
@@ -839,6 +890,7 @@ int cmlb_svm_debug_fast(const cmlb_svm* m, const float* x, int64_t n_rows, int64
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   svm::Args a = m->a;
   a.x = x; a.n_rows = n_rows; a.ldx = ldx; a.y = y; a.dec_out = decision; a.err_out = err; a.no_exact = 1;
+  if (const char* pe = std::getenv("CMLB_SVM_PROBE")) a.probe = std::atoi(pe);
   a.vec_x = ((reinterpret_cast<uintptr_t>(x) & 15) == 0 && (ldx & 3) == 0) ? 1 : 0;
   void* scratch = nullptr;
   CMLB_CUDA(cudaMallocAsync(&scratch, (size_t)(n_rows + 4) * sizeof(int32_t), s));
