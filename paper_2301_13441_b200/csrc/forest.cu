@@ -146,6 +146,7 @@ struct ForestArgs {
   int stage_bufs;             // 1 or 2 staging buffers
   // MMA variant
   int mma_k, mma_n, mma_feat_off, mma_thr_off, mma_pay_off;
+  int probe;                  // debug (CMLB_MMA_PROBE): 1 skip compares, 2 skip blob TMA, 4 skip epilogue reads
 };
 
 constexpr int NT = 256;  // threads per CTA for every forest kernel
@@ -513,6 +514,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 }
 __device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
@@ -815,39 +819,49 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
          ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
 }
 
+// Warp-specialized kernel: the bit producer,
+// the tree-blob TMA, the tcgen05 issue and the TMEM epilogue run as separate
+// warp roles over double-buffered A operands, tree blobs and TMEM
+// accumulators, so tree t's MMAs overlap tree t+1's compares and tree t-1's
+// leaf selection.  Roles: warps 0-15 bit producers (a warp covers all 128
+// rows, four per lane, so one broadcast node load serves 128 compares),
+// warp 16 TMA (lane 0), warp 17 MMA issuer + TMEM owner, warps 18-25
+// epilogue (two per TMEM lane group, one column half each; thread = row).  The accumulation replays the same per-row order as the
+// serial kernel (tree t goes to pairwise lane t % 8).
+constexpr int MMA2_PROD = 512;                // 16 warps; each warp covers all 128 rows (4 per lane) for its chunks
+constexpr int MMA2_TMA_WARP = MMA2_PROD / 32, MMA2_MMA_WARP = MMA2_TMA_WARP + 1, MMA2_EPI_WARP0 = MMA2_MMA_WARP + 1;
+constexpr int MMA2_EPI = 256;                 // 8 warps: two per TMEM lane group, one column half each
+constexpr int MMA2_THREADS = MMA2_EPI_WARP0 * 32 + MMA2_EPI;
+
 template <int CT, bool PW>
-__global__ void __launch_bounds__(MMA_M, 1) forest_mma_kernel(const ForestArgs a) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ __align__(8) uint64_t blob_bar[2];
-  __shared__ __align__(8) uint64_t mma_bar;
+__global__ void __launch_bounds__(MMA2_THREADS, 1) forest_mma2_kernel(const ForestArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t blob_full[2], blob_empty[2], a_full[2], a_empty[2], t_full[2], t_empty[2];
   __shared__ uint32_t tmem_slot;
-  const int tid = threadIdx.x, warp = tid >> 5;
+  __shared__ int16_t leaf_x[2][MMA_M];   // column-half 1's candidate leaf, per accumulator buffer
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int F = a.F, T = a.T;
   const int K = a.mma_k, N = a.mma_n;
-  const int64_t row = (int64_t)blockIdx.x * MMA_M + tid;
-  const bool valid = row < a.n_rows;
-
-  float* xs = reinterpret_cast<float*>(smem);                 // [F][128]
+  const int64_t row0 = (int64_t)blockIdx.x * MMA_M;
+  float* xs = reinterpret_cast<float*>(smem);                        // [F][128]
   const uint32_t a_off = (uint32_t)(((size_t)F * MMA_M * 4 + 1023) & ~(size_t)1023);
-  uint8_t* A = smem + a_off;                                   // [K/16][128 rows][16 B]
-  const uint32_t buf0 = a_off + (uint32_t)K * MMA_M;
+  const uint32_t a_bytes = (uint32_t)K * MMA_M;                        // one A buffer
+  const uint32_t blob_off = a_off + 2 * a_bytes;
   const uint32_t blob_bytes = (uint32_t)a.tree_bytes;
-
-  // ---- rows -> shared memory (feature-major), dense-selector poisoning ---
-  {
-    const float* src = a.x + row * a.ldx;
-    for (int f = 0; f < F; ++f) xs[f * MMA_M + tid] = valid ? load_col(a.pro, src, f) : 0.0f;
-    if (a.dense_sel && valid) poison_row(xs, MMA_M, F, tid);
-  }
   if (tid == 0) {
-    mbar_init(&blob_bar[0], 1);
-    mbar_init(&blob_bar[1], 1);
-    mbar_init(&mma_bar, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&blob_full[b], 1);
+      mbar_init(&blob_empty[b], MMA2_PROD + 1);   // bit producers (feat/thr) + the MMA's commit (path matrix)
+      mbar_init(&a_full[b], MMA2_PROD);
+      mbar_init(&a_empty[b], 1);
+      mbar_init(&t_full[b], 1);
+      mbar_init(&t_empty[b], MMA2_EPI);
+    }
     mbar_fence_init();
   }
-  if (warp == 0) {
+  if (warp == MMA2_MMA_WARP) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n"
-                 ::"r"(smem_u32(&tmem_slot)), "r"(256) : "memory");
+                 ::"r"(smem_u32(&tmem_slot)), "r"(512) : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -855,102 +869,183 @@ __global__ void __launch_bounds__(MMA_M, 1) forest_mma_kernel(const ForestArgs a
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = tmem_slot;
 
-  auto issue_blob = [&](int t) {  // thread 0
-    uint8_t* dst = smem + buf0 + (uint32_t)(t & 1) * blob_bytes;
-    const uint8_t* src = a.blob + (size_t)t * blob_bytes;
-    fence_proxy_async();
-    mbar_expect_tx(&blob_bar[t & 1], blob_bytes);
-    for (uint32_t off = 0; off < blob_bytes; off += 32768u)
-      bulk_g2s(dst + off, src + off, min(32768u, blob_bytes - off), &blob_bar[t & 1]);
-  };
-  if (tid == 0) issue_blob(0);
-
-  RowAcc<CT, PW> acc;
-  acc.init();
-  // instruction descriptor: D s32, A u8, B s8, both K-major, N = mma_n, M = 128
-  const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(MMA_M >> 4) << 24);
-  const uint32_t a_base = smem_u32(smem) + a_off;
-
-  auto tree_step = [&](auto jconst, int t) {
-    constexpr int J = decltype(jconst)::value;
-    const int b = t & 1;
-    if (tid == 0 && t + 1 < T) issue_blob(t + 1);  // buffer freed by the previous iteration's barrier
-    mbar_wait(&blob_bar[b], (uint32_t)(t >> 1) & 1u);
-    const uint8_t* blob = smem + buf0 + (uint32_t)b * blob_bytes;
-    const uint16_t* feat = reinterpret_cast<const uint16_t*>(blob + a.mma_feat_off);
-    const float* thr = reinterpret_cast<const float*>(blob + a.mma_thr_off);
-    // producer: this row's went_right bits, 16 per 16-byte core-matrix row
-    for (int c = 0; c < K / 16; ++c) {
-      uint32_t wds[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int i = c * 16 + j;
-        uint32_t bit;
-        if (i < K - 1) bit = xs[feat[i] * MMA_M + tid] > thr[i] ? 1u : 0u;
-        else bit = 1u;  // bias column
-        wds[j >> 2] |= bit << (8 * (j & 3));
+  if (tid < MMA2_PROD) {
+    // ---- bit producers: warp w owns 16-bit chunks w, w + 8, ...; lane l
+    // owns rows l, l + 32, l + 64, l + 96, so each broadcast node load (one
+    // 8-byte word: xs offset + threshold) serves 128 compares
+    constexpr int PW_ = MMA2_PROD / 32;
+    {
+      for (int i = tid; i < F * MMA_M; i += MMA2_PROD) {
+        const int f = i / MMA_M, rr = i - f * MMA_M;
+        const int64_t rw = row0 + rr;
+        xs[i] = rw < a.n_rows ? load_col(a.pro, a.x + rw * a.ldx, f) : 0.0f;
       }
-      *reinterpret_cast<uint4*>(A + (size_t)c * (MMA_M * 16) + tid * 16) = make_uint4(wds[0], wds[1], wds[2], wds[3]);
+      asm volatile("bar.sync 1, %0;\n" ::"r"(MMA2_PROD) : "memory");
+      if (tid < MMA_M && a.dense_sel && row0 + tid < a.n_rows) poison_row(xs, MMA_M, F, tid);
+      asm volatile("bar.sync 1, %0;\n" ::"r"(MMA2_PROD) : "memory");
     }
-    fence_proxy_async();  // generic-proxy A writes -> visible to the tensor core
-    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-    __syncthreads();
-    if (tid == 0) {
+    const uint8_t* xsb = reinterpret_cast<const uint8_t*>(xs) + lane * 4;
+    for (int t = 0; t < T; ++t) {
+      const int b = t & 1;
+      const uint32_t u = (uint32_t)(t >> 1) & 1u;
+      mbar_wait(&blob_full[b], u);
+      mbar_wait(&a_empty[b], u ^ 1u);
+      const uint8_t* blob = smem + blob_off + (uint32_t)b * blob_bytes;
+      const uint2* node = reinterpret_cast<const uint2*>(blob + a.mma_feat_off);
+      uint8_t* A = smem + a_off + (uint32_t)b * a_bytes;
+      for (int c = warp; c < K / 16; c += PW_) {
+        if (a.probe & 1) break;
+        uint32_t wds[4][4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int w = 0; w < 4; ++w) wds[k][w] = 0u;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int i = c * 16 + j;
+          if (i < K - 1) {
+            const uint2 nd = node[i];
+            const float th = __uint_as_float(nd.y);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float xv = *reinterpret_cast<const float*>(xsb + nd.x + k * 128);
+              wds[k][j >> 2] |= (xv > th ? 1u : 0u) << (8 * (j & 3));
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) wds[k][j >> 2] |= 1u << (8 * (j & 3));  // bias column
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          *reinterpret_cast<uint4*>(A + (size_t)c * (MMA_M * 16) + (lane + 32 * k) * 16) =
+              make_uint4(wds[k][0], wds[k][1], wds[k][2], wds[k][3]);
+      }
+      fence_proxy_async();
+      mbar_arrive(&a_full[b]);
+      mbar_arrive(&blob_empty[b]);
+    }
+  } else if (warp == MMA2_TMA_WARP) {
+    // ---- tree blobs via TMA bulk copies ----------------------------------
+    if (lane == 0) {
+      for (int t = 0; t < T; ++t) {
+        const int b = t & 1;
+        mbar_wait(&blob_empty[b], ((uint32_t)(t >> 1) & 1u) ^ 1u);
+        uint8_t* dst = smem + blob_off + (uint32_t)b * blob_bytes;
+        const uint8_t* src = a.blob + (size_t)t * blob_bytes;
+        if ((a.probe & 2) && t >= 2) {
+          mbar_arrive(&blob_full[b]);
+          continue;
+        }
+        mbar_expect_tx(&blob_full[b], blob_bytes);
+        for (uint32_t off = 0; off < blob_bytes; off += 32768u)
+          bulk_g2s(dst + off, src + off, min(32768u, blob_bytes - off), &blob_full[b]);
+      }
+    }
+  } else if (warp == MMA2_MMA_WARP) {
+    // ---- MMA issuer: went-right bits x path matrix -> TMEM ---------------
+    if (lane == 0) {
+      const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(MMA_M >> 4) << 24);
+      for (int t = 0; t < T; ++t) {
+        const int b = t & 1;
+        const uint32_t u = (uint32_t)(t >> 1) & 1u;
+        mbar_wait(&a_full[b], u);
+        mbar_wait(&t_empty[b], u ^ 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint32_t a_base = smem_u32(smem) + a_off + (uint32_t)b * a_bytes;
+        const uint32_t b_base = smem_u32(smem) + blob_off + (uint32_t)b * blob_bytes;
+        const uint32_t d = tmem + (uint32_t)(b * 256);
+        for (int s = 0; s < K / 32; ++s) {
+          const uint64_t ad = umma_desc(a_base + (uint32_t)s * 2 * (MMA_M * 16), MMA_M * 16, 128);
+          const uint64_t bd = umma_desc(b_base + (uint32_t)s * 2 * (N * 16), (uint32_t)N * 16, 128);
+          asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                       " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n"
+                       ::"r"(d), "l"(ad), "l"(bd), "r"(idesc), "r"(s) : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+                     ::"r"(smem_u32(&a_empty[b])) : "memory");
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+                     ::"r"(smem_u32(&blob_empty[b])) : "memory");
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+                     ::"r"(smem_u32(&t_full[b])) : "memory");
+      }
+    }
+  } else {
+    // ---- epilogue: the selected leaf is the zero column ------------------
+    // Two warps per TMEM lane group scan one column half each; half 1 posts
+    // its candidate (or -1) in shared memory and half 0 -- which owns the
+    // row's accumulator -- takes the leaf, its payload and the sum.
+    const int e = warp - MMA2_EPI_WARP0;
+    const int eg = warp & 3, half = e >> 2;
+    const int r = eg * 32 + lane;
+    const int64_t row = row0 + r;
+    const bool valid = row < a.n_rows;
+    const int hN = ((N / 2) + 31) / 32 * 32;            // columns per half
+    const int cbeg = half * hN, cend = min(N, cbeg + hN);
+    RowAcc<CT, PW> acc;
+    acc.init();
+    auto step = [&](auto jconst, int t) {
+      constexpr int J = decltype(jconst)::value;
+      const int b = t & 1;
+      mbar_wait(&t_full[b], (uint32_t)(t >> 1) & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      const uint32_t b_base = smem_u32(blob);
-      for (int s = 0; s < K / 32; ++s) {
-        const uint64_t ad = umma_desc(a_base + (uint32_t)s * 2 * (MMA_M * 16), MMA_M * 16, 128);
-        const uint64_t bd = umma_desc(b_base + (uint32_t)s * 2 * (N * 16), (uint32_t)N * 16, 128);
-        asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-                     " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n"
-                     ::"r"(tmem), "l"(ad), "l"(bd), "r"(idesc), "r"(s) : "memory");
+      int leaf = -1;
+      const uint32_t lane_addr = tmem + ((uint32_t)(eg * 32) << 16) + (uint32_t)(b * 256);
+      for (int c0 = cbeg; c0 < ((a.probe & 4) ? cbeg : cend); c0 += 32) {
+        uint32_t rr[32];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                     "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+                     : "=r"(rr[0]), "=r"(rr[1]), "=r"(rr[2]), "=r"(rr[3]), "=r"(rr[4]), "=r"(rr[5]), "=r"(rr[6]),
+                       "=r"(rr[7]), "=r"(rr[8]), "=r"(rr[9]), "=r"(rr[10]), "=r"(rr[11]), "=r"(rr[12]), "=r"(rr[13]),
+                       "=r"(rr[14]), "=r"(rr[15]), "=r"(rr[16]), "=r"(rr[17]), "=r"(rr[18]), "=r"(rr[19]),
+                       "=r"(rr[20]), "=r"(rr[21]), "=r"(rr[22]), "=r"(rr[23]), "=r"(rr[24]), "=r"(rr[25]),
+                       "=r"(rr[26]), "=r"(rr[27]), "=r"(rr[28]), "=r"(rr[29]), "=r"(rr[30]), "=r"(rr[31])
+                     : "r"(lane_addr + (uint32_t)c0));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (c0 + j < cend && rr[j] == 0u) leaf = c0 + j;
       }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
-                   ::"r"(smem_u32(&mma_bar)) : "memory");
-    }
-    mbar_wait(&mma_bar, (uint32_t)t & 1u);
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    // epilogue: the selected leaf is the column whose score is zero
-    int leaf = 0;
-    const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
-    for (int c0 = 0; c0 < N; c0 += 32) {
-      uint32_t r[32];
-      asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                   "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-                   : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                     "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-                     "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-                     "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
-                     "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-                   : "r"(lane_addr + (uint32_t)c0));
-      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      mbar_arrive(&t_empty[b]);
+      if (half == 1) leaf_x[b][r] = (int16_t)leaf;
+      asm volatile("bar.sync %0, 64;\n" ::"r"(2 + eg) : "memory");  // the lane group's two warps
+      if (half == 1) return;
+      leaf = max(leaf, (int)leaf_x[b][r]);
+      leaf = max(leaf, 0);
+      // payload from the global tree blob (2 KB per tree, L1-resident): the
+      // smem blob is recycled as soon as the MMA has consumed it
+      const float* pay = reinterpret_cast<const float*>(a.blob + (size_t)t * blob_bytes + a.mma_pay_off);
+      float v[CT];
 #pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (c0 + j < N && r[j] == 0u) leaf = c0 + j;
+      for (int c = 0; c < CT; ++c) v[c] = __ldg(pay + leaf * CT + c);
+      if (a.leaf_out && valid) a.leaf_out[row * T + t] = leaf;
+      const uint32_t code = PW ? __ldg(a.sched + t) : 0u;
+      accumulate<J, CT>(acc, v, a.C, code);
+    };
+    for (int tg = 0; tg < T; tg += 8) {
+      step(std::integral_constant<int, 0>{}, tg);
+      if (tg + 1 < T) step(std::integral_constant<int, 1>{}, tg + 1);
+      if (tg + 2 < T) step(std::integral_constant<int, 2>{}, tg + 2);
+      if (tg + 3 < T) step(std::integral_constant<int, 3>{}, tg + 3);
+      if (tg + 4 < T) step(std::integral_constant<int, 4>{}, tg + 4);
+      if (tg + 5 < T) step(std::integral_constant<int, 5>{}, tg + 5);
+      if (tg + 6 < T) step(std::integral_constant<int, 6>{}, tg + 6);
+      if (tg + 7 < T) step(std::integral_constant<int, 7>{}, tg + 7);
     }
-    float v[CT];
-    load_payload<CT>(reinterpret_cast<const float*>(blob + a.mma_pay_off) + leaf * CT, v);
-    if (a.leaf_out && valid) a.leaf_out[row * T + t] = leaf;
-    const uint32_t code = PW ? __ldg(a.sched + t) : 0u;
-    accumulate<J, CT>(acc, v, a.C, code);
-    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-    __syncthreads();  // TMEM, A and this blob buffer are free again
-  };
-  for (int tg = 0; tg < T; tg += 8) {
-    tree_step(std::integral_constant<int, 0>{}, tg);
-    if (tg + 1 < T) tree_step(std::integral_constant<int, 1>{}, tg + 1);
-    if (tg + 2 < T) tree_step(std::integral_constant<int, 2>{}, tg + 2);
-    if (tg + 3 < T) tree_step(std::integral_constant<int, 3>{}, tg + 3);
-    if (tg + 4 < T) tree_step(std::integral_constant<int, 4>{}, tg + 4);
-    if (tg + 5 < T) tree_step(std::integral_constant<int, 5>{}, tg + 5);
-    if (tg + 6 < T) tree_step(std::integral_constant<int, 6>{}, tg + 6);
-    if (tg + 7 < T) tree_step(std::integral_constant<int, 7>{}, tg + 7);
+    if (half == 1) return;
+    float none[CT];
+#pragma unroll
+    for (int c = 0; c < CT; ++c) none[c] = 0.0f;
+    if (valid) finish_row<CT, PW>(a, row, acc, none);
   }
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(256) : "memory");
-  float none[CT];
-#pragma unroll
-  for (int c = 0; c < CT; ++c) none[c] = 0.0f;
-  if (valid) finish_row<CT, PW>(a, row, acc, none);
+  // TMEM is released once the epilogue drained the last accumulator
+  if (warp == MMA2_MMA_WARP) {
+    const int tl = T - 1;
+    mbar_wait(&t_empty[tl & 1], (uint32_t)(tl >> 1) & 1u);
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512) : "memory");
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1070,10 +1165,10 @@ static KernelFn ranked_for(const cmlb_forest& f) {
 static KernelFn mma_for(const cmlb_forest& f) {
   const bool pw = f.C == 1 && f.agg != CMLB_AGG_NONE;
   switch (f.CT) {
-    case 1: return pw ? forest_mma_kernel<1, true> : forest_mma_kernel<1, false>;
-    case 2: return forest_mma_kernel<2, false>;
-    case 4: return forest_mma_kernel<4, false>;
-    case 8: return forest_mma_kernel<8, false>;
+    case 1: return pw ? forest_mma2_kernel<1, true> : forest_mma2_kernel<1, false>;
+    case 2: return forest_mma2_kernel<2, false>;
+    case 4: return forest_mma2_kernel<4, false>;
+    case 8: return forest_mma2_kernel<8, false>;
     default: return nullptr;
   }
 }
@@ -1237,11 +1332,14 @@ static void fill_mma(const cmlb_forest_desc* d, int t, int K, int N, int CT, int
     for (int n = mid[j]; n < hi; ++n) { B[bidx(n, j)] = 1; D[n] += 1; }
   }
   for (int n = 0; n < N; ++n) B[bidx(n, K - 1)] = n < L ? (int8_t)(-D[n]) : (int8_t)1;
-  uint16_t* feat = reinterpret_cast<uint16_t*>(blob + feat_off);
-  float* thr = reinterpret_cast<float*>(blob + thr_off);
+  // node table for the bit producers: {byte offset of the feature's row
+  // tile in xs (feature * 128 rows * 4 B), threshold}, one 8-byte word each
+  (void)thr_off;
+  uint32_t* node = reinterpret_cast<uint32_t*>(blob + feat_off);
   for (int i = 0; i < K - 1; ++i) {
-    feat[i] = i < I ? (uint16_t)d->feature[nb + i] : 0;
-    thr[i] = i < I ? d->threshold[nb + i] : std::numeric_limits<float>::infinity();
+    const float t = i < I ? d->threshold[nb + i] : std::numeric_limits<float>::infinity();
+    node[2 * i] = i < I ? (uint32_t)d->feature[nb + i] * (uint32_t)(MMA_M * 4) : 0u;
+    std::memcpy(&node[2 * i + 1], &t, 4);
   }
   float* pay = reinterpret_cast<float*>(blob + pay_off);
   for (int n = 0; n < L; ++n)
@@ -1402,11 +1500,11 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
     auto al = [](size_t v) { return (int)((v + 15) / 16 * 16); };
     f->mma_k = K; f->mma_n = N;
     f->mma_feat_off = al((size_t)N * K);
-    f->mma_thr_off = al((size_t)f->mma_feat_off + 2 * (size_t)(K - 1));
-    f->mma_pay_off = al((size_t)f->mma_thr_off + 4 * (size_t)(K - 1));
+    f->mma_thr_off = f->mma_feat_off;  // packed with the offsets (fill_mma)
+    f->mma_pay_off = al((size_t)f->mma_feat_off + 8 * (size_t)(K - 1));
     f->tree_bytes = al((size_t)f->mma_pay_off + 4 * (size_t)N * f->CT);
     const size_t xs = ((size_t)f->F * MMA_M * 4 + 1023) / 1024 * 1024;
-    f->smem = xs + (size_t)K * MMA_M + 2 * (size_t)f->tree_bytes;
+    f->smem = xs + 2 * (size_t)K * MMA_M + 2 * (size_t)f->tree_bytes;  // double-buffered A and tree blobs
     if (f->smem > SMEM_LIMIT) return fail(CMLB_E_UNRESOLVED, "MMA variant does not fit shared memory");
     f->rpt = 1;
     std::vector<uint8_t> blob((size_t)f->T * f->tree_bytes, 0);
@@ -1509,8 +1607,9 @@ static int run_forest(const cmlb_forest* f, const float* x, int64_t n_rows, int6
   KernelFn k = kernel_for(*f);
   a.mma_k = f->mma_k; a.mma_n = f->mma_n; a.mma_feat_off = f->mma_feat_off; a.mma_thr_off = f->mma_thr_off;
   a.mma_pay_off = f->mma_pay_off;
-  const int threads = f->variant == CMLB_FOREST_RANKED ? f->ntt : (f->variant == CMLB_FOREST_MMA ? MMA_M : NT);
-  const int64_t rows = (int64_t)threads * f->rpt;
+  if (const char* pe = getenv("CMLB_MMA_PROBE")) a.probe = atoi(pe);
+  const int threads = f->variant == CMLB_FOREST_RANKED ? f->ntt : (f->variant == CMLB_FOREST_MMA ? MMA2_THREADS : NT);
+  const int64_t rows = f->variant == CMLB_FOREST_MMA ? (int64_t)MMA_M : (int64_t)threads * f->rpt;
   const int64_t grid = ceil_div(n_rows, rows);
   if (grid > 0x7fffffff) return fail(CMLB_E_INPUT, "too many rows for one launch");
   k<<<(unsigned)grid, threads, f->smem, (cudaStream_t)stream>>>(a);
