@@ -480,22 +480,25 @@ __global__ void __launch_bounds__(LNT) linear_exact_rows_kernel(const LinearArgs
 // FMA chain (the n u |x| |w| bound of linear_cert_kernel applies verbatim);
 // FP32 work is 7,840 FMA per 784-feature row against 3,136 B of HBM reads, so
 // the kernel is HBM-bound.
+// (1024-thread blocks sharing one W copy measured slower: 64-register cap)
+constexpr int LR_NT = 128;
+
 template <int CM, int RPT>
-__global__ void __launch_bounds__(LNT) linear_rows_kernel(const LinearArgs a) {
+__global__ void __launch_bounds__(LR_NT, 4) linear_rows_kernel(const LinearArgs a) {
   constexpr int CE = (CM + 3) & ~3;
   extern __shared__ __align__(16) float wkm[];   // [F][CE]
   const int F = a.F, C = a.C;
-  for (int i = threadIdx.x; i < F * CE; i += LNT) {
+  for (int i = threadIdx.x; i < F * CE; i += LR_NT) {
     const int k = i / CE, c = i - k * CE;
     wkm[i] = c < C ? __ldg(a.w + (int64_t)c * F + k) : 0.0f;
   }
   __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * LNT * RPT + threadIdx.x;
+  const int64_t base = (int64_t)blockIdx.x * LR_NT * RPT + threadIdx.x;
   const float* rp[RPT];
   bool live[RPT];
 #pragma unroll
   for (int r = 0; r < RPT; ++r) {
-    const int64_t row = base + r * LNT;
+    const int64_t row = base + r * LR_NT;
     live[r] = row < a.n_rows;
     rp[r] = a.x + (live[r] ? row : 0) * a.ldx;
   }
@@ -506,7 +509,7 @@ __global__ void __launch_bounds__(LNT) linear_rows_kernel(const LinearArgs a) {
 #pragma unroll
     for (int c = 0; c < CM; ++c) acc[r][c] = 0.0f;
   }
-  constexpr int U = 4;  // float4 per row per step (16 features)
+  constexpr int U = 2;  // float4 per row per step (8 features), double-buffered
   float4 cur[RPT][U], nxt[RPT][U];
   auto load = [&](float4 (&dst)[RPT][U], int k0) {
 #pragma unroll
@@ -555,7 +558,7 @@ __global__ void __launch_bounds__(LNT) linear_rows_kernel(const LinearArgs a) {
 #pragma unroll
   for (int r = 0; r < RPT; ++r) {
     if (!live[r]) continue;
-    const int64_t row = base + r * LNT;
+    const int64_t row = base + r * LR_NT;
     const float xn = sqrtf(nx[r]) * 1.0625f;
     float z[CM], e[CM];
     bool ok = true;
@@ -712,7 +715,7 @@ int cmlb_linear_run(const cmlb_linear* m, const float* x, int64_t n_rows, int64_
              : cm == 12 ? linear_rows_kernel<12, 2> : linear_rows_kernel<16, 2>;
     const int rpt = 2;
     CMLB_CUDA(cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wbytes));
-    kr<<<(unsigned)ceil_div(n_rows, (int64_t)LNT * rpt), LNT, wbytes, s>>>(a);
+    kr<<<(unsigned)ceil_div(n_rows, (int64_t)LR_NT * rpt), LR_NT, wbytes, s>>>(a);
   } else {
     const int64_t grid = ceil_div(n_rows, rows);
     k<<<(unsigned)grid, LNT, 0, s>>>(a);
