@@ -1130,6 +1130,8 @@ static KernelFn pick4(bool perfect, bool xs) {
 struct RankedCfg { int ntt, rpt, ti; };
 constexpr RankedCfg RANKED_CFGS[] = {
     {512, 2, 2}, {512, 2, 4}, {1024, 1, 2}, {1024, 1, 4}, {256, 2, 2}, {256, 1, 2}, {128, 2, 2}, {512, 1, 2}};
+// (512x1 and 256x2 threads with 4 trees per step were measured on GBR1000 d10:
+// 6x slower than 512x1 with 2 -- register spills; tools/gbr_cfg_probe.sh)
 constexpr int N_RANKED_CFGS = sizeof(RANKED_CFGS) / sizeof(RANKED_CFGS[0]);
 
 template <int CT, bool PW>
