@@ -323,14 +323,14 @@ def main(argv=None):
                 "model": "sklearn RF500 max_depth=8 fit on make_classification(200k x 28), "
                          "bench_assets/rf500_d8.npz",
                 "rows_per_gpu": n, "trees": len(model.trees), "features": 28,
-                "parallelism": f"row-shard dp{world}", "variant": f"{info['variant']}-traversal",
+                "parallelism": f"row-shard dp{world}", "variant": info['variant'] + ("-path-matrix" if info['variant'] == "mma" else "-traversal"),
                 "chunk_trees": info["chunk_trees"], "rows_per_cta": info["rows_per_cta"],
                 "l2": "inputs 1.12 GB per step > 126 MB L2 (no flush needed)"},
             "roofline": {
                 "bound": "tensor", "achieved": achieved_tops, "peak": pk["int8_tops"], "unit": "TOPS",
                 "frac": achieved_tops / pk["int8_tops"], "traffic": traffic,
                 "basis": "GEMM-equivalent int8 work of the reference encoding, ops_row = sum_t 2*I_t*L_t "
-                         f"= {ops_row} (SURVEY 8d); kernel = traversal variant",
+                         f"= {ops_row} (SURVEY 8d); kernel = {info['variant']} variant",
                 "peak_source": pk["source"]["int8"],
                 "hbm": {"achieved": achieved_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
                         "frac": achieved_gbs / pk["hbm_gbs"], "bytes_row": BYTES_ROW,
