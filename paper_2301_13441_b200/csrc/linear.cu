@@ -424,39 +424,57 @@ __global__ void __launch_bounds__(LNT) linear_cert_kernel(const LinearArgs a) {
   }
 }
 
-// Persistent: one warp per queued row, float64 in the reference's order --
-// lane c runs output c's ascending-k FMA chain (kernels.py:95-100), x
-// arrives 32 features at a time by one coalesced load and shuffles.
+// Persistent: RPW queued rows per warp (two when C <= 16: one per half-warp),
+// float64 in the reference's order -- lane c of a row's lane group runs output
+// c's ascending-k FMA chain (kernels.py:95-100); x arrives 32 features at a
+// time by coalesced loads, converted once and shuffled within the group.
 template <int CM>
 __global__ void __launch_bounds__(LNT) linear_exact_rows_kernel(const LinearArgs a) {
+  constexpr int RPW = CM <= 16 ? 2 : 1;
+  constexpr int GL = 32 / RPW;                      // lanes per row group
   const int nq = *a.queue_len;
   const int lane = threadIdx.x & 31;
+  const int slot = lane / GL, c = lane % GL;
   const int64_t gw = ((int64_t)blockIdx.x * LNT + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * LNT) >> 5;
   const int F = a.F, C = a.C;
-  for (int64_t i = gw; i < nq; i += nw) {
-    const int64_t row = a.queue[i];
+  for (int64_t i0 = gw * RPW; i0 < nq; i0 += nw * RPW) {
+    const int64_t qi = i0 + slot;
+    const bool live = qi < nq;
+    const int64_t row = live ? a.queue[qi] : a.queue[i0];
     const float* src = a.x + row * a.ldx;
     double acc = 0.0;
-    const int c = lane;
     const float* wr = a.w + (int64_t)(c < C ? c : 0) * F;
     for (int k0 = 0; k0 < F; k0 += 32) {
       const int kn = min(32, F - k0);
-      const float xl = lane < kn ? load_col(a.pro, src, k0 + lane) : 0.0f;
-      float wv[32];  // this lane's coefficients for the 32 features, loaded up front
+      double xl[RPW == 2 ? 2 : 1];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) wv[j] = (j < kn && c < C) ? __ldg(wr + k0 + j) : 0.0f;
+      for (int h = 0; h < RPW; ++h) {
+        const int k = k0 + h * GL + c;
+        xl[h] = k < k0 + kn ? (double)load_col(a.pro, src, k) : 0.0;
+      }
+      float wv[32];  // this lane's coefficients for the 32 features, loaded up front
+      if (kn == 32 && c < C && ((reinterpret_cast<uintptr_t>(wr + k0) & 15) == 0)) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          const float4 q = __ldg(reinterpret_cast<const float4*>(wr + k0 + j));
+          wv[j] = q.x; wv[j + 1] = q.y; wv[j + 2] = q.z; wv[j + 3] = q.w;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) wv[j] = (j < kn && c < C) ? __ldg(wr + k0 + j) : 0.0f;
+      }
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        const double xv = (double)__shfl_sync(0xffffffffu, xl, j);
+        const double xv = __shfl_sync(0xffffffffu, xl[j / GL], slot * GL + (j % GL));
         if (j < kn && c < C && !(a.sparse && wv[j] == 0.0f)) acc = fma(xv, (double)wv[j], acc);
       }
     }
     float zl = c < C ? __fadd_rn(__double2float_rn(acc), __ldg(a.b + c)) : 0.0f;
     float z[CM];
 #pragma unroll
-    for (int q = 0; q < CM; ++q) z[q] = __shfl_sync(0xffffffffu, zl, q & 31);
-    if (lane == 0) {
+    for (int q = 0; q < CM; ++q) z[q] = __shfl_sync(0xffffffffu, zl, slot * GL + (q % GL));
+    if (c == 0 && live) {
       if (a.tail == CMLB_LIN_ARGMAX) {
         store_out(a.y, row, a.out_dt, a.classes[first_max<CM>(z, C)]);
       } else if (a.tail == CMLB_LIN_SIGMOID) {
@@ -468,8 +486,6 @@ __global__ void __launch_bounds__(LNT) linear_exact_rows_kernel(const LinearArgs
     }
   }
 }
-
-
 
 // Thread-per-row certified kernel (the default for class tails, F % 4 == 0):
 // each thread streams its rows' features straight from HBM with float4 loads
