@@ -281,6 +281,19 @@ int cmlb_columns_run(const cmlb_columns* c, const float* x, int64_t n_rows, int6
                      int64_t* bad_row, void* stream);
 void cmlb_columns_destroy(cmlb_columns* c);
 
+/* ------------------------------------------------------------------------ *
+ * Diagnostics (tests and measurement tools only; not on the predict path).
+ * ------------------------------------------------------------------------ */
+
+/* The numpy pairwise-sum replay codes the forest kernels use for C == 1
+ * ensembles (tests/test_native_abi.py checks them against numpy). */
+int cmlb_debug_pairwise_schedule(int64_t n, uint32_t* codes);
+/* SVM fast path only, on every row, with the epilogue's per-row error bound
+ * written to err (device float32 [n_rows]); CMLB_SVM_PROBE switches pipeline
+ * roles off (tools/svm_pipe_probe.py). */
+int cmlb_svm_debug_fast(const cmlb_svm* m, const float* x, int64_t n_rows, int64_t ldx, void* y, double* decision,
+                        float* err, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1609,7 +1609,11 @@ static int run_forest(const cmlb_forest* f, const float* x, int64_t n_rows, int6
   KernelFn k = kernel_for(*f);
   a.mma_k = f->mma_k; a.mma_n = f->mma_n; a.mma_feat_off = f->mma_feat_off; a.mma_thr_off = f->mma_thr_off;
   a.mma_pay_off = f->mma_pay_off;
-  if (const char* pe = getenv("CMLB_MMA_PROBE")) a.probe = atoi(pe);
+  static const int mma_probe = [] {  // measurement hook (tools/mma_pipe_probe.sh), read once
+    const char* pe = getenv("CMLB_MMA_PROBE");
+    return pe ? atoi(pe) : 0;
+  }();
+  a.probe = mma_probe;
   const int threads = f->variant == CMLB_FOREST_RANKED ? f->ntt : (f->variant == CMLB_FOREST_MMA ? MMA2_THREADS : NT);
   const int64_t rows = f->variant == CMLB_FOREST_MMA ? (int64_t)MMA_M : (int64_t)threads * f->rpt;
   const int64_t grid = ceil_div(n_rows, rows);
