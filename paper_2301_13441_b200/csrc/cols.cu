@@ -33,18 +33,29 @@ struct ColsArgs {
 };
 
 // One thread per 4 consecutive outputs of a row (y row-major): coalesced
-// stores; the raw row is gathered through L1.
+// float4 stores when rows are 16-byte multiples; the raw row is gathered
+// through L1 (consecutive threads share a row).
 __global__ void columns_kernel(const ColsArgs a) {
   const int groups = (a.n_out + 3) / 4;
   const int64_t total = a.n_rows * groups;
+  const bool vec = (a.n_out & 3) == 0 && (reinterpret_cast<uintptr_t>(a.y) & 15) == 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / groups;
     const int f0 = (int)(i - r * groups) * 4;
     const float* row = a.x + r * a.ldx;
     float* out = a.y + r * a.n_out + f0;
+    if (vec) {
+      float4 v;
+      v.x = load_col(a.ops, row, f0);
+      v.y = load_col(a.ops, row, f0 + 1);
+      v.z = load_col(a.ops, row, f0 + 2);
+      v.w = load_col(a.ops, row, f0 + 3);
+      __stcs(reinterpret_cast<float4*>(out), v);
+    } else {
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (f0 + q < a.n_out) out[q] = load_col(a.ops, row, f0 + q);
+      for (int q = 0; q < 4; ++q)
+        if (f0 + q < a.n_out) out[q] = load_col(a.ops, row, f0 + q);
+    }
   }
 }
 
