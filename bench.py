@@ -320,8 +320,8 @@ def main(argv=None):
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {
                 "workload": f"RandomForestClassifier 500 trees depth 8 on {n} x 28 fp32 rows per GPU",
-                "model": "sklearn RF500 max_depth=8 fit on make_classification(200k x 28), "
-                         "bench_assets/rf500_d8.npz",
+                "forest_source": "sklearn RF500 max_depth=8 fit on make_classification(200k x 28), "
+                                 "bench_assets/rf500_d8.npz",
                 "rows_per_gpu": n, "trees": len(model.trees), "features": 28,
                 "parallelism": f"row-shard dp{world}", "variant": info['variant'] + ("-path-matrix" if info['variant'] == "mma" else "-traversal"),
                 "chunk_trees": info["chunk_trees"], "rows_per_cta": info["rows_per_cta"],
