@@ -45,3 +45,31 @@ def test_config5_pipeline_all_5m_rows_bit_exact():
     want, _ = fast.forest_predict(fast.PackedForest(forest), xt)
     mism = np.flatnonzero(got != want.ravel())
     assert mism.size == 0, f"{mism.size} of {len(xh)} rows differ"
+
+
+def test_config3_gbr_all_1m_rows_bit_exact():
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from bench_configs import perfect_gbdt
+    from paper_2301_13441_b200 import api
+    m = perfect_gbdt()
+    x = torch.randn((1_000_000, 90), generator=torch.Generator(device="cuda").manual_seed(2), device="cuda")
+    got = api.compile_model(m).program(0).run(x).cpu().numpy().astype(np.float64).ravel()
+    want, _ = fast.forest_predict(fast.PackedForest(m), x.cpu().numpy())
+    mism = np.flatnonzero(got != want.ravel())
+    assert mism.size == 0, f"{mism.size} rows differ"
+
+
+def test_config4a_logreg_all_1m_rows_bit_exact():
+    from oracle import semantics as sem
+    from paper_2301_13441_b200 import api
+    from paper_2301_13441_b200.models import LinearModel
+    rng = np.random.default_rng(3)
+    lm = LinearModel("logistic_regression", 784,
+                     tuple(tuple(float(v) for v in r) for r in rng.standard_normal((10, 784)).astype(np.float32) * 0.05),
+                     tuple(float(v) for v in rng.standard_normal(10).astype(np.float32)), tuple(float(c) for c in range(10)))
+    x = torch.randn((1_000_000, 784), generator=torch.Generator(device="cuda").manual_seed(3), device="cuda")
+    got = api.compile_model(lm).program(0).run(x).cpu().numpy().astype(np.float64).ravel()
+    xh = x.cpu().numpy()
+    want = np.concatenate([sem.predict(lm, xh[i:i + 100_000])[0].ravel() for i in range(0, len(xh), 100_000)])
+    mism = np.flatnonzero(got != want)
+    assert mism.size == 0, f"{mism.size} rows differ"
