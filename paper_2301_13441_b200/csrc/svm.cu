@@ -477,13 +477,20 @@ __global__ void __launch_bounds__(THREADS, 1) svm_tc_kernel(const Args a) {
 // ---------------------------------------------------------------------------
 
 // OpenBLAS SkylakeX ddot order (oracle/svm_oracle.c: ddot_skx) for one
-// (row, SV) pair; xs = the row's features in shared memory (float64, column
-// stride XR), s = the SV in float64.  RBF: the vectors are d = x - s
+// (row, SV) pair; xs = the row's features in shared memory (float64, one
+// padded row), s = the SV in float64.  RBF: the vectors are d = x - s
 // (ddot(d, d)); otherwise ddot(x, s).
 __device__ double exact_dot(const double* xs, const double* s, int F, bool rbf) {
   const int n1 = F & -16, n32 = n1 & ~31;
   auto term = [&](int k, double acc) {
-    const double xv = xs[k * XR], sv = __ldg(s + k);
+    const double xv = xs[k], sv = __ldg(s + k);
+    if (rbf) {
+      const double d = __dsub_rn(xv, sv);
+      return fma(d, d, acc);
+    }
+    return fma(xv, sv, acc);
+  };
+  auto term2 = [&](double xv, double sv, double acc) {
     if (rbf) {
       const double d = __dsub_rn(xv, sv);
       return fma(d, d, acc);
@@ -492,14 +499,27 @@ __device__ double exact_dot(const double* xs, const double* s, int F, bool rbf) 
   };
   // stream k in order: element k feeds lane k % 32 of the 4 x 8 AVX-512
   // accumulators (32 independent FMA chains), then lane k % 16 of the
-  // 4 x 4 AVX2 ones
+  // 4 x 4 AVX2 ones; x (padded shared-memory row) and the SV are read two
+  // doubles at a time when F is even
   double a8[32];
 #pragma unroll
   for (int u = 0; u < 32; ++u) a8[u] = 0.0;
   int k = 0;
-  for (; k < n32; k += 32) {
+  if ((F & 1) == 0) {
+    for (; k < n32; k += 32) {
 #pragma unroll
-    for (int u = 0; u < 32; ++u) a8[u] = term(k + u, a8[u]);
+      for (int u = 0; u < 32; u += 2) {
+        const double2 xv = *reinterpret_cast<const double2*>(xs + k + u);
+        const double2 sv = __ldg(reinterpret_cast<const double2*>(s + k + u));
+        a8[u] = term2(xv.x, sv.x, a8[u]);
+        a8[u + 1] = term2(xv.y, sv.y, a8[u + 1]);
+      }
+    }
+  } else {
+    for (; k < n32; k += 32) {
+#pragma unroll
+      for (int u = 0; u < 32; ++u) a8[u] = term(k + u, a8[u]);
+    }
   }
   double a4[16];
 #pragma unroll
@@ -536,8 +556,9 @@ constexpr int XTHREADS = 256;
 
 __global__ void __launch_bounds__(XTHREADS) svm_exact_kernel(const Args a, const int* n_sv_start) {
   extern __shared__ __align__(16) uint8_t xsm[];
-  double* xs = reinterpret_cast<double*>(xsm);                       // [F][XR]
-  double* kv = xs + (size_t)a.F * XR;                                 // [XCH][XR]
+  const int xstr = a.F + 2;                                           // padded row stride (doubles)
+  double* xs = reinterpret_cast<double*>(xsm);                       // [XR][xstr] row-major
+  double* kv = xs + (size_t)xstr * XR;                                // [XCH][XR]
   double* decs = kv + XCH * XR;                                      // [XR][pairs]
   __shared__ int32_t rows[XR];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -550,8 +571,8 @@ __global__ void __launch_bounds__(XTHREADS) svm_exact_kernel(const Args a, const
     if (tid < XR) rows[tid] = tid < nb ? a.queue[b0 + tid] : -1;
     __syncthreads();
     for (int i = tid; i < a.F * XR; i += XTHREADS) {
-      const int k = i / XR, r = i % XR;
-      xs[i] = rows[r] >= 0 ? (double)load_col(a.pro, a.x + (int64_t)rows[r] * a.ldx, k) : 0.0;
+      const int r = i / a.F, k = i - r * a.F;
+      xs[(size_t)r * xstr + k] = rows[r] >= 0 ? (double)load_col(a.pro, a.x + (int64_t)rows[r] * a.ldx, k) : 0.0;
     }
     double sum[4];
     for (int q = 0; q < 4; ++q) sum[q] = 0.0;
@@ -562,7 +583,7 @@ __global__ void __launch_bounds__(XTHREADS) svm_exact_kernel(const Args a, const
       // lane % XR = row
       constexpr int SPW = 32 / XR;
       for (int jj = SPW * warp + lane / XR; jj < nj; jj += SPW * (XTHREADS / 32))
-        kv[jj * XR + (lane % XR)] = exact_k(a, xs + (lane % XR), a.sv + (size_t)(j0 + jj) * a.F);
+        kv[jj * XR + (lane % XR)] = exact_k(a, xs + (size_t)(lane % XR) * xstr, a.sv + (size_t)(j0 + jj) * a.F);
       __syncthreads();
       // sequential decision sums in libsvm order, one (row, pair) per slot
       for (int q = 0; q < TPT; ++q) {
@@ -792,7 +813,7 @@ static int make_svm(const cmlb_svm_desc* d, int device, cmlb_svm** out) {
     m->n_inputs = d->n_inputs;
   }
   m->tc_smem = (size_t)STAGES * STAGE_BYTES + (size_t)BN * CPS * 4 + BN * 4 * 4;
-  m->x_smem = (size_t)F * XR * 8 + (size_t)XCH * XR * 8 + (size_t)XR * pairs * 8;
+  m->x_smem = (size_t)(F + 2) * XR * 8 + (size_t)XCH * XR * 8 + (size_t)XR * pairs * 8;
   if (m->x_smem > 227 * 1024) {
     destroy_svm(m);
     return fail(CMLB_E_UNRESOLVED, "svm exact path: features x classes exceed shared memory");
