@@ -487,6 +487,51 @@ __global__ void __launch_bounds__(LNT) linear_exact_rows_kernel(const LinearArgs
   }
 }
 
+// Certified class decision for one row from its float32 logit accumulators
+// (sequential FMA chains) and sum of squares: store the label, or queue the
+// row for the float64 recompute when the n u |x| |w| bound cannot settle it.
+template <int CM>
+__device__ __forceinline__ void cert_finish(const LinearArgs& a, int64_t row, const float (&acc)[CM], float nxr) {
+  const int C = a.C;
+  const float nu = (float)(a.F + 2) * 5.9604644775390625e-08f;
+  const float xn = sqrtf(nxr) * 1.0625f;
+  float z[CM], e[CM];
+  bool ok = true;
+#pragma unroll
+  for (int c = 0; c < CM; ++c) {
+    if (c < C) {
+      z[c] = __fadd_rn(acc[c], __ldg(a.b + c));
+      e[c] = nu * xn * __ldg(a.wnorm + c) + 2.4e-7f * (fabsf(acc[c]) + fabsf(z[c]));
+      ok = ok && (z[c] - z[c] == 0.0f) && (e[c] < 3.0e38f);
+    } else {
+      z[c] = 0.0f;
+      e[c] = 0.0f;
+    }
+  }
+  if (ok) {
+    if (a.tail == CMLB_LIN_ARGMAX) {
+      const int t = first_max<CM>(z, C);
+      float zt = z[0], et = e[0];
+#pragma unroll
+      for (int c = 1; c < CM; ++c)
+        if (c == t) { zt = z[c]; et = e[c]; }
+#pragma unroll
+      for (int c = 0; c < CM; ++c)
+        if (c < C && c != t) ok = ok && (zt - z[c] > 2.0f * (et + e[c]));
+      if (ok) store_out(a.y, row, a.out_dt, a.classes[t]);
+    } else if (a.tail == CMLB_LIN_SIGMOID) {
+      if (z[0] - 2.0f * e[0] > 4.76837158203125e-07f) store_out(a.y, row, a.out_dt, a.classes[1]);
+      else if (z[0] + 2.0f * e[0] < 0.0f) store_out(a.y, row, a.out_dt, a.classes[0]);
+      else ok = false;
+    } else {
+      if (z[0] - 2.0f * e[0] > 0.0f) store_out(a.y, row, a.out_dt, a.classes[1]);
+      else if (z[0] + 2.0f * e[0] < 0.0f) store_out(a.y, row, a.out_dt, a.classes[0]);
+      else ok = false;
+    }
+  }
+  if (!ok) a.queue[atomicAdd(a.queue_len, 1)] = (int32_t)row;
+}
+
 // Thread-per-row certified kernel (the default for class tails, F % 4 == 0):
 // each thread streams its rows' features straight from HBM with float4 loads
 // (16 features in flight per row, double-buffered in registers; a warp's 32
@@ -570,43 +615,253 @@ __global__ void __launch_bounds__(LR_NT, 4) linear_rows_kernel(const LinearArgs 
 #pragma unroll
       for (int u = 0; u < U; ++u) cur[r][u] = nxt[r][u];
   }
-  const float nu = (float)(F + 2) * 5.9604644775390625e-08f;
 #pragma unroll
-  for (int r = 0; r < RPT; ++r) {
-    if (!live[r]) continue;
-    const int64_t row = base + r * LR_NT;
-    const float xn = sqrtf(nx[r]) * 1.0625f;
-    float z[CM], e[CM];
-    bool ok = true;
+  for (int r = 0; r < RPT; ++r)
+    if (live[r]) cert_finish<CM>(a, base + r * LR_NT, acc[r], nx[r]);
+}
+
+// Tiled variant of the thread-per-row kernel: a CTA owns NT consecutive rows
+// and streams them through shared memory in KC-feature slices with cp.async
+// (16-byte pieces; consecutive lanes fetch one row's contiguous slice, so
+// every request covers whole sectors) in an ST-deep ring; the CTA's warps
+// share one copy of W.  The 16-byte pieces land XOR-swizzled by row so the
+// thread-per-row float4 reads of a quarter warp (8 rows) hit eight distinct
+// 16-byte bank groups.  Arithmetic and the certificate are the rows kernel's.
+// Stage W ([C][F] float32, F % 4 == 0, 16-byte aligned) into shared memory
+// k-major as T [F][ldw] (zero for c >= C), with float4 loads issued eight at
+// a time so the copy costs a few L2 round trips, not one per element.
+template <typename T, int NTH>
+__device__ __forceinline__ void stage_w_kmajor(T* dst, int ldw, const float* w, int C, int F) {
+  const int n4 = C * F / 4;
+  for (int i0 = threadIdx.x; i0 < n4; i0 += NTH * 8) {
+    float4 v[8];
 #pragma unroll
-    for (int c = 0; c < CM; ++c) {
-      if (c < C) {
-        z[c] = __fadd_rn(acc[r][c], __ldg(a.b + c));
-        e[c] = nu * xn * __ldg(a.wnorm + c) + 2.4e-7f * (fabsf(acc[r][c]) + fabsf(z[c]));
-        ok = ok && (z[c] - z[c] == 0.0f) && (e[c] < 3.0e38f);
-      } else {
-        z[c] = 0.0f;
-        e[c] = 0.0f;
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * NTH;
+      v[u] = i < n4 ? __ldg(reinterpret_cast<const float4*>(w) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * NTH;
+      if (i < n4) {
+        const int c = (4 * i) / F, k = 4 * i - c * F;
+        dst[(k + 0) * ldw + c] = (T)v[u].x;
+        dst[(k + 1) * ldw + c] = (T)v[u].y;
+        dst[(k + 2) * ldw + c] = (T)v[u].z;
+        dst[(k + 3) * ldw + c] = (T)v[u].w;
       }
     }
-    if (ok) {
+  }
+  for (int i = threadIdx.x; i < F * (ldw - C); i += NTH) {   // padding columns
+    const int k = i / (ldw - C), c = C + i % (ldw - C);
+    dst[k * ldw + c] = (T)0;
+  }
+}
+
+template <int KC>
+__device__ __forceinline__ int lt_swz(int r, int p) {
+  if constexpr (KC == 32) return p ^ (r & 7);        // 128-byte rows
+  else return p ^ ((r >> 1) & 3);                     // 64-byte rows: two rows per line
+}
+
+template <int CM, int NT, int KC, int ST>
+__global__ void __launch_bounds__(NT, 1) linear_tile_kernel(const LinearArgs a) {
+  static_assert(KC == 16 || KC == 32, "slice width");
+  constexpr int CE = (CM + 3) & ~3, PC = KC / 4;      // 16-byte pieces per row slice
+  extern __shared__ __align__(16) float lsm[];
+  float* xt = lsm;                                   // [ST][NT][KC], swizzled
+  float* wkm = lsm + ST * NT * KC;                   // [F][CE]
+  const int F = a.F, C = a.C, tid = threadIdx.x;
+  const int nk = (F + KC - 1) / KC;
+  // persistent: this CTA's row tiles are blockIdx.x + i * gridDim.x; the
+  // slice stream (tile i, slice kc) runs through the ring without draining
+  // between tiles
+  const int64_t ntiles = (a.n_rows + NT - 1) / NT;
+  const int64_t total = ntiles > blockIdx.x ? ((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x) * nk : 0;
+  // issue cursor: this thread's PC pieces keep their row and column within a
+  // slice, so their source pointers are set once per tile and advanced by KC
+  int64_t iss_row0 = (int64_t)blockIdx.x * NT;
+  int iss_kc = 0;
+  int64_t iss_g = 0;
+  const float* isrc[PC];
+  uint32_t idst[PC];
+  bool irow[PC];
+  const uint32_t xt_s = (uint32_t)__cvta_generic_to_shared(xt);
+#pragma unroll
+  for (int j = 0; j < PC; ++j) {
+    const int c = tid + j * NT, r = c / PC, p = c % PC;
+    idst[j] = xt_s + (uint32_t)(r * KC + (lt_swz<KC>(r, p) << 2)) * 4u;
+  }
+  auto set_tile = [&]() {
+#pragma unroll
+    for (int j = 0; j < PC; ++j) {
+      const int c = tid + j * NT, r = c / PC, p = c % PC;
+      irow[j] = iss_row0 + r < a.n_rows;
+      isrc[j] = a.x + (irow[j] ? iss_row0 + r : 0) * a.ldx + 4 * p;
+    }
+  };
+  set_tile();
+  auto issue = [&]() {
+    if (iss_g < total) {
+      const uint32_t boff = (uint32_t)(iss_g % ST) * (NT * KC * 4);
+      const int k0 = iss_kc * KC;
+      const bool full = k0 + KC <= F;
+#pragma unroll
+      for (int j = 0; j < PC; ++j) {
+        const int p = (tid + j * NT) % PC;
+        const bool ok = irow[j] && (full || k0 + 4 * p < F);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(idst[j] + boff),
+                     "l"(ok ? isrc[j] + k0 : a.x), "r"(ok ? 16 : 0) : "memory");
+      }
+      if (++iss_kc == nk) {
+        iss_kc = 0;
+        iss_row0 += (int64_t)gridDim.x * NT;
+        set_tile();
+      }
+    }
+    ++iss_g;
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+#pragma unroll
+  for (int s = 0; s < ST - 1; ++s) issue();
+  stage_w_kmajor<float, NT>(wkm, CE, a.w, C, F);
+  float acc[CM], nx = 0.0f;
+#pragma unroll
+  for (int c = 0; c < CM; ++c) acc[c] = 0.0f;
+  int64_t row0 = (int64_t)blockIdx.x * NT;
+  int kc = 0;
+  for (int64_t g = 0; g < total; ++g) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(ST - 2) : "memory");
+    __syncthreads();               // slice g visible to all; slice g-1's buffer is free
+    issue();
+    const float* xr = xt + (int)(g % ST) * (NT * KC) + tid * KC;
+    const int k0 = kc * KC;
+    const int kn = min(KC, F - k0);
+#pragma unroll
+    for (int p = 0; p < PC; ++p) {
+      if (4 * p >= kn) break;
+      const float4 v = *reinterpret_cast<const float4*>(xr + (lt_swz<KC>(tid, p) << 2));
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float xv = e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
+        nx = fmaf(xv, xv, nx);
+        const float4* w4 = reinterpret_cast<const float4*>(wkm + (k0 + 4 * p + e) * CE);
+#pragma unroll
+        for (int c4 = 0; c4 < CE / 4; ++c4) {
+          const float4 w = w4[c4];
+          if (4 * c4 + 0 < CM) acc[4 * c4 + 0] = fmaf(xv, w.x, acc[4 * c4 + 0]);
+          if (4 * c4 + 1 < CM) acc[4 * c4 + 1] = fmaf(xv, w.y, acc[4 * c4 + 1]);
+          if (4 * c4 + 2 < CM) acc[4 * c4 + 2] = fmaf(xv, w.z, acc[4 * c4 + 2]);
+          if (4 * c4 + 3 < CM) acc[4 * c4 + 3] = fmaf(xv, w.w, acc[4 * c4 + 3]);
+        }
+      }
+    }
+    if (++kc == nk) {
+      if (row0 + tid < a.n_rows) cert_finish<CM>(a, row0 + tid, acc, nx);
+#pragma unroll
+      for (int c = 0; c < CM; ++c) acc[c] = 0.0f;
+      nx = 0.0f;
+      kc = 0;
+      row0 += (int64_t)gridDim.x * NT;
+    }
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+struct TileCfg { int nt, kc, st; };
+static const TileCfg kTileCfg[] = {{128, 32, 4}, {512, 16, 4}, {512, 16, 3}, {256, 32, 3}, {256, 16, 6}};
+
+template <int CM>
+static LinFn tile_fn(int cfg) {
+  switch (cfg) {
+    case 0: return linear_tile_kernel<CM, 128, 32, 4>;
+    case 1: return linear_tile_kernel<CM, 512, 16, 4>;
+    case 2: return linear_tile_kernel<CM, 512, 16, 3>;
+    case 3: return linear_tile_kernel<CM, 256, 32, 3>;
+    default: return linear_tile_kernel<CM, 256, 16, 6>;
+  }
+}
+
+// Float64 recompute of the queued rows (C <= 16, no prologue, float4-aligned
+// rows), one thread per (row, output): thread (r, c) runs output c's
+// ascending-k FMA chain of row r (kernels.py:95-100) -- the same arithmetic
+// as linear_exact_rows_kernel.  A CTA takes LX_R queued rows x 16 output
+// slots; W sits in shared memory as float64 [F][16] (a half warp reads 128
+// contiguous bytes per feature), and the rows stream through a cp.async ring
+// of 32-feature slices (a half warp's x value is one broadcast read).  Many
+// short independent chains per SM keep the float64 pipe fed.
+constexpr int LX_R = 16, LX_ST = 4, LX_NT = LX_R * 16;
+
+__global__ void __launch_bounds__(LX_NT) linear_exact_lanes_kernel(const LinearArgs a) {
+  extern __shared__ __align__(16) double wq[];        // [F][16], then the x ring [LX_ST][LX_R][32]
+  const int nq = *a.queue_len;
+  const int64_t first = (int64_t)blockIdx.x * LX_R;
+  if (first >= nq) return;
+  const int F = a.F, C = a.C, tid = threadIdx.x;
+  stage_w_kmajor<double, LX_NT>(wq, 16, a.w, C, F);
+  float* ring = reinterpret_cast<float*>(wq + F * 16);
+  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
+  const int r = tid >> 4, c = tid & 15;
+  const int nk = (F + 31) / 32;
+  __syncthreads();
+  for (int64_t qb = first; qb < nq; qb += (int64_t)gridDim.x * LX_R) {
+    const int64_t qi = qb + r;
+    const bool live = qi < nq;
+    const int64_t row = a.queue[live ? qi : qb];
+    // pieces: thread t < LX_R * 8 fetches row t / 8's piece t % 8 of each slice
+    const int pr = tid >> 3, pp = tid & 7;
+    const int64_t prow = tid < LX_R * 8 ? a.queue[qb + pr < nq ? qb + pr : qb] : 0;
+    const float* psrc = a.x + prow * a.ldx + 4 * pp;
+    auto issue = [&](int kc) {
+      if (kc < nk && tid < LX_R * 8) {
+        const int k0 = kc * 32;
+        const bool ok = k0 + 4 * pp < F;
+        const uint32_t d = ring_s + (uint32_t)(((kc % LX_ST) * LX_R + pr) * 32 + 4 * pp) * 4u;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(ok ? psrc + k0 : a.x),
+                     "r"(ok ? 16 : 0) : "memory");
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+#pragma unroll
+    for (int s2 = 0; s2 < LX_ST - 1; ++s2) issue(s2);
+    double acc = 0.0;
+    const bool act = c < C;
+    for (int kc = 0; kc < nk; ++kc) {
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(LX_ST - 2) : "memory");
+      __syncthreads();
+      issue(kc + LX_ST - 1);
+      const float* xs = ring + ((kc % LX_ST) * LX_R + r) * 32;
+      const int k0 = kc * 32, kn = min(32, F - k0);
+      const double* wk = wq + k0 * 16 + c;
+      if (kn == 32) {
+#pragma unroll 8
+        for (int j = 0; j < 32; ++j) {
+          const double w = wk[j * 16];
+          if (act && !(a.sparse && w == 0.0)) acc = fma((double)xs[j], w, acc);
+        }
+      } else {
+        for (int j = 0; j < kn; ++j) {
+          const double w = wk[j * 16];
+          if (act && !(a.sparse && w == 0.0)) acc = fma((double)xs[j], w, acc);
+        }
+      }
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();               // ring free before the next batch's prologue
+    const float zl = act ? __fadd_rn(__double2float_rn(acc), __ldg(a.b + c)) : 0.0f;
+    float z[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) z[q] = __shfl_sync(0xffffffffu, zl, (tid & 16) + q);
+    if (c == 0 && live) {
       if (a.tail == CMLB_LIN_ARGMAX) {
-        const int t = first_max<CM>(z, C);
-#pragma unroll
-        for (int c = 0; c < CM; ++c)
-          if (c < C && c != t) ok = ok && (z[t] - z[c] > 2.0f * (e[t] + e[c]));
-        if (ok) store_out(a.y, row, a.out_dt, a.classes[t]);
+        store_out(a.y, row, a.out_dt, a.classes[first_max<16>(z, C)]);
       } else if (a.tail == CMLB_LIN_SIGMOID) {
-        if (z[0] - 2.0f * e[0] > 4.76837158203125e-07f) store_out(a.y, row, a.out_dt, a.classes[1]);
-        else if (z[0] + 2.0f * e[0] < 0.0f) store_out(a.y, row, a.out_dt, a.classes[0]);
-        else ok = false;
+        const float pz = __double2float_rn(ref_sigmoid((double)z[0]));
+        store_out(a.y, row, a.out_dt, a.classes[pz > 0.5f ? 1 : 0]);
       } else {
-        if (z[0] - 2.0f * e[0] > 0.0f) store_out(a.y, row, a.out_dt, a.classes[1]);
-        else if (z[0] + 2.0f * e[0] < 0.0f) store_out(a.y, row, a.out_dt, a.classes[0]);
-        else ok = false;
+        store_out(a.y, row, a.out_dt, a.classes[z[0] > 0.0f ? 1 : 0]);
       }
     }
-    if (!ok) a.queue[atomicAdd(a.queue_len, 1)] = (int32_t)row;
   }
 }
 
@@ -723,15 +978,31 @@ int cmlb_linear_run(const cmlb_linear* m, const float* x, int64_t n_rows, int64_
     CMLB_CUDA(cudaMemsetAsync(a.queue_len, 0, sizeof(int32_t), s));
   }
   // thread-per-row certified kernel when rows are float4-aligned and W fits
-  const int cm = m->C <= 2 ? 2 : m->C <= 4 ? 4 : m->C <= 8 ? 8 : m->C <= 12 ? 12 : 16;
+  const int cm = m->C <= 2 ? 2 : m->C <= 4 ? 4 : m->C <= 8 ? 8 : m->C <= 10 ? 10 : m->C <= 12 ? 12 : 16;
   const size_t wbytes = (size_t)m->F * ((cm + 3) & ~3) * 4;
   const bool aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (ldx % 4) == 0 && (m->F % 4) == 0;
   if (fixup && !m->pro && m->C <= 16 && aligned && wbytes <= 100 * 1024) {
-    LinFn kr = cm == 2 ? linear_rows_kernel<2, 2> : cm == 4 ? linear_rows_kernel<4, 2> : cm == 8 ? linear_rows_kernel<8, 2>
-             : cm == 12 ? linear_rows_kernel<12, 2> : linear_rows_kernel<16, 2>;
-    const int rpt = 2;
-    CMLB_CUDA(cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wbytes));
-    kr<<<(unsigned)ceil_div(n_rows, (int64_t)LR_NT * rpt), LR_NT, wbytes, s>>>(a);
+    static const int lin_impl = [] {
+      const char* e = std::getenv("CMLB_LINEAR_IMPL");
+      return e ? std::atoi(e) : 1;
+    }();
+    if (lin_impl >= 1) {
+      const int cfg = std::min(lin_impl - 1, 4);
+      LinFn kt = cm == 2 ? tile_fn<2>(cfg) : cm == 4 ? tile_fn<4>(cfg) : cm == 8 ? tile_fn<8>(cfg)
+               : cm == 10 ? tile_fn<10>(cfg) : cm == 12 ? tile_fn<12>(cfg) : tile_fn<16>(cfg);
+      const TileCfg tc = kTileCfg[cfg];
+      const size_t sb = (size_t)tc.st * tc.nt * tc.kc * 4 + wbytes;
+      CMLB_CUDA(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+      const int per_sm = tc.nt <= 128 ? 2 : 1;
+      const int64_t g = std::min<int64_t>(ceil_div(n_rows, (int64_t)tc.nt), (int64_t)num_sms(m->device) * per_sm);
+      kt<<<(unsigned)g, tc.nt, sb, s>>>(a);
+    } else {
+      LinFn kr = cm == 2 ? linear_rows_kernel<2, 2> : cm == 4 ? linear_rows_kernel<4, 2> : cm == 8 ? linear_rows_kernel<8, 2>
+               : cm == 10 ? linear_rows_kernel<10, 2> : cm == 12 ? linear_rows_kernel<12, 2> : linear_rows_kernel<16, 2>;
+      const int rpt = 2;
+      CMLB_CUDA(cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wbytes));
+      kr<<<(unsigned)ceil_div(n_rows, (int64_t)LR_NT * rpt), LR_NT, wbytes, s>>>(a);
+    }
   } else {
     const int64_t grid = ceil_div(n_rows, rows);
     k<<<(unsigned)grid, LNT, 0, s>>>(a);
@@ -739,8 +1010,18 @@ int cmlb_linear_run(const cmlb_linear* m, const float* x, int64_t n_rows, int64_
   note_launch();
   CMLB_CUDA(cudaGetLastError());
   if (fixup) {
-    const int g = (int)std::min<int64_t>(ceil_div(n_rows, LNT), (int64_t)num_sms(m->device) * 4);
-    fixup<<<g, LNT, 0, s>>>(a);
+    static const bool old_fix = std::getenv("CMLB_LINEAR_FIXUP_WARP") != nullptr;
+    const size_t xb = (size_t)m->F * 16 * 8 + (size_t)LX_ST * LX_R * 32 * 4;
+    if (!old_fix && m->C <= 16 && !m->pro && aligned && xb <= 200 * 1024) {
+      CMLB_CUDA(cudaFuncSetAttribute(linear_exact_lanes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xb));
+      int per_sm = 0;
+      CMLB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, linear_exact_lanes_kernel, LX_NT, xb));
+      const int g = (int)std::min<int64_t>(ceil_div(n_rows, (int64_t)LX_R), (int64_t)num_sms(m->device) * std::max(per_sm, 1));
+      linear_exact_lanes_kernel<<<g, LX_NT, xb, s>>>(a);
+    } else {
+      const int g = (int)std::min<int64_t>(ceil_div(n_rows, LNT), (int64_t)num_sms(m->device) * 4);
+      fixup<<<g, LNT, 0, s>>>(a);
+    }
     note_launch();
     CMLB_CUDA(cudaGetLastError());
     CMLB_CUDA(cudaFreeAsync(scratch, s));
