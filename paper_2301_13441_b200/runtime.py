@@ -350,12 +350,12 @@ class DeviceProgram:
             pass
 
 
-def run_host(program: DeviceProgram, x_host: torch.Tensor, chunk_rows: int = 1 << 19,
+def run_host(program: DeviceProgram, x_host: torch.Tensor, chunk_rows: int = 1 << 18,
              out_host: torch.Tensor | None = None, n_streams: int = 3) -> torch.Tensor:
     """Host (N, F) float32 -> host output, H2D / compute / D2H pipelined in
     row chunks over ``n_streams`` streams so transfers overlap the kernels.
-    Defaults measured on B200 for RF500 (tools/e2e_probe.py): 512K-row chunks
-    on 3 streams reach 463M rows/s, 93% of the 55 GB/s pinned H2D copy rate."""
+    Defaults measured on B200 for RF500 (tools/e2e_probe.py): 256K-row chunks
+    on 3 streams reach 473M rows/s, 96% of the 55 GB/s pinned H2D copy rate."""
     program.check_input(x_host)
     n = int(x_host.shape[0])
     dt = TORCH_DTYPE[program.out_dtype]

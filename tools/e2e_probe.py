@@ -27,7 +27,8 @@ torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(); d.copy_(x, non_blocking=True); e1.record(); torch.cuda.synchronize()
 print(json.dumps({"h2d_gbs": n * 112 / (e0.elapsed_time(e1) / 1e3) / 1e9}), flush=True)
-for chunk, ns in itertools.product((1 << 19, 1 << 20, 1 << 21, 1 << 22), (2, 3, 4)):
+CH = tuple(int(v) for v in os.environ.get("E2E_CHUNKS", str((1 << 19, 1 << 20, 1 << 21, 1 << 22))).strip("()").split(",") if v.strip())
+for chunk, ns in itertools.product(CH, (2, 3, 4)):
     run_host(prog, x[: chunk * ns], out_host=y[: chunk * ns], chunk_rows=chunk, n_streams=ns)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
