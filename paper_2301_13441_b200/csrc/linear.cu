@@ -620,7 +620,8 @@ __global__ void __launch_bounds__(LR_NT, 4) linear_rows_kernel(const LinearArgs 
     if (live[r]) cert_finish<CM>(a, base + r * LR_NT, acc[r], nx[r]);
 }
 
-// Tiled variant of the thread-per-row kernel: a CTA owns NT consecutive rows
+// Tiled variant of the thread-per-row kernel: a CTA owns NT * RPT consecutive rows
+// (RPT per thread, so each W broadcast read feeds RPT rows)
 // and streams them through shared memory in KC-feature slices with cp.async
 // (16-byte pieces; consecutive lanes fetch one row's contiguous slice, so
 // every request covers whole sectors) in an ST-deep ring; the CTA's warps
@@ -664,37 +665,39 @@ __device__ __forceinline__ int lt_swz(int r, int p) {
   else return p ^ ((r >> 1) & 3);                     // 64-byte rows: two rows per line
 }
 
-template <int CM, int NT, int KC, int ST>
+template <int CM, int NT, int KC, int ST, int RPT>
 __global__ void __launch_bounds__(NT, 1) linear_tile_kernel(const LinearArgs a) {
   static_assert(KC == 16 || KC == 32, "slice width");
   constexpr int CE = (CM + 3) & ~3, PC = KC / 4;      // 16-byte pieces per row slice
+  constexpr int TR = NT * RPT;                        // rows per tile; thread rows tid + k NT
   extern __shared__ __align__(16) float lsm[];
-  float* xt = lsm;                                   // [ST][NT][KC], swizzled
-  float* wkm = lsm + ST * NT * KC;                   // [F][CE]
+  float* xt = lsm;                                   // [ST][TR][KC], swizzled
+  float* wkm = lsm + ST * TR * KC;                   // [F][CE]
   const int F = a.F, C = a.C, tid = threadIdx.x;
   const int nk = (F + KC - 1) / KC;
   // persistent: this CTA's row tiles are blockIdx.x + i * gridDim.x; the
   // slice stream (tile i, slice kc) runs through the ring without draining
   // between tiles
-  const int64_t ntiles = (a.n_rows + NT - 1) / NT;
+  const int64_t ntiles = (a.n_rows + TR - 1) / TR;
   const int64_t total = ntiles > blockIdx.x ? ((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x) * nk : 0;
-  // issue cursor: this thread's PC pieces keep their row and column within a
-  // slice, so their source pointers are set once per tile and advanced by KC
-  int64_t iss_row0 = (int64_t)blockIdx.x * NT;
+  // issue cursor: this thread's RPT * PC pieces keep their row and column
+  // within a slice, so their source pointers are set once per tile
+  int64_t iss_row0 = (int64_t)blockIdx.x * TR;
   int iss_kc = 0;
   int64_t iss_g = 0;
-  const float* isrc[PC];
-  uint32_t idst[PC];
-  bool irow[PC];
+  constexpr int NP = RPT * PC;
+  const float* isrc[NP];
+  uint32_t idst[NP];
+  bool irow[NP];
   const uint32_t xt_s = (uint32_t)__cvta_generic_to_shared(xt);
 #pragma unroll
-  for (int j = 0; j < PC; ++j) {
+  for (int j = 0; j < NP; ++j) {
     const int c = tid + j * NT, r = c / PC, p = c % PC;
     idst[j] = xt_s + (uint32_t)(r * KC + (lt_swz<KC>(r, p) << 2)) * 4u;
   }
   auto set_tile = [&]() {
 #pragma unroll
-    for (int j = 0; j < PC; ++j) {
+    for (int j = 0; j < NP; ++j) {
       const int c = tid + j * NT, r = c / PC, p = c % PC;
       irow[j] = iss_row0 + r < a.n_rows;
       isrc[j] = a.x + (irow[j] ? iss_row0 + r : 0) * a.ldx + 4 * p;
@@ -703,11 +706,11 @@ __global__ void __launch_bounds__(NT, 1) linear_tile_kernel(const LinearArgs a) 
   set_tile();
   auto issue = [&]() {
     if (iss_g < total) {
-      const uint32_t boff = (uint32_t)(iss_g % ST) * (NT * KC * 4);
+      const uint32_t boff = (uint32_t)(iss_g % ST) * (TR * KC * 4);
       const int k0 = iss_kc * KC;
       const bool full = k0 + KC <= F;
 #pragma unroll
-      for (int j = 0; j < PC; ++j) {
+      for (int j = 0; j < NP; ++j) {
         const int p = (tid + j * NT) % PC;
         const bool ok = irow[j] && (full || k0 + 4 * p < F);
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(idst[j] + boff),
@@ -715,7 +718,7 @@ __global__ void __launch_bounds__(NT, 1) linear_tile_kernel(const LinearArgs a) 
       }
       if (++iss_kc == nk) {
         iss_kc = 0;
-        iss_row0 += (int64_t)gridDim.x * NT;
+        iss_row0 += (int64_t)gridDim.x * TR;
         set_tile();
       }
     }
@@ -725,60 +728,80 @@ __global__ void __launch_bounds__(NT, 1) linear_tile_kernel(const LinearArgs a) 
 #pragma unroll
   for (int s = 0; s < ST - 1; ++s) issue();
   stage_w_kmajor<float, NT>(wkm, CE, a.w, C, F);
-  float acc[CM], nx = 0.0f;
+  float acc[RPT][CM], nx[RPT];
 #pragma unroll
-  for (int c = 0; c < CM; ++c) acc[c] = 0.0f;
-  int64_t row0 = (int64_t)blockIdx.x * NT;
+  for (int q = 0; q < RPT; ++q) {
+    nx[q] = 0.0f;
+#pragma unroll
+    for (int c = 0; c < CM; ++c) acc[q][c] = 0.0f;
+  }
+  int64_t row0 = (int64_t)blockIdx.x * TR;
   int kc = 0;
   for (int64_t g = 0; g < total; ++g) {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(ST - 2) : "memory");
     __syncthreads();               // slice g visible to all; slice g-1's buffer is free
     issue();
-    const float* xr = xt + (int)(g % ST) * (NT * KC) + tid * KC;
+    const float* xb = xt + (int)(g % ST) * (TR * KC);
     const int k0 = kc * KC;
     const int kn = min(KC, F - k0);
 #pragma unroll
     for (int p = 0; p < PC; ++p) {
       if (4 * p >= kn) break;
-      const float4 v = *reinterpret_cast<const float4*>(xr + (lt_swz<KC>(tid, p) << 2));
+      float4 v[RPT];
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) {
+        const int r = tid + q * NT;
+        v[q] = *reinterpret_cast<const float4*>(xb + r * KC + (lt_swz<KC>(r, p) << 2));
+      }
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const float xv = e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
-        nx = fmaf(xv, xv, nx);
+        float xv[RPT];
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+          xv[q] = e == 0 ? v[q].x : e == 1 ? v[q].y : e == 2 ? v[q].z : v[q].w;
+          nx[q] = fmaf(xv[q], xv[q], nx[q]);
+        }
         const float4* w4 = reinterpret_cast<const float4*>(wkm + (k0 + 4 * p + e) * CE);
 #pragma unroll
         for (int c4 = 0; c4 < CE / 4; ++c4) {
           const float4 w = w4[c4];
-          if (4 * c4 + 0 < CM) acc[4 * c4 + 0] = fmaf(xv, w.x, acc[4 * c4 + 0]);
-          if (4 * c4 + 1 < CM) acc[4 * c4 + 1] = fmaf(xv, w.y, acc[4 * c4 + 1]);
-          if (4 * c4 + 2 < CM) acc[4 * c4 + 2] = fmaf(xv, w.z, acc[4 * c4 + 2]);
-          if (4 * c4 + 3 < CM) acc[4 * c4 + 3] = fmaf(xv, w.w, acc[4 * c4 + 3]);
+#pragma unroll
+          for (int q = 0; q < RPT; ++q) {
+            if (4 * c4 + 0 < CM) acc[q][4 * c4 + 0] = fmaf(xv[q], w.x, acc[q][4 * c4 + 0]);
+            if (4 * c4 + 1 < CM) acc[q][4 * c4 + 1] = fmaf(xv[q], w.y, acc[q][4 * c4 + 1]);
+            if (4 * c4 + 2 < CM) acc[q][4 * c4 + 2] = fmaf(xv[q], w.z, acc[q][4 * c4 + 2]);
+            if (4 * c4 + 3 < CM) acc[q][4 * c4 + 3] = fmaf(xv[q], w.w, acc[q][4 * c4 + 3]);
+          }
         }
       }
     }
     if (++kc == nk) {
-      if (row0 + tid < a.n_rows) cert_finish<CM>(a, row0 + tid, acc, nx);
 #pragma unroll
-      for (int c = 0; c < CM; ++c) acc[c] = 0.0f;
-      nx = 0.0f;
+      for (int q = 0; q < RPT; ++q) {
+        const int64_t row = row0 + tid + q * NT;
+        if (row < a.n_rows) cert_finish<CM>(a, row, acc[q], nx[q]);
+        nx[q] = 0.0f;
+#pragma unroll
+        for (int c = 0; c < CM; ++c) acc[q][c] = 0.0f;
+      }
       kc = 0;
-      row0 += (int64_t)gridDim.x * NT;
+      row0 += (int64_t)gridDim.x * TR;
     }
   }
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
-struct TileCfg { int nt, kc, st; };
-static const TileCfg kTileCfg[] = {{128, 32, 4}, {512, 16, 4}, {512, 16, 3}, {256, 32, 3}, {256, 16, 6}};
+struct TileCfg { int nt, kc, st, rpt, per_sm; };
+static const TileCfg kTileCfg[] = {{128, 32, 4, 1, 2}, {128, 16, 4, 2, 2}, {128, 16, 4, 4, 1}, {64, 16, 4, 4, 2}, {128, 16, 3, 2, 2}};
 
 template <int CM>
 static LinFn tile_fn(int cfg) {
   switch (cfg) {
-    case 0: return linear_tile_kernel<CM, 128, 32, 4>;
-    case 1: return linear_tile_kernel<CM, 512, 16, 4>;
-    case 2: return linear_tile_kernel<CM, 512, 16, 3>;
-    case 3: return linear_tile_kernel<CM, 256, 32, 3>;
-    default: return linear_tile_kernel<CM, 256, 16, 6>;
+    case 0: return linear_tile_kernel<CM, 128, 32, 4, 1>;
+    case 1: return linear_tile_kernel<CM, 128, 16, 4, 2>;
+    case 2: return linear_tile_kernel<CM, 128, 16, 4, 4>;
+    case 3: return linear_tile_kernel<CM, 64, 16, 4, 4>;
+    default: return linear_tile_kernel<CM, 128, 16, 3, 2>;
   }
 }
 
@@ -983,18 +1006,17 @@ int cmlb_linear_run(const cmlb_linear* m, const float* x, int64_t n_rows, int64_
   const bool aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (ldx % 4) == 0 && (m->F % 4) == 0;
   if (fixup && !m->pro && m->C <= 16 && aligned && wbytes <= 100 * 1024) {
     static const int lin_impl = [] {
-      const char* e = std::getenv("CMLB_LINEAR_IMPL");
-      return e ? std::atoi(e) : 1;
+      const char* e = std::getenv("CMLB_LINEAR_IMPL");   // 0: rows kernel; n >= 1: tile config n - 1
+      return e ? std::atoi(e) : 2;
     }();
     if (lin_impl >= 1) {
       const int cfg = std::min(lin_impl - 1, 4);
       LinFn kt = cm == 2 ? tile_fn<2>(cfg) : cm == 4 ? tile_fn<4>(cfg) : cm == 8 ? tile_fn<8>(cfg)
                : cm == 10 ? tile_fn<10>(cfg) : cm == 12 ? tile_fn<12>(cfg) : tile_fn<16>(cfg);
       const TileCfg tc = kTileCfg[cfg];
-      const size_t sb = (size_t)tc.st * tc.nt * tc.kc * 4 + wbytes;
+      const size_t sb = (size_t)tc.st * tc.nt * tc.rpt * tc.kc * 4 + wbytes;
       CMLB_CUDA(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
-      const int per_sm = tc.nt <= 128 ? 2 : 1;
-      const int64_t g = std::min<int64_t>(ceil_div(n_rows, (int64_t)tc.nt), (int64_t)num_sms(m->device) * per_sm);
+      const int64_t g = std::min<int64_t>(ceil_div(n_rows, (int64_t)tc.nt * tc.rpt), (int64_t)num_sms(m->device) * tc.per_sm);
       kt<<<(unsigned)g, tc.nt, sb, s>>>(a);
     } else {
       LinFn kr = cm == 2 ? linear_rows_kernel<2, 2> : cm == 4 ? linear_rows_kernel<4, 2> : cm == 8 ? linear_rows_kernel<8, 2>
