@@ -748,7 +748,7 @@ __global__ void __launch_bounds__(NTT, 1) forest_ranked_kernel(const ForestArgs 
           if constexpr (LEAF) {
             if (rowk[k] < a.n_rows) a.leaf_out[rowk[k] * T + t] = __ldg(a.slot_leaf + (int64_t)t * a.ns + slot);
           }
-          accumulate<(J + q) & 7, CT>(acc[k], v, a.C, code);
+          accumulate<(J + q) & 7, CT>(acc[k], v, CT, code);  // payload columns >= C are 0 (fill_ranked)
         }
       }
     };
