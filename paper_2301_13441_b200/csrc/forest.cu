@@ -172,13 +172,16 @@ struct RowAcc<CT, true> {
   static_assert(CT == 1, "pairwise replay is for scalar leaves");
   double r[8];
   double res;
+  // pending pairwise halves (st[sp - 1] = most recent); pushed a few times
+  // per row, so it lives in local memory instead of a register shift chain
   double st[SMAX];
+  int sp;
   __device__ __forceinline__ void init() {
 #pragma unroll
     for (int j = 0; j < 8; ++j) r[j] = 0.0;
     res = 0.0;
-#pragma unroll
-    for (int s = 0; s < SMAX; ++s) st[s] = 0.0;
+    st[0] = 0.0;
+    sp = 0;
   }
   // numpy: the reduction output starts at +0.0, then adds pairwise_sum(...)
   __device__ __forceinline__ double total(int) const { return 0.0 + st[0]; }
@@ -202,6 +205,10 @@ template <int J, int CT>
 __device__ __forceinline__ void accumulate(RowAcc<CT, true>& a, const float (&v)[CT], int, uint32_t code) {
   constexpr int j = J;
   const double val = (double)v[0];
+  if (code == SC_ADD) {  // the common case (warp-uniform: code depends on the tree only)
+    a.r[j] += val;
+    return;
+  }
   if (code & SC_FOLD_PRE) a.res = fold8(a.r);
   switch (code & SC_OPMASK) {
     case SC_ASSIGN: a.r[j] = val; break;
@@ -211,16 +218,11 @@ __device__ __forceinline__ void accumulate(RowAcc<CT, true>& a, const float (&v)
   }
   if (code & SC_FOLD_POST) a.res = fold8(a.r);
   if (code & SC_PUSH) {
-    // shift-register stack (st[0] = top): no runtime indices, stays in registers
-#pragma unroll
-    for (int q = SMAX - 1; q > 0; --q) a.st[q] = a.st[q - 1];
-    a.st[0] = a.res;
+    int sp = a.sp;
+    a.st[sp++] = a.res;
     const int pops = (int)(code >> 8);
-    for (int p = 0; p < pops; ++p) {
-      a.st[0] = a.st[1] + a.st[0];  // (earlier half) + (later half)
-#pragma unroll
-      for (int q = 1; q < SMAX - 1; ++q) a.st[q] = a.st[q + 1];
-    }
+    for (int p = 0; p < pops; ++p, --sp) a.st[sp - 2] = a.st[sp - 2] + a.st[sp - 1];  // (earlier half) + (later half)
+    a.sp = sp;
   }
 }
 
@@ -698,11 +700,12 @@ __global__ void __launch_bounds__(NTT, 1) forest_ranked_kernel(const ForestArgs 
   auto walk_group = [&](auto jconst, auto leafconst, uint32_t buf_off, int c0, int tl0, int nt) {
     constexpr int J = decltype(jconst)::value;
     constexpr bool LEAF = decltype(leafconst)::value;
-    uint32_t base[TI], cst[TI];
+    uint32_t base[TI], cst[TI], code[TI];
     bool has[TI];
 #pragma unroll
     for (int q = 0; q < TI; ++q) {
       has[q] = tl0 + q < nt;
+      code[q] = PW && has[q] ? __ldg(a.sched + c0 + tl0 + q) : 0u;  // loaded before the walk hides its latency
       const int tl = has[q] ? tl0 + q : tl0;
       base[q] = buf_off + (uint32_t)tl * a.tree_bytes + a.node_off_bytes;
       cst[q] = 4u - base[q];
@@ -738,7 +741,6 @@ __global__ void __launch_bounds__(NTT, 1) forest_ranked_kernel(const ForestArgs 
       if constexpr (q < TI) {
         if (!has[q]) return;
         const int t = t0 + q;
-        const uint32_t code = PW ? __ldg(a.sched + t) : 0u;
         const uint32_t tb = smem_base + base[q] - a.node_off_bytes;  // 16-aligned blob start
 #pragma unroll
         for (int k = 0; k < RPT; ++k) {
@@ -748,7 +750,7 @@ __global__ void __launch_bounds__(NTT, 1) forest_ranked_kernel(const ForestArgs 
           if constexpr (LEAF) {
             if (rowk[k] < a.n_rows) a.leaf_out[rowk[k] * T + t] = __ldg(a.slot_leaf + (int64_t)t * a.ns + slot);
           }
-          accumulate<(J + q) & 7, CT>(acc[k], v, CT, code);  // payload columns >= C are 0 (fill_ranked)
+          accumulate<(J + q) & 7, CT>(acc[k], v, CT, code[q]);  // payload columns >= C are 0 (fill_ranked)
         }
       }
     };
@@ -1129,9 +1131,11 @@ static KernelFn pick4(bool perfect, bool xs) {
 // Ranked launch configurations: (threads, rows per thread, trees per step).
 struct RankedCfg { int ntt, rpt, ti; };
 constexpr RankedCfg RANKED_CFGS[] = {
-    {512, 2, 2}, {512, 2, 4}, {1024, 1, 2}, {1024, 1, 4}, {256, 2, 2}, {256, 1, 2}, {128, 2, 2}, {512, 1, 2}};
-// (512x1 and 256x2 threads with 4 trees per step were measured on GBR1000 d10:
-// 6x slower than 512x1 with 2 -- register spills; tools/gbr_cfg_probe.sh)
+    {512, 2, 2}, {512, 2, 4}, {1024, 1, 2}, {1024, 1, 4}, {256, 2, 2}, {256, 1, 2}, {128, 2, 2}, {512, 1, 2},
+    {512, 1, 4}, {256, 2, 4}};
+// (with the replay stack in registers, 512x1 and 256x2 threads with 4 trees per
+// step spilled on GBR1000 d10, 6x slower; with it in local memory 512x1x4 is
+// the fastest scalar shape; tools/gbr_cfg_probe.sh)
 constexpr int N_RANKED_CFGS = sizeof(RANKED_CFGS) / sizeof(RANKED_CFGS[0]);
 
 template <int CT, bool PW>
@@ -1150,6 +1154,8 @@ static KernelFn ranked_cfg(int cfg) {
     case 5: return forest_ranked_kernel<CT, 256, 1, 2, PW>;
     case 6: return forest_ranked_kernel<CT, 128, 2, 2, PW>;
     case 7: return forest_ranked_kernel<CT, 512, 1, 2, PW>;
+    case 8: return forest_ranked_kernel<CT, 512, 1, 4, PW>;
+    case 9: return forest_ranked_kernel<CT, 256, 2, 4, PW>;
     default: return nullptr;
   }
 }
@@ -1441,6 +1447,9 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
     ranked_ok = max_nf <= 16382;  // ranks < 2^14 (see the node word layout)
     // preference order (measured on B200); CMLB_RANKED_CFG forces one
     std::vector<int> order = {1, 3, 0, 2, 7, 4, 5, 6};
+    // scalar (pairwise-replay) ensembles: four trees per step wins on GBR1000 d10
+    // (10.3 vs 10.8 ms); the replay's stack lives in local memory, so it fits
+    if (f->C == 1) order = {8, 7, 4, 5, 6};
     if (const char* env = getenv("CMLB_RANKED_CFG")) order = {atoi(env)};
     bool found = false;
     for (size_t oi = 0; oi < order.size() && ranked_ok && !found; ++oi) {
