@@ -59,3 +59,53 @@ def test_sign_tail_and_nonfinite_rows():
     x[1, 3] = np.nan
     x[2, :] = 0.0
     check(m, x)
+
+
+# --- the cp.async-tiled kernel (F % 4 == 0, aligned rows) and the per-(row,
+# output) float64 recompute: ragged tiles, strides, ties, non-finite values
+
+@pytest.mark.parametrize("n_rows", [1, 255, 256, 257, 4099])
+@pytest.mark.parametrize("C", [3, 10, 16])
+def test_tile_ragged_rows(n_rows, C):
+    rng = np.random.default_rng(10 + C)
+    m = lm("logistic_regression", rng.standard_normal((C, 64)) * 0.2, rng.standard_normal(C), range(C))
+    check(m, rng.standard_normal((n_rows, 64)).astype(np.float32))
+
+
+def test_tile_binary_sigmoid_and_tail_slice():
+    rng = np.random.default_rng(20)
+    m = lm("logistic_regression", rng.standard_normal((1, 36)) * 0.3, [0.05], (0.0, 1.0))
+    x = rng.standard_normal((3001, 36)).astype(np.float32)   # 36 = two 16-feature slices + 4
+    x[:50] *= 1e-7                                           # sigmoid-window rows -> recompute
+    check(m, x)
+
+
+def test_tile_strided_rows():
+    rng = np.random.default_rng(21)
+    m = lm("linear_svc", rng.standard_normal((7, 48)), rng.standard_normal(7), range(7))
+    big = rng.standard_normal((2000, 56)).astype(np.float32)
+    x = torch.from_numpy(big).cuda()[:, :48]                  # ldx = 56, 16-byte aligned rows
+    got = api.predict(api.compile_model(m), x).cpu().numpy().astype(np.float64)
+    want, _ = sem.predict(m, np.ascontiguousarray(big[:, :48]))
+    np.testing.assert_array_equal(got, want)
+
+
+def test_tile_ties_go_to_recompute_first_max():
+    rng = np.random.default_rng(22)
+    w = rng.standard_normal((12, 52)).astype(np.float32)
+    w[9] = w[2]                                               # classes 2 and 9 always tie
+    m = lm("linear_svc", w, np.zeros(12), range(12))
+    check(m, rng.standard_normal((5000, 52)).astype(np.float32))
+
+
+def test_tile_nonfinite_and_sparse_zero_weight():
+    rng = np.random.default_rng(23)
+    w = rng.standard_normal((4, 32)).astype(np.float32)
+    w[:, 7] = 0.0
+    m = lm("linear_svc", w, rng.standard_normal(4), range(4))
+    x = rng.standard_normal((1000, 32)).astype(np.float32)
+    x[0, 7] = np.inf     # only meets zero weights
+    x[1, 3] = np.nan
+    x[2, 0] = -np.inf
+    x[3, :] = 0.0
+    check(m, x)
