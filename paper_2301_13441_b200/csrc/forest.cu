@@ -165,6 +165,7 @@ struct RowAcc<CT, false> {
     for (int c = 0; c < CT; ++c) acc[c] = 0.0;
   }
   __device__ __forceinline__ double total(int c) const { return acc[c]; }
+  __device__ __forceinline__ void bind(double*) {}
 };
 
 template <int CT>
@@ -172,20 +173,23 @@ struct RowAcc<CT, true> {
   static_assert(CT == 1, "pairwise replay is for scalar leaves");
   double r[8];
   double res;
-  // pending pairwise halves (st[sp - 1] = most recent); pushed a few times
-  // per row, so it lives in local memory instead of a register shift chain
-  double st[SMAX];
+  // pending pairwise halves (st[sp - 1] = most recent): pushed a few times per
+  // row, so they live in a kernel-local array (bind) while r / res stay in
+  // registers -- a dynamically indexed member would demote the whole struct
+  double* st;
   int sp;
+  double bottom;  // st[0] once the replay has folded everything
   __device__ __forceinline__ void init() {
 #pragma unroll
     for (int j = 0; j < 8; ++j) r[j] = 0.0;
     res = 0.0;
-    st[0] = 0.0;
     sp = 0;
+    bottom = 0.0;
   }
+  __device__ __forceinline__ void bind(double* s) { st = s; }
   // numpy: the reduction output starts at +0.0, then adds pairwise_sum(...)
-  __device__ __forceinline__ double total(int) const { return 0.0 + st[0]; }
-  __device__ __forceinline__ double raw(int) const { return st[0]; }
+  __device__ __forceinline__ double total(int) const { return 0.0 + bottom; }
+  __device__ __forceinline__ double raw(int) const { return bottom; }
 };
 
 __device__ __forceinline__ double fold8(const double (&r)[8]) {
@@ -223,6 +227,7 @@ __device__ __forceinline__ void accumulate(RowAcc<CT, true>& a, const float (&v)
     const int pops = (int)(code >> 8);
     for (int p = 0; p < pops; ++p, --sp) a.st[sp - 2] = a.st[sp - 2] + a.st[sp - 1];  // (earlier half) + (later half)
     a.sp = sp;
+    a.bottom = a.st[0];
   }
 }
 
@@ -349,10 +354,12 @@ __global__ void __launch_bounds__(NT) forest_kernel(const ForestArgs a) {
   // then applied on the fly (general layout only, see xval()).
 
   RowAcc<CT, PW> acc[RPT];
+  double pw_stack[PW ? RPT : 1][PW ? SMAX : 1];
   float single[RPT][CT];  // AGG_NONE: the one tree's payload
 #pragma unroll
   for (int k = 0; k < RPT; ++k) {
     acc[k].init();
+    acc[k].bind(pw_stack[PW ? k : 0]);
 #pragma unroll
     for (int c = 0; c < CT; ++c) single[k][c] = 0.0f;
   }
@@ -687,8 +694,12 @@ __global__ void __launch_bounds__(NTT, 1) forest_ranked_kernel(const ForestArgs 
   }
 
   RowAcc<CT, PW> acc[RPT];
+  double pw_stack[PW ? RPT : 1][PW ? SMAX : 1];
 #pragma unroll
-  for (int k = 0; k < RPT; ++k) acc[k].init();
+  for (int k = 0; k < RPT; ++k) {
+    acc[k].init();
+    acc[k].bind(pw_stack[PW ? k : 0]);
+  }
 
   const int D = a.depth;
   const uint8_t* xrb = reinterpret_cast<const uint8_t*>(xr);
@@ -985,7 +996,9 @@ __global__ void __launch_bounds__(MMA2_THREADS, 1) forest_mma2_kernel(const Fore
     const int hN = ((N / 2) + 31) / 32 * 32;            // columns per half
     const int cbeg = half * hN, cend = min(N, cbeg + hN);
     RowAcc<CT, PW> acc;
+    double pw_stack[PW ? SMAX : 1];
     acc.init();
+    acc.bind(pw_stack);
     auto step = [&](auto jconst, int t) {
       constexpr int J = decltype(jconst)::value;
       const int b = t & 1;
