@@ -656,21 +656,30 @@ __global__ void __launch_bounds__(NTT, 1) forest_ranked_kernel(const ForestArgs 
     cp_async_commit();
   };
   issue_stage(0);
-  for (int g0 = 0; g0 < F; g0 += 8) {
-    float xv[RPT][8];
+  // row values for features g0..g0+7; the next group's loads are issued
+  // before this group's searches so their latency hides behind them
+  float xn[RPT][8];
+  auto load_group = [&](int g) {
 #pragma unroll
     for (int k = 0; k < RPT; ++k) {
       const float* src = a.x + rowk[k] * a.ldx;
 #pragma unroll
+      for (int j = 0; j < 8; ++j)
+        xn[k][j] = (rowk[k] < a.n_rows && g + j < F) ? load_col(a.pro, src, g + j) : 0.0f;
+    }
+  };
+  load_group(0);
+  for (int g0 = 0; g0 < F; g0 += 8) {
+    float xv[RPT][8];
+#pragma unroll
+    for (int k = 0; k < RPT; ++k)
+#pragma unroll
       for (int j = 0; j < 8; ++j) {
-        float v = 0.0f;
-        if (rowk[k] < a.n_rows && g0 + j < F) {
-          v = load_col(a.pro, src, g0 + j);
-          if (nbad[k] && (nbad[k] >= 2 || isfinite(v))) v = __int_as_float(0x7fc00000);
-        }
+        float v = xn[k][j];
+        if (nbad[k] && rowk[k] < a.n_rows && g0 + j < F && (nbad[k] >= 2 || isfinite(v))) v = __int_as_float(0x7fc00000);
         xv[k][j] = v;
       }
-    }
+    if (g0 + 8 < F) load_group(g0 + 8);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int f = g0 + j;
