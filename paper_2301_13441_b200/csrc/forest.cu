@@ -140,7 +140,8 @@ struct ForestArgs {
   const float* uthr;          // per feature: sorted unique thresholds in Eytzinger (BFS) order
   const int32_t* uoff;        // [F + 1]
   const uint16_t* umap;       // per feature: Eytzinger position -> sorted index (even-aligned)
-  const int32_t* moff;        // [F + 1] offsets into umap (even)
+  const int32_t* moff;        // [F + 1] offsets into umap (multiples of 8 entries)
+  const int32_t* unf;         // [F] distinct thresholds per feature (uoff starts are 4-aligned)
   int node_off_bytes;         // byte offset of the node words inside a ranked tree blob
   int stage_off;              // byte offset of the ranking staging area inside the chunk area
   int stage_bufs;             // 1 or 2 staging buffers
@@ -592,6 +593,7 @@ __global__ void __launch_bounds__(NTT, 1) forest_ranked_kernel(const ForestArgs 
   // chunk ahead of the walk.  The ranking staging area lives in buffer 1 when
   // it fits there (a.stage_off != 0), so chunk 0 streams in during ranking.
   __shared__ __align__(8) uint64_t tree_bar[2];
+  __shared__ __align__(8) uint64_t stage_bar[2];   // per-feature threshold staging (TMA)
   const uint32_t buf_bytes = (uint32_t)a.chunk_trees * a.tree_bytes;
   const int T = a.T;
   const int nchunks = (T + a.chunk_trees - 1) / a.chunk_trees;
@@ -608,6 +610,8 @@ __global__ void __launch_bounds__(NTT, 1) forest_ranked_kernel(const ForestArgs 
   if (tid == 0) {
     mbar_init(&tree_bar[0], 1);
     mbar_init(&tree_bar[1], 1);
+    mbar_init(&stage_bar[0], 1);
+    mbar_init(&stage_bar[1], 1);
     mbar_fence_init();
   }
   __syncthreads();
@@ -645,15 +649,23 @@ __global__ void __launch_bounds__(NTT, 1) forest_ranked_kernel(const ForestArgs 
   auto stage_f = [&](int b) {
     return reinterpret_cast<float*>(chunk + a.stage_off) + (size_t)(dbl ? b : 0) * (cap + cap / 2);
   };
+  // feature f's Eytzinger thresholds + index map: two TMA bulk copies by
+  // thread 0 (16-byte aligned, padded arrays), completing on stage_bar
   auto issue_stage = [&](int f) {
-    float* fb = stage_f(f & 1);
-    uint32_t* mb = reinterpret_cast<uint32_t*>(fb + cap);
-    const int u0 = __ldg(a.uoff + f), nf = __ldg(a.uoff + f + 1) - u0;
-    const int m0 = __ldg(a.moff + f);
-    for (int i = tid; i < nf; i += NTT) cp_async4(fb + i, a.uthr + u0 + i);
-    const uint32_t* msrc = reinterpret_cast<const uint32_t*>(a.umap + m0);
-    for (int i = tid; i < (nf + 1) / 2; i += NTT) cp_async4(mb + i, msrc + i);
-    cp_async_commit();
+    if (tid != 0) return;
+    const int b = dbl ? (f & 1) : 0;
+    float* fb = stage_f(b);
+    uint8_t* mb = reinterpret_cast<uint8_t*>(fb + cap);
+    const int nf = __ldg(a.unf + f);
+    const uint32_t tbytes = (uint32_t)((nf + 3) & ~3) * 4u, mbytes = (uint32_t)((nf + 7) & ~7) * 2u;
+    const uint8_t* ts = reinterpret_cast<const uint8_t*>(a.uthr + __ldg(a.uoff + f));
+    const uint8_t* ms = reinterpret_cast<const uint8_t*>(a.umap + __ldg(a.moff + f));
+    fence_proxy_async();
+    mbar_expect_tx(&stage_bar[b], tbytes + mbytes);
+    for (uint32_t off = 0; off < tbytes; off += 32768u)
+      bulk_g2s(reinterpret_cast<uint8_t*>(fb) + off, ts + off, min(32768u, tbytes - off), &stage_bar[b]);
+    for (uint32_t off = 0; off < mbytes; off += 32768u)
+      bulk_g2s(mb + off, ms + off, min(32768u, mbytes - off), &stage_bar[b]);
   };
   issue_stage(0);
   // row values for features g0..g0+7; the next group's loads are issued
@@ -688,12 +700,12 @@ __global__ void __launch_bounds__(NTT, 1) forest_ranked_kernel(const ForestArgs 
           __syncthreads();  // everyone done searching f-1 in the single buffer
           issue_stage(f);
         }
-        cp_async_wait_all();
+        mbar_wait(&stage_bar[dbl ? (f & 1) : 0], (uint32_t)((dbl ? (f >> 1) : f) & 1));
         __syncthreads();  // stage f landed for everyone; buffer (f+1)&1 is free
         if (dbl && f + 1 < F) issue_stage(f + 1);
         const float* fb = stage_f(f & 1);
         const uint16_t* mb = reinterpret_cast<const uint16_t*>(fb + cap);
-        const int nf = __ldg(a.uoff + f + 1) - __ldg(a.uoff + f);
+        const int nf = __ldg(a.unf + f);
         uint8_t* xrow = reinterpret_cast<uint8_t*>(xr) + (size_t)f * ROWS * 2;
 #pragma unroll
         for (int k = 0; k < RPT; ++k)
@@ -1101,6 +1113,7 @@ struct cmlb_forest {
   int32_t* uoff = nullptr;
   uint16_t* umap = nullptr;
   int32_t* moff = nullptr;
+  int32_t* unf = nullptr;
   int ntt = 256, stage_cap = 0, node_off_bytes = 0, rcfg = 0, stage_off = 0, stage_bufs = 2;
   int mma_k = 0, mma_n = 0, mma_feat_off = 0, mma_thr_off = 0, mma_pay_off = 0;
   cmlb_column_op* pro = nullptr;  // fused preprocessing
@@ -1109,7 +1122,7 @@ struct cmlb_forest {
     cudaFree(pro);
     cudaFree(blob); cudaFree(slot_leaf); cudaFree(gnode); cudaFree(node_off);
     cudaFree(gpay); cudaFree(leaf_off); cudaFree(sched); cudaFree(classes);
-    cudaFree(uthr); cudaFree(uoff); cudaFree(umap); cudaFree(moff);
+    cudaFree(uthr); cudaFree(uoff); cudaFree(umap); cudaFree(moff); cudaFree(unf);
   }
 };
 
@@ -1559,7 +1572,7 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
     // from Eytzinger position back to sorted index
     std::vector<float> uthr;
     std::vector<uint16_t> umap;
-    std::vector<int32_t> uoff(f->F + 1, 0), moff(f->F + 1, 0);
+    std::vector<int32_t> uoff(f->F + 1, 0), moff(f->F + 1, 0), unf(f->F, 0);
     for (int k = 0; k < f->F; ++k) {
       const auto& u = U[k];
       const size_t n = u.size();
@@ -1578,11 +1591,15 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
         ++next;
         node = 2 * node + 1;
       }
+      // each feature's arrays start 16-byte aligned and span whole 16-byte
+      // units, so the kernel stages them with two TMA bulk copies
+      unf[k] = (int32_t)n;
       uthr.insert(uthr.end(), e.begin(), e.end());
+      while (uthr.size() % 4) uthr.push_back(0.0f);
       uoff[k + 1] = (int32_t)uthr.size();
       moff[k] = (int32_t)umap.size();
       umap.insert(umap.end(), m.begin(), m.end());
-      if (umap.size() % 2) umap.push_back(0);
+      while (umap.size() % 8) umap.push_back(0);
     }
     moff[f->F] = (int32_t)umap.size();
     if (int st = upload(&f->blob, blob.data(), blob.size())) return st;
@@ -1591,6 +1608,7 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
     if (int st = upload(&f->uoff, uoff.data(), uoff.size())) return st;
     if (int st = upload(&f->umap, umap.data(), umap.size())) return st;
     if (int st = upload(&f->moff, moff.data(), moff.size())) return st;
+    if (int st = upload(&f->unf, unf.data(), unf.size())) return st;
   }
 
   if (f->variant == CMLB_FOREST_RANKED || f->variant == CMLB_FOREST_MMA) {
@@ -1636,7 +1654,7 @@ static int run_forest(const cmlb_forest* f, const float* x, int64_t n_rows, int6
   a.agg = f->agg; a.tail = f->tail; a.out_dt = f->out_dt; a.dense_sel = f->dense_sel;
   a.n_classes = f->n_classes; a.lr = f->lr; a.base = f->base; a.classes = f->classes;
   a.pay_off = f->pay_off; a.feat_off = f->feat_off;
-  a.uthr = f->uthr; a.uoff = f->uoff; a.umap = f->umap; a.moff = f->moff; a.stage_cap = f->stage_cap; a.node_off_bytes = f->node_off_bytes; a.stage_off = f->stage_off; a.stage_bufs = f->stage_bufs;
+  a.uthr = f->uthr; a.uoff = f->uoff; a.umap = f->umap; a.moff = f->moff; a.unf = f->unf; a.stage_cap = f->stage_cap; a.node_off_bytes = f->node_off_bytes; a.stage_off = f->stage_off; a.stage_bufs = f->stage_bufs;
   KernelFn k = kernel_for(*f);
   a.mma_k = f->mma_k; a.mma_n = f->mma_n; a.mma_feat_off = f->mma_feat_off; a.mma_thr_off = f->mma_thr_off;
   a.mma_pay_off = f->mma_pay_off;
