@@ -314,6 +314,21 @@ def main(argv=None):
         if os.path.exists(tpath):  # ncu dram__bytes_read+write per row, scaled to this launch
             with open(tpath) as fh:
                 traffic = json.load(fh)["dram_bytes_per_row"] * n
+        clocks = clk.summary()
+        smem = None  # the traversal's binding resource: shared-memory load wavefronts
+        spath = os.path.join(ROOT, "profiles", "r1_forest_ranked_ncu_summary.json")
+        if info["variant"] == "ranked" and os.path.exists(spath):
+            with open(spath) as fh:
+                js = json.load(fh)
+            wf_row = float(str(js["l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum"]).split()[0]) / js["rows"]
+            sms = torch.cuda.get_device_properties(dev).multi_processor_count
+            mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965.0
+            ach = rows_per_s_kernel * wf_row / 1e9
+            pk_w = sms * mhz * 1e6 / 1e9
+            smem = {"achieved": ach, "peak": pk_w, "unit": "Gwavefronts/s", "frac": ach / pk_w,
+                    "wavefronts_row": wf_row,
+                    "basis": "shared-memory load wavefronts per row (ncu, profiles/r1_forest_ranked_ncu_summary.json) "
+                             "x live rows/s; peak = 1 wavefront/clk/SM at the measured SM clock"}
         line = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
@@ -335,11 +350,12 @@ def main(argv=None):
                 "hbm": {"achieved": achieved_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
                         "frac": achieved_gbs / pk["hbm_gbs"], "bytes_row": BYTES_ROW,
                         "peak_source": pk["source"]["hbm"]},
+                "smem": smem,
                 "kernel_ms": statistics.mean(kernel_ms)},
             "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": n * 28 * 4,
                     "d2h_bytes_per_step": n * 1, "steps": args.e2e_steps, "parity_vs_device": parity_ok},
             "gpu_launches": int(launches),
-            "clocks": clk.summary(),
+            "clocks": clocks,
         }
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(model, mu, sigma)
