@@ -1016,7 +1016,10 @@ int cmlb_linear_run(const cmlb_linear* m, const float* x, int64_t n_rows, int64_
       const TileCfg tc = kTileCfg[cfg];
       const size_t sb = (size_t)tc.st * tc.nt * tc.rpt * tc.kc * 4 + wbytes;
       CMLB_CUDA(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
-      const int64_t g = std::min<int64_t>(ceil_div(n_rows, (int64_t)tc.nt * tc.rpt), (int64_t)num_sms(m->device) * tc.per_sm);
+      int occ = 0;   // persistent grid: as many CTAs per SM as registers / shared memory allow
+      CMLB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kt, tc.nt, sb));
+      const int64_t g = std::min<int64_t>(ceil_div(n_rows, (int64_t)tc.nt * tc.rpt),
+                                          (int64_t)num_sms(m->device) * std::max(occ, 1));
       kt<<<(unsigned)g, tc.nt, sb, s>>>(a);
     } else {
       LinFn kr = cm == 2 ? linear_rows_kernel<2, 2> : cm == 4 ? linear_rows_kernel<4, 2> : cm == 8 ? linear_rows_kernel<8, 2>
