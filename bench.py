@@ -155,10 +155,30 @@ def cpu_baseline(model, mu, sigma, target_s: float = 10.0):
                       f"(C restatement of mlower execute semantics)"}
 
 
-def init_dist():
+def launch_ranks(n: int, argv) -> int:
+    """``--gpus N`` without a launcher: start N ranks (one per GPU) under
+    torch.distributed.run ourselves, as the driver would."""
+    import socket
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < n:
+        print(f"bench.py: --gpus {n} but only {have} CUDA device(s) visible", file=sys.stderr, flush=True)
+        return 2
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + list(argv)
+    return subprocess.call(cmd)
+
+
+def init_dist(gpus: int):
     import torch
     import torch.distributed as dist
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != gpus:
+        raise SystemExit(f"bench.py: --gpus {gpus} but WORLD_SIZE={world}")
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
@@ -223,6 +243,8 @@ def main(argv=None):
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return launch_ranks(args.gpus, sys.argv[1:] if argv is None else argv)
 
     import torch
     import torch.distributed as dist
@@ -231,7 +253,7 @@ def main(argv=None):
     from paper_2301_13441_b200 import api
     from paper_2301_13441_b200.runtime import run_host
 
-    rank, world, local = init_dist()
+    rank, world, local = init_dist(args.gpus)
     dev = torch.device("cuda", torch.cuda.current_device())
     model, mu, sigma = load_model()
     compiled = api.compile_model(model)

@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define CMLB_ABI_VERSION 2
+#define CMLB_ABI_VERSION 3
 
 enum cmlb_status {
   CMLB_OK = 0,
@@ -125,6 +125,8 @@ typedef struct cmlb_forest_desc {
   int32_t variant;              /* cmlb_forest_variant */
   const cmlb_column_op* prologue; /* optional [n_features]: feature f = op(x[src]) (ABI 2) */
   int32_t n_inputs;             /* raw input columns when prologue != NULL */
+  int32_t n_trees_total;        /* ABI 3: trees of the WHOLE ensemble when this program is one
+                                 * tree shard (MEAN divides by it); 0 = n_trees */
 } cmlb_forest_desc;
 
 typedef struct cmlb_forest cmlb_forest;
@@ -140,13 +142,22 @@ int cmlb_forest_run(const cmlb_forest* f, const float* x, int64_t n_rows, int64_
  * reference's pairwise order restricted to the shard (no tail), [n_rows][C]. */
 int cmlb_forest_partial(const cmlb_forest* f, const float* x, int64_t n_rows, int64_t ldx,
                         double* partial, void* stream);
-/* Tree-shard combine + tail on this (whole-forest) program's tail parameters:
- * partials = device float64 [n_shards][n_rows][C], each the raw sum of one
- * contiguous tree range; merges = host int32 pairs (a, b) applied in order as
- * p[a] += p[b] (the shard nodes of numpy's pairwise recursion, leaving the sum
- * in p[0]); then the reference tail (kernels.py:180-190, convert.py:297-311). */
+/* Tree-shard combine + tail: partials = device float64 [n_shards][n_rows][1],
+ * each the raw sum of one contiguous tree range; merges = host int32 pairs
+ * (a, b) applied in order as p[a] += p[b] (the shard nodes of numpy's pairwise
+ * recursion, leaving the sum in p[0]); then the reference tail
+ * (kernels.py:180-190, convert.py:297-311) with this program's tail
+ * parameters and n_trees_total.  Scalar ensembles only (C == 1): numpy sums a
+ * (N, T, C >= 2) stack tree after tree, which no shard cut reproduces, so
+ * those are sharded by rows (CMLB_E_UNRESOLVED otherwise).  n_shards == 1,
+ * n_merges == 0 finishes an already-reduced partial. */
 int cmlb_forest_finish(const cmlb_forest* f, const double* partials, int32_t n_shards, const int32_t* merges,
                        int32_t n_merges, int64_t n_rows, void* y, void* stream);
+/* One step of the cross-GPU pairwise tree reduce (reference kernels.py:185-190,
+ * numpy pairwise_sum): dst[i] = dst[i] + src[i] in float64 for the n_rows
+ * scalar partials, on this program's device.  The caller received src from the
+ * peer that owns the right-hand shard node (NCCL point-to-point over NVLink). */
+int cmlb_forest_merge(const cmlb_forest* f, double* dst, const double* src, int64_t n_rows, void* stream);
 /* Introspection: chosen variant, padded depth, trees per shared-memory chunk. */
 int cmlb_forest_info(const cmlb_forest* f, int32_t* variant, int32_t* depth, int32_t* chunk_trees,
                      int32_t* rows_per_cta);
@@ -275,8 +286,10 @@ typedef struct cmlb_columns_desc {
 typedef struct cmlb_columns cmlb_columns;
 int cmlb_columns_create(const cmlb_columns_desc* desc, int device, cmlb_columns** out);
 /* y: device float32 [n_rows][n_outputs] (NULL: check only).  bad_row:
- * optional device int64, receives the first row holding an unknown category
- * or -1 (the caller raises, as OneHotEncoder.transform does). */
+ * optional device int64 the caller initialises to -1; it is lowered to the
+ * first row holding an unknown category (min-combined, so several check
+ * stages may share one slot) and the caller raises, as
+ * OneHotEncoder.transform does. */
 int cmlb_columns_run(const cmlb_columns* c, const float* x, int64_t n_rows, int64_t ldx, float* y,
                      int64_t* bad_row, void* stream);
 void cmlb_columns_destroy(cmlb_columns* c);

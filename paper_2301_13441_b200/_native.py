@@ -17,6 +17,8 @@ from .errors import DeviceError, error_for_status
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libcmlb.so")
 
+ABI_VERSION = 3  # CMLB_ABI_VERSION in include/cmlb.h
+
 c_i32, c_i64, c_f32, c_f64, c_vp = C.c_int32, C.c_int64, C.c_float, C.c_double, C.c_void_p
 P = C.POINTER
 
@@ -34,7 +36,7 @@ class ForestDesc(C.Structure):
         ("aggregation", c_i32), ("tail", c_i32), ("learning_rate", c_f32), ("base_score", c_f32),
         ("classes", P(c_f64)), ("n_classes", c_i32), ("out_dtype", c_i32),
         ("dense_selector", c_i32), ("variant", c_i32),
-        ("prologue", c_vp), ("n_inputs", c_i32),
+        ("prologue", c_vp), ("n_inputs", c_i32), ("n_trees_total", c_i32),
     ]
 
 
@@ -89,6 +91,7 @@ SIGNATURES = {
     "cmlb_forest_run": (C.c_int, [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp]),
     "cmlb_forest_partial": (C.c_int, [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp]),
     "cmlb_forest_finish": (C.c_int, [c_vp, c_vp, c_i32, P(c_i32), c_i32, c_i64, c_vp, c_vp]),
+    "cmlb_forest_merge": (C.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp]),
     "cmlb_forest_info": (C.c_int, [c_vp, P(c_i32), P(c_i32), P(c_i32), P(c_i32)]),
     "cmlb_forest_destroy": (None, [c_vp]),
     "cmlb_linear_create": (C.c_int, [P(LinearDesc), C.c_int, P(c_vp)]),
@@ -124,6 +127,9 @@ def lib():
                 fn = getattr(handle, name)
                 fn.restype = res
                 fn.argtypes = args
+            if handle.cmlb_abi_version() != ABI_VERSION:
+                raise DeviceError(f"{LIB_PATH} has ABI {handle.cmlb_abi_version()}, this package needs "
+                                  f"{ABI_VERSION}; rebuild with `python -m paper_2301_13441_b200.build`")
             _lib = handle
     return _lib
 

@@ -23,6 +23,12 @@ kernel per operator representation runs on the GPU.  Inputs may be
   result stays on the device (uint8 for BOOL outputs);
 * a CPU ``torch.Tensor`` (ideally pinned): streamed through the GPU in
   overlapped chunks, result returned as a CPU tensor.
+
+``predict(..., devices=[0, 1, ...])`` / ``execute(..., devices=...)`` shard the
+batch by rows over several GPUs of this process (one program replica per GPU,
+no collective); the reference requires this to be bit-transparent
+(``SPEC.md:574``), and it is: every row is computed by the same kernel
+whatever shard it lands in, and the pieces are concatenated in row order.
 """
 
 from __future__ import annotations
@@ -175,19 +181,77 @@ def _run(owner, spec_getter, x, device=None):
     return wrap_like(x, values, prog.out_dtype)
 
 
-def execute(plan, x, device=None):
+def _run_sharded(owner, spec_getter, x, devices):
+    """Row-shard one batch over ``devices`` (threads: one per device, so the
+    host copies and kernels of all shards overlap).  Same input/output
+    families as :func:`_run`."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from .shard import row_range
+
+    devices = [_device_of(d) for d in devices]
+    if not devices:
+        raise ValidationError("devices must name at least one GPU")
+    if len(devices) == 1:
+        return _run(owner, spec_getter, x, devices[0])
+    host_wrap = None
+    if isinstance(x, torch.Tensor):
+        xt = x
+    else:
+        arr = _host_array(x)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", UserWarning)
+            xt = torch.from_numpy(np.ascontiguousarray(arr))
+        host_wrap = x
+    progs = [_program_for(owner, d, spec_getter()) for d in devices]
+    progs[0].check_input(xt)
+    n = int(xt.shape[0])
+    ranges = [row_range(n, r, len(devices)) for r in range(len(devices))]
+
+    def piece(i):
+        lo, hi = ranges[i]
+        prog, dev = progs[i], devices[i]
+        if xt.is_cuda:
+            with torch.cuda.device(dev):
+                xs = xt[lo:hi].to(torch.device("cuda", dev), non_blocking=True)
+                y = prog.run(xs)
+                torch.cuda.current_stream(dev).synchronize()
+                return y
+        return run_host(prog, xt[lo:hi])
+
+    with ThreadPoolExecutor(max_workers=len(devices)) as pool:
+        outs = list(pool.map(piece, range(len(devices))))
+    if xt.is_cuda:
+        return torch.cat([o.to(xt.device) for o in outs], dim=0)
+    out = torch.cat(outs, dim=0)
+    if host_wrap is None:
+        return out
+    values = out.numpy()
+    if progs[0].out_dtype == "bool":
+        values = values.astype(np.uint8)
+    if isinstance(host_wrap, np.ndarray):
+        return values
+    return wrap_like(host_wrap, values, progs[0].out_dtype)
+
+
+def execute(plan, x, device=None, devices=None):
     """Run a reference ``KernelPlan`` on the GPU; drop-in for ``mlower.execute``."""
+    if devices is not None:
+        return _run_sharded(plan, lambda: _spec_of_plan(plan), x, devices)
     return _run(plan, lambda: _spec_of_plan(plan), x, device)
 
 
-def predict(compiled, x, device=None):
-    """Drop-in for ``mlower.predict``; also accepts a reference CompileResult."""
+def predict(compiled, x, device=None, devices=None):
+    """Drop-in for ``mlower.predict``; also accepts a reference CompileResult.
+    ``devices``: row-shard the batch over these GPUs (bit-transparent)."""
     if isinstance(compiled, CompileResult):
+        if devices is not None:
+            return _run_sharded(compiled, lambda: compiled.spec, x, devices)
         return _run(compiled, lambda: compiled.spec, x, device)
     plan = getattr(compiled, "plan", None)
     if plan is None:
         raise ValidationError("predict() needs a CompileResult")
-    return execute(plan, x, device)
+    return execute(plan, x, device, devices)
 
 
 __all__ = ["CompileResult", "compile_model", "from_plan", "predict", "execute", "DEFAULT_TOLERANCE",

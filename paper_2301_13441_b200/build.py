@@ -38,13 +38,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
         flags += ["-Xptxas", "-v"]
     objs = []
     procs = []
+    headers = deps[len(srcs):]
     for s in srcs:
         obj = os.path.join(objdir, os.path.basename(s) + ".o")
         objs.append(obj)
-        procs.append(subprocess.Popen([NVCC, *flags, "-c", s, "-o", obj],
-                                      stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True))
+        # per-object rebuild: a source is recompiled when it or a header is newer
+        if not force and not verbose and os.path.exists(obj) and os.path.getmtime(obj) >= _newest([s] + headers):
+            continue
+        procs.append((s, subprocess.Popen([NVCC, *flags, "-c", s, "-o", obj],
+                                          stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
     logs = []
-    for p, s in zip(procs, srcs):
+    for s, p in procs:
         out, _ = p.communicate()
         logs.append(out)
         if p.returncode != 0:

@@ -78,8 +78,13 @@ __global__ void columns_check_kernel(const ColsArgs a) {
   }
 }
 
+// Folds this stage's first offending row into *out (initialised to -1 by the
+// caller): several check stages may share one slot, and a clean stage must not
+// erase an earlier stage's hit.
 __global__ void columns_bad_finish(const unsigned long long* bad, int64_t* out) {
-  *out = *bad == ~0ull ? -1 : (int64_t)*bad;
+  if (*bad == ~0ull) return;
+  const int64_t r = (int64_t)*bad;
+  if (*out < 0 || r < *out) *out = r;
 }
 
 }  // namespace cmlb

@@ -125,6 +125,7 @@ struct ForestArgs {
   double* partial;
   // program
   int T, F, C, depth, ni, ns, tree_bytes, chunk_trees, rows_per_cta, stage_cap;
+  int T_tail;                 // whole-ensemble tree count for MEAN (tree shards: > T)
   const uint8_t* blob;        // perfect: [T][tree_bytes]
   const int32_t* slot_leaf;   // perfect: [T][ns]
   const int4* gnode;          // general: packed nodes
@@ -257,7 +258,7 @@ __device__ __forceinline__ void finish_totals(const ForestArgs& a, int64_t row, 
     for (int c = 0; c < CT; ++c) v[c] = single[c];
   } else if (a.agg == CMLB_AGG_MEAN) {
 #pragma unroll
-    for (int c = 0; c < CT; ++c) v[c] = __double2float_rn(total[c] / (double)a.T);
+    for (int c = 0; c < CT; ++c) v[c] = __double2float_rn(total[c] / (double)a.T_tail);
   } else {
     const float s = __double2float_rn(total[0]);
     v[0] = __fadd_rn(__fmul_rn(s, a.lr), a.base);
@@ -322,6 +323,13 @@ __global__ void forest_finish_kernel(const ForestArgs a, const double* partials,
     total[c] = C == 1 ? 0.0 + p[0] : p[0];
   }
   finish_totals<CT>(a, row, total, none);
+}
+
+// p[a] += p[b] of the pairwise tree reduce across GPUs (float64, IEEE add).
+__global__ void partial_add_kernel(double* __restrict__ dst, const double* __restrict__ src, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    dst[i] = __dadd_rn(dst[i], src[i]);
 }
 
 // One kernel body for both layouts.  Thread `tid` owns rows
@@ -1093,6 +1101,7 @@ __global__ void __launch_bounds__(MMA2_THREADS, 1) forest_mma2_kernel(const Fore
 struct cmlb_forest {
   int device = 0;
   int T = 0, F = 0, C = 0, CT = 1;
+  int T_tail = 0;
   int variant = CMLB_FOREST_GENERAL;
   int depth = 0, ni = 0, ns = 0, tree_bytes = 0, chunk_trees = 0, rpt = 1;
   int pay_off = 0, feat_off = 0;
@@ -1238,6 +1247,8 @@ static int validate(const cmlb_forest_desc* d) {
   if (d->n_trees < 1 || d->n_features < 1 || d->n_outputs < 1)
     return fail(CMLB_E_VALIDATION, "forest needs >= 1 tree, feature and output");
   if (d->n_outputs > 32) return fail(CMLB_E_UNRESOLVED, "more than 32 outputs per leaf");
+  if (d->n_trees_total != 0 && (d->n_trees_total < d->n_trees || d->aggregation == CMLB_AGG_NONE))
+    return fail(CMLB_E_VALIDATION, "n_trees_total must be 0 or >= n_trees of an ensemble");
   if (!out_dtype_ok(d->out_dtype)) return fail(CMLB_E_VALIDATION, "bad out_dtype");
   if (d->aggregation == CMLB_AGG_NONE && d->n_trees != 1)
     return fail(CMLB_E_VALIDATION, "aggregation NONE needs exactly one tree");
@@ -1395,6 +1406,7 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
   DeviceGuard guard(device);
   f->device = device;
   f->T = d->n_trees; f->F = d->n_features; f->C = d->n_outputs;
+  f->T_tail = d->n_trees_total > 0 ? d->n_trees_total : d->n_trees;
   f->CT = class_width(f->C);
   f->agg = d->aggregation; f->tail = d->tail; f->out_dt = d->out_dtype;
   f->dense_sel = d->dense_selector ? 1 : 0;
@@ -1647,7 +1659,7 @@ static int run_forest(const cmlb_forest* f, const float* x, int64_t n_rows, int6
   ForestArgs a{};
   a.x = x; a.n_rows = n_rows; a.ldx = ldx; a.y = y; a.leaf_out = leaf_out; a.partial = partial;
   a.pro = f->pro;
-  a.T = f->T; a.F = f->F; a.C = f->C; a.depth = f->depth; a.ni = f->ni; a.ns = f->ns;
+  a.T = f->T; a.T_tail = f->T_tail; a.F = f->F; a.C = f->C; a.depth = f->depth; a.ni = f->ni; a.ns = f->ns;
   a.tree_bytes = f->tree_bytes; a.chunk_trees = f->chunk_trees; a.rows_per_cta = NT * f->rpt;
   a.blob = f->blob; a.slot_leaf = f->slot_leaf; a.gnode = f->gnode; a.node_off = f->node_off;
   a.gpay = f->gpay; a.leaf_off = f->leaf_off; a.sched = f->sched;
@@ -1705,6 +1717,8 @@ int cmlb_forest_finish(const cmlb_forest* f, const double* partials, int32_t n_s
   if (n_shards < 1 || n_shards > 64 || n_merges < 0 || n_merges > MAX_MERGES || (n_merges && !merges))
     return fail(CMLB_E_VALIDATION, "bad shard merge plan");
   if (n_rows < 0) return fail(CMLB_E_INPUT, "bad row count");
+  if (f->C != 1 || f->agg == CMLB_AGG_NONE)
+    return fail(CMLB_E_UNRESOLVED, "tree sharding needs a scalar ensemble (numpy sums C >= 2 tree after tree)");
   if (n_rows == 0) return CMLB_OK;
   MergePlan mp{};
   mp.n = n_merges;
@@ -1716,16 +1730,25 @@ int cmlb_forest_finish(const cmlb_forest* f, const double* partials, int32_t n_s
   }
   DeviceGuard guard(f->device);
   ForestArgs a{};
-  a.n_rows = n_rows; a.y = y; a.T = f->T; a.C = f->C; a.agg = f->agg; a.tail = f->tail; a.out_dt = f->out_dt;
+  a.n_rows = n_rows; a.y = y; a.T = f->T; a.T_tail = f->T_tail; a.C = f->C; a.agg = f->agg; a.tail = f->tail; a.out_dt = f->out_dt;
   a.lr = f->lr; a.base = f->base; a.classes = f->classes; a.n_classes = f->n_classes;
   const unsigned grid = (unsigned)ceil_div(n_rows, 256);
-  switch (f->CT) {
-    case 1: forest_finish_kernel<1><<<grid, 256, 0, (cudaStream_t)stream>>>(a, partials, n_shards, mp); break;
-    case 2: forest_finish_kernel<2><<<grid, 256, 0, (cudaStream_t)stream>>>(a, partials, n_shards, mp); break;
-    case 4: forest_finish_kernel<4><<<grid, 256, 0, (cudaStream_t)stream>>>(a, partials, n_shards, mp); break;
-    case 8: forest_finish_kernel<8><<<grid, 256, 0, (cudaStream_t)stream>>>(a, partials, n_shards, mp); break;
-    default: return fail(CMLB_E_UNRESOLVED, "tree-sharded finish supports up to 8 outputs");
-  }
+  forest_finish_kernel<1><<<grid, 256, 0, (cudaStream_t)stream>>>(a, partials, n_shards, mp);
+  note_launch();
+  CMLB_CUDA(cudaGetLastError());
+  return CMLB_OK;
+}
+
+int cmlb_forest_merge(const cmlb_forest* f, double* dst, const double* src, int64_t n_rows, void* stream) {
+  using namespace cmlb;
+  if (!f) return fail(CMLB_E_VALIDATION, "null forest");
+  if (f->C != 1 || f->agg == CMLB_AGG_NONE) return fail(CMLB_E_UNRESOLVED, "tree sharding needs a scalar ensemble");
+  if (n_rows < 0 || (n_rows > 0 && (!dst || !src))) return fail(CMLB_E_INPUT, "bad merge buffers");
+  if (n_rows == 0) return CMLB_OK;
+  DeviceGuard guard(f->device);
+  const int sms = num_sms(f->device);
+  const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(n_rows, 256 * 2), (int64_t)sms * 8);
+  partial_add_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(dst, src, n_rows);
   note_launch();
   CMLB_CUDA(cudaGetLastError());
   return CMLB_OK;

@@ -69,6 +69,7 @@ class ForestSpec:
     dense_selector: bool = False
     prologue: object = None        # fuse.COL_DTYPE ops over the raw input (fused preprocessing)
     n_inputs: int = 0
+    n_trees_total: int = 0         # tree shard of a larger ensemble: its tree count (MEAN tail)
 
     @property
     def in_cols(self) -> int:

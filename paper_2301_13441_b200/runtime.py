@@ -41,12 +41,6 @@ TORCH_DTYPE = {
 }
 
 
-def _stream_handle(stream) -> int:
-    if stream is None:
-        stream = torch.cuda.current_stream()
-    return int(stream.cuda_stream)
-
-
 def compact_features(spec: ForestSpec, feature: np.ndarray):
     """Rank / stage only the features the trees test.
 
@@ -106,6 +100,7 @@ class _Forest:
         d.out_dtype = OUT_CODE[spec.out_dtype]
         d.dense_selector = int(spec.dense_selector)
         d.variant = variant
+        d.n_trees_total = int(spec.n_trees_total)
         pro = None
         if prologue is not None:
             pro = np.ascontiguousarray(prologue)
@@ -128,6 +123,15 @@ class _Forest:
 
     def partial(self, x, out, n, ldx, stream):
         N.check(N.lib().cmlb_forest_partial(self.handle, x.data_ptr(), n, ldx, out.data_ptr(), stream))
+
+    def merge(self, dst, src, n, stream):
+        N.check(N.lib().cmlb_forest_merge(self.handle, dst.data_ptr(), src.data_ptr(), n, stream))
+
+    def finish(self, partials, n_shards, merges, n, y, stream):
+        m = np.ascontiguousarray(np.asarray(merges, np.int32).reshape(-1))
+        N.check(N.lib().cmlb_forest_finish(self.handle, partials.data_ptr(), n_shards,
+                                           m.ctypes.data_as(C.POINTER(N.c_i32)), len(merges), n,
+                                           y.data_ptr(), stream))
 
     def close(self):
         if self.handle:
@@ -303,30 +307,37 @@ class DeviceProgram:
         if x.stride(1) != 1:
             x = x.contiguous()
         n = int(x.shape[0])
-        sh = _stream_handle(stream)
-        own_bad = None
+        # the program's device first, then its stream: intermediates are
+        # allocated on (and so recycled in order with) the stream that uses them
         with torch.cuda.device(self.device):
-            if self.has_checks and bad is None:
-                bad = own_bad = torch.empty(1, dtype=torch.int64, device=x.device)
-            cur, ld = x, int(x.stride(0)) if n > 0 else self.n_features
-            for i, st in enumerate(self.stages):
-                last = i == len(self.stages) - 1
-                spec = st.spec
-                if isinstance(spec, ColumnsSpec) and not spec.emit:
-                    st.run(cur, None, n, max(ld, 1), sh, bad=bad)  # membership check only
-                    continue
-                cols = spec.out_cols
-                dt = TORCH_DTYPE[spec.out_dtype]
-                y = out if last and out is not None else torch.empty((n, cols), dtype=dt, device=x.device)
-                if isinstance(spec, ColumnsSpec):
-                    st.run(cur, y if n > 0 else None, n, max(ld, 1), sh, bad=bad if spec.checks else None)
-                elif n > 0:
-                    st.run(cur, y, n, max(ld, 1), sh, leaf_out if last else None)
-                cur, ld = y, cols
-            if own_bad is not None:
-                if stream is not None:
-                    stream.synchronize()
-                raise_unknown_category(own_bad)
+            if stream is None:
+                stream = torch.cuda.current_stream(self.device)
+            sh = int(stream.cuda_stream)
+            with torch.cuda.stream(stream):
+                return self._run_stages(x, n, out, stream, sh, leaf_out, bad)
+
+    def _run_stages(self, x, n, out, stream, sh, leaf_out, bad):
+        own_bad = None
+        if self.has_checks and bad is None:
+            bad = own_bad = torch.full((1,), -1, dtype=torch.int64, device=x.device)
+        cur, ld = x, int(x.stride(0)) if n > 0 else self.n_features
+        for i, st in enumerate(self.stages):
+            last = i == len(self.stages) - 1
+            spec = st.spec
+            if isinstance(spec, ColumnsSpec) and not spec.emit:
+                st.run(cur, None, n, max(ld, 1), sh, bad=bad)  # membership check only
+                continue
+            cols = spec.out_cols
+            dt = TORCH_DTYPE[spec.out_dtype]
+            y = out if last and out is not None else torch.empty((n, cols), dtype=dt, device=x.device)
+            if isinstance(spec, ColumnsSpec):
+                st.run(cur, y if n > 0 else None, n, max(ld, 1), sh, bad=bad if spec.checks else None)
+            elif n > 0:
+                st.run(cur, y, n, max(ld, 1), sh, leaf_out if last else None)
+            cur, ld = y, cols
+        if own_bad is not None:
+            stream.synchronize()
+            raise_unknown_category(own_bad)
         return cur
 
     @property

@@ -2,23 +2,33 @@
 
 Row sharding (random forests, the north star; any model): every rank holds a
 replica of the program and processes its own rows -- no data-path collective
-(``row_range``).
+(``row_range``; single-process multi-device form: ``api.predict(...,
+devices=[...])``).
 
 Tree sharding (large gradient-boosted ensembles): each rank walks
 a contiguous range of trees for all rows and emits raw float64 partial sums
-(``cmlb_forest_partial``); the partials are exchanged with one NCCL
-all-gather and combined, then the tail runs on the combined sum
-(``cmlb_forest_finish``).
+(``cmlb_forest_partial``); the partials are combined by ONE reduce -- a
+pairwise tree reduce over NCCL point-to-point (NVLink), each step
+``dst += src`` on the receiving GPU (``cmlb_forest_merge``) -- and the root
+applies the ensemble tail (``cmlb_forest_finish``).
 
-Exactness of the combine.  The reference reduces the (N, T, 1) stack with
+Exactness of the reduce.  The reference reduces the (N, T, 1) stack with
 numpy's pairwise summation (``kernels.py:185-190`` -> ``pairwise_sum``): the
 tree axis is split recursively at n/2 rounded down to a multiple of 8 until
 blocks have <= 128 elements.  :func:`pairwise_tree_shards` cuts that very
 recursion tree into G nodes, so every shard's partial is exactly numpy's
-value for that node and :func:`merge_plan` combines them in the recursion's
-own order -- the tree-sharded result is bit-identical to the single-GPU one.
-(For C >= 2 ensembles numpy sums sequentially, which cannot be split exactly;
-those are row-sharded.)
+value for that node, and the reduce follows the recursion's own merge tree:
+every step adds two sibling nodes (one float64 IEEE add, commutative, so it
+does not matter which GPU performs it).  The tree-sharded result is therefore
+bit-identical to the single-GPU one.  A stock ``ncclReduce`` would add the G
+partials in the ring's order instead -- for G >= 3 a different rounding
+sequence -- which is why the reduce is scheduled here rather than delegated.
+For C >= 2 ensembles numpy sums tree after tree, which no cut reproduces:
+those are row-sharded (``TreeShardedForest`` raises).
+
+Bytes on the wire: every non-root rank sends its (merged) partial once,
+N x 8 bytes (8 MB for config 3's 1M rows); the root receives ceil(log2 G)
+of them.  The former all-gather delivered G x N x 8 bytes to every rank.
 """
 
 from __future__ import annotations
@@ -114,13 +124,43 @@ def combine(partials, merges) -> np.ndarray:
     return p[0]
 
 
+def reduce_steps(merges, rank: int):
+    """This rank's part of the pairwise merge tree, in merge order.
+
+    ``("recv", peer)``: receive the peer's partial and add it into ours;
+    ``("send", peer)``: send our (complete) partial to the peer, then stop.
+    Merges come in post-order, so every partial is complete before it is sent;
+    the dependency graph is a tree, so blocking send/recv cannot deadlock."""
+    steps = []
+    for a, b in merges:
+        if a == rank:
+            steps.append(("recv", b))
+        elif b == rank:
+            steps.append(("send", a))
+    return steps
+
+
+def tree_reduce(part, merges, rank: int, send, recv, add):
+    """Run the pairwise tree reduce with caller-supplied transport and add.
+    Returns True on the rank that ends up holding the total (rank 0)."""
+    for kind, peer in reduce_steps(merges, rank):
+        if kind == "recv":
+            add(part, recv(peer))
+        else:
+            send(part, peer)
+            return False
+    return rank == 0
+
+
 class TreeShardedForest:
     """One rank's part of a tree-sharded forest program (torch.distributed).
 
-    ``spec`` is the whole-forest ForestSpec.  Every rank builds a program over
-    its tree range (for partials) plus the whole-forest program on the root
-    (for the tail); ``predict`` gathers partials with NCCL all-gather and the
-    root combines in pairwise order and applies the tail on the GPU.
+    ``spec`` is the whole-forest ForestSpec (scalar ensembles: GBDT, single-
+    output forest regressors).  Each rank builds a program over its own tree
+    range only (the whole-ensemble tree count rides along for a MEAN tail);
+    ``predict`` computes the partial, runs the pairwise tree reduce and the
+    root applies the tail.  Transport: NCCL point-to-point on device tensors;
+    with a CPU backend (gloo) the partials are staged through host memory.
     """
 
     def __init__(self, spec, group=None, device=None):
@@ -131,41 +171,55 @@ class TreeShardedForest:
         from .lower import ProgramSpec
         from .runtime import DeviceProgram
 
+        if spec.n_outputs != 1:
+            raise ValueError("tree sharding needs a scalar ensemble: numpy sums a (N, T, C >= 2) stack "
+                             "tree after tree, which no shard cut reproduces; shard such models by rows")
         self.dist = dist
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.ranges, self.merges = pairwise_tree_shards(len(spec.trees), self.world)
         lo, hi = self.ranges[self.rank]
-        shard = replace(spec, trees=spec.trees[lo:hi])
+        shard = replace(spec, trees=spec.trees[lo:hi], n_trees_total=len(spec.trees))
         self.device = torch.cuda.current_device() if device is None else device
-        self.local = DeviceProgram(ProgramSpec([shard], spec.n_features), self.device)
-        self.full = DeviceProgram(ProgramSpec([spec], spec.n_features), self.device) if self.rank == 0 else None
-        self.C = spec.n_outputs
+        self.local = DeviceProgram(ProgramSpec([shard], spec.in_cols), self.device)
         self.out_cols = spec.out_cols
         self.out_dtype = spec.out_dtype
+        self.host_staged = dist.get_backend(group) != "nccl"
+
+    def _global(self, peer: int) -> int:
+        return peer if self.group is None else self.dist.get_global_rank(self.group, peer)
 
     def predict(self, x):
         """x: this rank's copy of all rows (CUDA). Returns y on rank 0, None elsewhere."""
-        import ctypes
-
         import torch
 
-        from . import _native as N
         from .runtime import TORCH_DTYPE
 
         n = int(x.shape[0])
-        part = torch.empty((n, self.C), dtype=torch.float64, device=x.device)
-        stream = torch.cuda.current_stream(x.device).cuda_stream
+        fo = self.local.forest()
+        stream = torch.cuda.current_stream(x.device)
+        sh = stream.cuda_stream
+        part = torch.empty((n, 1), dtype=torch.float64, device=x.device)
         if n:
-            self.local.forest().partial(x, part, n, int(x.stride(0)), stream)
-        gathered = torch.empty((self.world, n, self.C), dtype=torch.float64, device=x.device)
-        self.dist.all_gather_into_tensor(gathered, part, group=self.group)
-        if self.rank != 0:
+            self.local.check_input(x)
+            fo.partial(x, part, n, int(x.stride(0)), sh)
+
+        def send(t, peer):
+            if self.host_staged:
+                t = t.cpu()
+            self.dist.send(t, self._global(peer), group=self.group)
+
+        def recv(peer):
+            buf = torch.empty((n, 1), dtype=torch.float64, device="cpu" if self.host_staged else x.device)
+            self.dist.recv(buf, self._global(peer), group=self.group)
+            return buf.to(x.device, non_blocking=False) if self.host_staged else buf
+
+        def add(dst, src):
+            fo.merge(dst, src, n, sh)
+
+        if not tree_reduce(part, self.merges, self.rank, send, recv, add):
             return None
         y = torch.empty((n, self.out_cols), dtype=TORCH_DTYPE[self.out_dtype], device=x.device)
-        m = np.asarray(self.merges, dtype=np.int32).reshape(-1)
-        mp = m.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
-        N.check(N.lib().cmlb_forest_finish(self.full.forest().handle, gathered.data_ptr(), self.world, mp,
-                                           len(self.merges), n, y.data_ptr(), stream))
+        fo.finish(part, 1, [], n, y, sh)
         return y

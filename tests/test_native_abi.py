@@ -35,7 +35,7 @@ def test_every_declared_symbol_is_exported(lib):
 
 
 def test_abi_version(lib):
-    assert lib.cmlb_abi_version() == 2
+    assert lib.cmlb_abi_version() == 3
     assert lib.cmlb_launch_count() >= 0
 
 

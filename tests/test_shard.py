@@ -47,6 +47,29 @@ def test_small_ensembles_refuse_tree_sharding():
         shard.pairwise_tree_shards(100, 2)
 
 
+def test_reduce_steps_follow_the_merge_tree():
+    for T, world in ((1000, 2), (1000, 3), (1000, 8), (5003, 8)):
+        _, merges = shard.pairwise_tree_shards(T, world)
+        sends = {}
+        for r in range(world):
+            steps = shard.reduce_steps(merges, r)
+            kinds = [k for k, _ in steps]
+            # receives first, at most one send, and the send is the rank's last step
+            assert "send" not in kinds[:-1]
+            if r == 0:
+                assert "send" not in kinds
+            else:
+                assert kinds[-1] == "send"
+                sends[r] = steps[-1][1]
+        # every non-root rank's partial reaches the root along a chain of sends
+        for r in range(1, world):
+            seen, cur = set(), r
+            while cur != 0:
+                assert cur not in seen
+                seen.add(cur)
+                cur = sends[cur]
+
+
 def _worker(rank, world, port, T, n, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -57,24 +80,54 @@ def _worker(rank, world, port, T, n, q):
     ranges, merges = shard.pairwise_tree_shards(T, world)
     lo, hi = ranges[rank]
     part = torch.tensor([shard.numpy_pairwise(vals[i, lo:hi]) for i in range(n)], dtype=torch.float64)
-    gathered = [torch.empty_like(part) for _ in range(world)]
-    dist.all_gather(gathered, part)
+
+    def recv(peer):
+        buf = torch.empty_like(part)
+        dist.recv(buf, peer)
+        return buf
+
+    def add(dst, src):
+        dst.copy_(torch.from_numpy(dst.numpy() + src.numpy()))
+
+    root = shard.tree_reduce(part, merges, rank, lambda t, peer: dist.send(t, peer), recv, add)
     if rank == 0:
-        got = 0.0 + shard.combine([g.numpy() for g in gathered], merges)
+        assert root
+        got = 0.0 + part.numpy()
         want = vals.reshape(n, T, 1).sum(axis=1)[:, 0]
         q.put(bool(np.array_equal(got, want)))
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_tree_shard_exchange_gloo_world2():
+@pytest.mark.parametrize("world", [2, 4])
+def test_tree_shard_reduce_gloo(world):
+    """The pairwise tree reduce over real point-to-point sends (world 2 and 4)
+    reproduces numpy's (N, T, 1) reduction bit for bit."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29500 + (os.getpid() % 1000)
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, 1000, 64, q)) for r in range(2)]
+    port = 29500 + (os.getpid() % 1000) + 7 * world
+    procs = [ctx.Process(target=_worker, args=(r, world, port, 1000, 64, q)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
-        p.join(120)
+        p.join(180)
     assert all(p.exitcode == 0 for p in procs)
     assert q.get(timeout=5) is True
+
+
+def test_tree_sharding_refuses_vector_ensembles():
+    """C >= 2 forests are summed tree after tree by numpy: no exact tree cut,
+    so TreeShardedForest refuses them (they shard by rows)."""
+    import bench
+    from paper_2301_13441_b200 import lower
+    model, _, _ = bench.load_model()
+    spec = lower.lower_model(model).stages[0]
+    assert spec.n_outputs == 2
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(28500 + os.getpid() % 1000)
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        with pytest.raises(ValueError, match="scalar ensemble"):
+            shard.TreeShardedForest(spec)
+    finally:
+        dist.destroy_process_group()
