@@ -236,7 +236,7 @@ def main(argv=None):
     ap.add_argument("--rows", type=int, default=10_000_000)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--variant", default="auto", choices=["auto", "ranked", "perfect", "general", "mma"],
+    ap.add_argument("--variant", default="auto", choices=["auto", "ranked", "skew", "perfect", "general", "mma"],
                     help="force a forest kernel variant (measurement; default: the measured AUTO choice)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
@@ -262,7 +262,7 @@ def main(argv=None):
     else:
         from paper_2301_13441_b200.runtime import DeviceProgram
         prog = DeviceProgram(compiled.spec, dev.index, forest_variant={
-            "ranked": N.FOREST_RANKED, "perfect": N.FOREST_PERFECT, "general": N.FOREST_GENERAL,
+            "ranked": N.FOREST_RANKED, "skew": N.FOREST_SKEW, "perfect": N.FOREST_PERFECT, "general": N.FOREST_GENERAL,
             "mma": N.FOREST_MMA}[args.variant])
     info = prog.forest().info()
     n = args.rows

@@ -100,7 +100,9 @@ enum cmlb_forest_variant {
   CMLB_FOREST_PERFECT = 1,     /* perfect-padded trees staged in shared memory */
   CMLB_FOREST_GENERAL = 2,     /* arbitrary depth, canonical nodes read through L1 */
   CMLB_FOREST_RANKED = 3,      /* perfect trees, rank-quantized thresholds: one word per node */
-  CMLB_FOREST_MMA = 4          /* the GEMM form on tcgen05 kind::i8: bits x path matrix in TMEM */
+  CMLB_FOREST_MMA = 4,         /* the GEMM form on tcgen05 kind::i8: bits x path matrix in TMEM */
+  CMLB_FOREST_SKEW = 5         /* ranked walk, 32-tree groups skewed across the smem banks; only
+                                * for forests whose float64 sums are certified order-free (ABI 3) */
 };
 
 typedef struct cmlb_forest_desc {
@@ -301,6 +303,10 @@ void cmlb_columns_destroy(cmlb_columns* c);
 /* The numpy pairwise-sum replay codes the forest kernels use for C == 1
  * ensembles (tests/test_native_abi.py checks them against numpy). */
 int cmlb_debug_pairwise_schedule(int64_t n, uint32_t* codes);
+/* 1 when the forest's float64 sums over trees are certified exact in any
+ * order (the SKEW variant's precondition), 0 when not, <0 on a bad
+ * descriptor.  Host only. */
+int cmlb_debug_sums_order_free(const cmlb_forest_desc* desc);
 /* SVM fast path only, on every row, with the epilogue's per-row error bound
  * written to err (device float32 [n_rows]); CMLB_SVM_PROBE switches pipeline
  * roles off (tools/svm_pipe_probe.py). */

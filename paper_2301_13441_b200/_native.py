@@ -73,7 +73,7 @@ class ColumnsDesc(C.Structure):
 # enum values (cmlb.h)
 AGG_NONE, AGG_MEAN, AGG_SUM = 0, 1, 2
 TAIL_VALUES, TAIL_ARGMAX, TAIL_SIGMOID = 0, 1, 2
-FOREST_AUTO, FOREST_PERFECT, FOREST_GENERAL, FOREST_RANKED, FOREST_MMA = 0, 1, 2, 3, 4
+FOREST_AUTO, FOREST_PERFECT, FOREST_GENERAL, FOREST_RANKED, FOREST_MMA, FOREST_SKEW = 0, 1, 2, 3, 4, 5
 LIN_VALUES, LIN_ARGMAX, LIN_SOFTMAX_ARGMAX, LIN_SIGMOID, LIN_SIGN = 0, 1, 2, 3, 4
 (SCALER_BINARIZER, SCALER_NORM_L1, SCALER_NORM_L2, SCALER_NORM_MAX, SCALER_MINMAX,
  SCALER_SUB_DIV, SCALER_DIV) = range(7)
@@ -108,6 +108,7 @@ SIGNATURES = {
     "cmlb_columns_run": (C.c_int, [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp]),
     "cmlb_columns_destroy": (None, [c_vp]),
     "cmlb_debug_pairwise_schedule": (C.c_int, [c_i64, P(C.c_uint32)]),
+    "cmlb_debug_sums_order_free": (C.c_int, [P(ForestDesc)]),
 }
 
 

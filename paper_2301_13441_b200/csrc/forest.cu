@@ -36,6 +36,7 @@
 //           stack.  Verified against numpy in tests/test_pairwise_schedule.py.
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <limits>
 #include <cstring>
@@ -585,71 +586,21 @@ __device__ __forceinline__ void load_payload(const float* p, float (&v)[CT]) {
   }
 }
 
-template <int CT, int NTT, int RPT, int TI, bool PW>
-__global__ void __launch_bounds__(NTT, 1) forest_ranked_kernel(const ForestArgs a) {
-  extern __shared__ __align__(16) uint8_t smem[];
+// Rank the CTA's row tile (both ranked kernels): for every feature f and row
+// r of the tile, rank(x[r][f]) = #{u in U_f : u < x} into the u16 rank tile at
+// the start of shared memory (layout: see the callers' pb()).
+// Feature f's Eytzinger thresholds + index map are staged with TMA into
+// buffer f&1 of the staging area (inside the tree-chunk region) while the CTA
+// searches feature f-1's buffer (double buffering: one barrier per feature).
+// Row values are read eight features at a time.
+template <int NTT, int RPT>
+__device__ __forceinline__ void rank_tile(const ForestArgs& a, uint8_t* smem, uint8_t* chunk, uint64_t* stage_bar,
+                                          const int64_t (&rowk)[RPT], const uint32_t (&pb)[RPT],
+                                          const int (&nbad)[RPT]) {
   constexpr int ROWS = NTT * RPT;
-  static_assert(ROWS % 64 == 0, "rank tile interleave needs 64-row groups");
-  static_assert(TI == 2 || TI == 4, "trees per step");
   const int tid = threadIdx.x;
-  const int64_t tile = (int64_t)blockIdx.x * ROWS;
   const int F = a.F;
   uint16_t* xr = reinterpret_cast<uint16_t*>(smem);
-  const uint32_t chunk_off = (uint32_t)(((size_t)F * ROWS * 2 + 15) & ~(size_t)15);
-  uint8_t* chunk = smem + chunk_off;
-  // Two tree buffers of chunk_trees trees each, filled by TMA bulk copies one
-  // chunk ahead of the walk.  The ranking staging area lives in buffer 1 when
-  // it fits there (a.stage_off != 0), so chunk 0 streams in during ranking.
-  __shared__ __align__(8) uint64_t tree_bar[2];
-  __shared__ __align__(8) uint64_t stage_bar[2];   // per-feature threshold staging (TMA)
-  const uint32_t buf_bytes = (uint32_t)a.chunk_trees * a.tree_bytes;
-  const int T = a.T;
-  const int nchunks = (T + a.chunk_trees - 1) / a.chunk_trees;
-  auto issue_chunk = [&](int ci) {  // thread 0 only
-    const int c0 = ci * a.chunk_trees;
-    const uint32_t bytes = (uint32_t)min(a.chunk_trees, T - c0) * a.tree_bytes;
-    uint8_t* dst = chunk + (ci & 1) * buf_bytes;
-    const uint8_t* src = a.blob + (size_t)c0 * a.tree_bytes;
-    fence_proxy_async();
-    mbar_expect_tx(&tree_bar[ci & 1], bytes);
-    for (uint32_t off = 0; off < bytes; off += 32768u)
-      bulk_g2s(dst + off, src + off, min(32768u, bytes - off), &tree_bar[ci & 1]);
-  };
-  if (tid == 0) {
-    mbar_init(&tree_bar[0], 1);
-    mbar_init(&tree_bar[1], 1);
-    mbar_init(&stage_bar[0], 1);
-    mbar_init(&stage_bar[1], 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-  if (tid == 0 && a.stage_off) issue_chunk(0);
-
-  // Rank tile layout: u16 rank of (feature f, row r) at byte f*ROWS*2 + pb(r)
-  // with pb(r) = 2*((r/64)*64 + (r%32)*2 + (r/32)%2): rows r and r+32 share a
-  // 32-bit word, so lane l of every warp owns bank l for every feature and the
-  // per-level gathers are conflict-free whatever features the lanes test.
-  // Node words carry the feature as that byte offset (f*ROWS*2 < 65536, its
-  // bits disjoint from pb's), so a gather address is one LOP3.
-  int64_t rowk[RPT];
-  uint32_t pb[RPT];
-  int nbad[RPT];
-#pragma unroll
-  for (int k = 0; k < RPT; ++k) {
-    const int r = tid + k * NTT;
-    rowk[k] = tile + r;
-    pb[k] = 2u * (uint32_t)(((r >> 6) << 6) | ((r & 31) << 1) | ((r >> 5) & 1));
-    nbad[k] = 0;
-    if (a.dense_sel && rowk[k] < a.n_rows) {
-      const float* src = a.x + rowk[k] * a.ldx;
-      for (int f = 0; f < F; ++f) nbad[k] += !isfinite(load_col(a.pro, src, f));
-    }
-  }
-
-  // ---- rank the row tile ---------------------------------------------------
-  // Feature f's Eytzinger thresholds + index map are staged with cp.async into
-  // buffer f&1 while the CTA searches feature f-1's buffer (double buffering:
-  // one barrier per feature).  Row values are read eight features at a time.
   const int cap = a.stage_cap;  // thresholds per staging buffer
   // two staging buffers when they fit (a.stage_bufs == 2: prefetch feature f+1
   // while searching f), else one (an extra barrier per feature)
@@ -721,6 +672,70 @@ __global__ void __launch_bounds__(NTT, 1) forest_ranked_kernel(const ForestArgs 
       }
     }
   }
+}
+
+template <int CT, int NTT, int RPT, int TI, bool PW>
+__global__ void __launch_bounds__(NTT, 1) forest_ranked_kernel(const ForestArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int ROWS = NTT * RPT;
+  static_assert(ROWS % 64 == 0, "rank tile interleave needs 64-row groups");
+  static_assert(TI == 2 || TI == 4, "trees per step");
+  const int tid = threadIdx.x;
+  const int64_t tile = (int64_t)blockIdx.x * ROWS;
+  const int F = a.F;
+  uint16_t* xr = reinterpret_cast<uint16_t*>(smem);
+  const uint32_t chunk_off = (uint32_t)(((size_t)F * ROWS * 2 + 15) & ~(size_t)15);
+  uint8_t* chunk = smem + chunk_off;
+  // Two tree buffers of chunk_trees trees each, filled by TMA bulk copies one
+  // chunk ahead of the walk.  The ranking staging area lives in buffer 1 when
+  // it fits there (a.stage_off != 0), so chunk 0 streams in during ranking.
+  __shared__ __align__(8) uint64_t tree_bar[2];
+  __shared__ __align__(8) uint64_t stage_bar[2];   // per-feature threshold staging (TMA)
+  const uint32_t buf_bytes = (uint32_t)a.chunk_trees * a.tree_bytes;
+  const int T = a.T;
+  const int nchunks = (T + a.chunk_trees - 1) / a.chunk_trees;
+  auto issue_chunk = [&](int ci) {  // thread 0 only
+    const int c0 = ci * a.chunk_trees;
+    const uint32_t bytes = (uint32_t)min(a.chunk_trees, T - c0) * a.tree_bytes;
+    uint8_t* dst = chunk + (ci & 1) * buf_bytes;
+    const uint8_t* src = a.blob + (size_t)c0 * a.tree_bytes;
+    fence_proxy_async();
+    mbar_expect_tx(&tree_bar[ci & 1], bytes);
+    for (uint32_t off = 0; off < bytes; off += 32768u)
+      bulk_g2s(dst + off, src + off, min(32768u, bytes - off), &tree_bar[ci & 1]);
+  };
+  if (tid == 0) {
+    mbar_init(&tree_bar[0], 1);
+    mbar_init(&tree_bar[1], 1);
+    mbar_init(&stage_bar[0], 1);
+    mbar_init(&stage_bar[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (tid == 0 && a.stage_off) issue_chunk(0);
+
+  // Rank tile layout: u16 rank of (feature f, row r) at byte f*ROWS*2 + pb(r)
+  // with pb(r) = 2*((r/64)*64 + (r%32)*2 + (r/32)%2): rows r and r+32 share a
+  // 32-bit word, so lane l of every warp owns bank l for every feature and the
+  // per-level gathers are conflict-free whatever features the lanes test.
+  // Node words carry the feature as that byte offset (f*ROWS*2 < 65536, its
+  // bits disjoint from pb's), so a gather address is one LOP3.
+  int64_t rowk[RPT];
+  uint32_t pb[RPT];
+  int nbad[RPT];
+#pragma unroll
+  for (int k = 0; k < RPT; ++k) {
+    const int r = tid + k * NTT;
+    rowk[k] = tile + r;
+    pb[k] = 2u * (uint32_t)(((r >> 6) << 6) | ((r & 31) << 1) | ((r >> 5) & 1));
+    nbad[k] = 0;
+    if (a.dense_sel && rowk[k] < a.n_rows) {
+      const float* src = a.x + rowk[k] * a.ldx;
+      for (int f = 0; f < F; ++f) nbad[k] += !isfinite(load_col(a.pro, src, f));
+    }
+  }
+
+  rank_tile<NTT, RPT>(a, smem, chunk, stage_bar, rowk, pb, nbad);
 
   RowAcc<CT, PW> acc[RPT];
   double pw_stack[PW ? RPT : 1][PW ? SMAX : 1];
@@ -838,6 +853,176 @@ __global__ void __launch_bounds__(NTT, 1) forest_ranked_kernel(const ForestArgs 
 #pragma unroll
   for (int k = 0; k < RPT; ++k)
     if (rowk[k] < a.n_rows) finish_row<CT, PW>(a, rowk[k], acc[k], none);
+}
+
+// ---------------------------------------------------------------------------
+// SKEW variant: the ranked walk with trees skewed across the shared-memory banks
+// ---------------------------------------------------------------------------
+//
+// In the row-parallel walk every lane of a warp walks the SAME tree for its own
+// row, so below level 5 the lanes read different node words of one small array
+// and collide in the banks (ncu, RF500 d8: 26% of all shared-memory wavefronts
+// were conflict replays on levels 6-7 and the leaf payloads).  Here trees come
+// in groups of 32 stored interleaved -- node j of tree t at word 32*j + t,
+// payload of leaf slot s of tree t at (32*s + t) * CT floats -- and at step s
+// lane l walks tree (l + s + q*32/TI) mod 32 of the group for its rows
+// (q < TI independent walks).  The 32 lanes of a warp therefore touch 32
+// different trees, i.e. 32 different banks, at every level and for the
+// payload: every node, rank and payload load is conflict-free.
+//
+// Each lane now visits the trees of a group in a rotated order, so the
+// per-row sums are no longer formed in tree order.  This variant is only
+// selected when the host has CERTIFIED the sums order-free (sums_order_free():
+// every payload is a multiple of 2^-q and the largest possible partial sum is
+// below 2^(53-q), so every float64 partial sum in ANY order is exact and equals
+// numpy's sequential or pairwise result bit for bit).  Padding trees of the
+// last group go always-left onto a zero payload (+0.0 changes no exact sum).
+template <int CT, int NTT, int RPT, int TI>
+__global__ void __launch_bounds__(NTT, 1) forest_skew_kernel(const ForestArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int ROWS = NTT * RPT;
+  constexpr int STEPS = 32 / TI;
+  static_assert(ROWS % 64 == 0, "rank tile interleave needs 64-row groups");
+  static_assert(TI == 1 || TI == 2 || TI == 4 || TI == 8, "walks per step");
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t tile = (int64_t)blockIdx.x * ROWS;
+  const int F = a.F;
+  const uint32_t chunk_off = (uint32_t)(((size_t)F * ROWS * 2 + 15) & ~(size_t)15);
+  uint8_t* chunk = smem + chunk_off;
+  __shared__ __align__(8) uint64_t tree_bar[2];
+  __shared__ __align__(8) uint64_t stage_bar[2];
+  const uint32_t gbytes = (uint32_t)a.tree_bytes;              // one 32-tree group
+  const uint32_t buf_bytes = (uint32_t)a.chunk_trees * gbytes;  // chunk_trees = groups per buffer here
+  const int T = a.T;
+  const int G = (T + 31) >> 5;
+  const int nchunks = (G + a.chunk_trees - 1) / a.chunk_trees;
+  auto issue_chunk = [&](int ci) {  // thread 0 only
+    const int g0 = ci * a.chunk_trees;
+    const uint32_t bytes = (uint32_t)min(a.chunk_trees, G - g0) * gbytes;
+    uint8_t* dst = chunk + (ci & 1) * buf_bytes;
+    const uint8_t* src = a.blob + (size_t)g0 * gbytes;
+    fence_proxy_async();
+    mbar_expect_tx(&tree_bar[ci & 1], bytes);
+    for (uint32_t off = 0; off < bytes; off += 32768u)
+      bulk_g2s(dst + off, src + off, min(32768u, bytes - off), &tree_bar[ci & 1]);
+  };
+  if (tid == 0) {
+    mbar_init(&tree_bar[0], 1);
+    mbar_init(&tree_bar[1], 1);
+    mbar_init(&stage_bar[0], 1);
+    mbar_init(&stage_bar[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (tid == 0 && a.stage_off) issue_chunk(0);
+
+  int64_t rowk[RPT];
+  uint32_t pb[RPT];
+  int nbad[RPT];
+#pragma unroll
+  for (int k = 0; k < RPT; ++k) {
+    const int r = tid + k * NTT;
+    rowk[k] = tile + r;
+    pb[k] = 2u * (uint32_t)(((r >> 6) << 6) | ((r & 31) << 1) | ((r >> 5) & 1));
+    nbad[k] = 0;
+    if (a.dense_sel && rowk[k] < a.n_rows) {
+      const float* src = a.x + rowk[k] * a.ldx;
+      for (int f = 0; f < F; ++f) nbad[k] += !isfinite(load_col(a.pro, src, f));
+    }
+  }
+  rank_tile<NTT, RPT>(a, smem, chunk, stage_bar, rowk, pb, nbad);
+
+  double acc[RPT][CT];
+#pragma unroll
+  for (int k = 0; k < RPT; ++k)
+#pragma unroll
+    for (int c = 0; c < CT; ++c) acc[k][c] = 0.0;
+
+  const int D = a.depth;
+  const int ni = a.ni;
+  const uint8_t* xrb = smem;
+  const uint32_t smem_base = smem_u32(smem);
+
+  // One step of one group: TI walks per row, tree (lane + s + q*STEPS) & 31.
+  auto walk_step = [&](auto leafconst, uint32_t gofs, int g, int s) {
+    constexpr bool LEAF = decltype(leafconst)::value;
+    const uint32_t nb = gofs + (uint32_t)a.node_off_bytes;  // node words of this group
+    uint32_t o[TI][RPT], cst[TI], tq[TI];
+#pragma unroll
+    for (int q = 0; q < TI; ++q) {
+      tq[q] = (uint32_t)(lane + s + q * STEPS) & 31u;
+      cst[q] = 128u - nb - 4u * tq[q];  // child j' = 2j+1(+1): o' = 2o + cst (+128)
+#pragma unroll
+      for (int k = 0; k < RPT; ++k) o[q][k] = nb + 4u * tq[q];
+    }
+    auto level = [&]() {
+#pragma unroll
+      for (int q = 0; q < TI; ++q) {
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) {
+          const uint32_t w = *reinterpret_cast<const uint32_t*>(smem + o[q][k]);
+          const uint32_t rk = *reinterpret_cast<const uint16_t*>(xrb + ((w >> 14) + pb[k]));
+          uint32_t nx = 2u * o[q][k] + cst[q];
+          if (rk > (w & 0xFFFFu)) nx += 128u;
+          o[q][k] = nx;
+        }
+      }
+    };
+    int lvl = 0;
+    for (; lvl + 2 <= D; lvl += 2) { level(); level(); }
+    if (lvl < D) level();
+    // leaf: o = nb + 4*(32*j + t), j >= ni; payload at gofs + (32*(j - ni) + t)*CT*4
+    const uint32_t pay_c = smem_base + gofs - (nb + (uint32_t)ni * 128u) * CT;
+#pragma unroll
+    for (int q = 0; q < TI; ++q) {
+#pragma unroll
+      for (int k = 0; k < RPT; ++k) {
+        float v[CT];
+        load_payload_shared<CT>(pay_c + o[q][k] * CT, v);
+#pragma unroll
+        for (int c = 0; c < CT; ++c) acc[k][c] += (double)v[c];
+        if constexpr (LEAF) {
+          const int t = g * 32 + (int)tq[q];
+          if (t < T && rowk[k] < a.n_rows) {
+            const int slot = (int)(((o[q][k] - nb) >> 2) >> 5) - ni;
+            a.leaf_out[rowk[k] * T + t] = __ldg(a.slot_leaf + (int64_t)t * a.ns + slot);
+          }
+        }
+      }
+    }
+  };
+
+  __syncthreads();  // ranks complete; staging buffers no longer read
+  if (tid == 0 && !a.stage_off) issue_chunk(0);
+  for (int ci = 0; ci < nchunks; ++ci) {
+    const int g0 = ci * a.chunk_trees;
+    const int ng = min(a.chunk_trees, G - g0);
+    if (tid == 0 && ci + 1 < nchunks) issue_chunk(ci + 1);
+    mbar_wait(&tree_bar[ci & 1], (uint32_t)(ci >> 1) & 1u);
+    const uint32_t buf_off = chunk_off + (uint32_t)(ci & 1) * buf_bytes;
+    for (int gl = 0; gl < ng; ++gl) {
+      const uint32_t gofs = buf_off + (uint32_t)gl * gbytes;
+      if (a.leaf_out) {
+        for (int s = 0; s < STEPS; ++s) walk_step(std::true_type{}, gofs, g0 + gl, s);
+      } else {
+#pragma unroll 1
+        for (int s = 0; s < STEPS; ++s) walk_step(std::false_type{}, gofs, g0 + gl, s);
+      }
+    }
+    __syncthreads();  // every thread done with this buffer before it is refilled
+  }
+
+  float none[CT];
+#pragma unroll
+  for (int c = 0; c < CT; ++c) none[c] = 0.0f;
+#pragma unroll
+  for (int k = 0; k < RPT; ++k) {
+    if (rowk[k] >= a.n_rows) continue;
+    RowAcc<CT, false> r;
+#pragma unroll
+    for (int c = 0; c < CT; ++c) r.acc[c] = acc[k][c];
+    finish_row<CT, false>(a, rowk[k], r, none);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1214,6 +1399,32 @@ static KernelFn ranked_for(const cmlb_forest& f) {
   }
 }
 
+// Skew launch configurations: (threads, rows per thread, walks per step).
+constexpr RankedCfg SKEW_CFGS[] = {{512, 1, 4}, {256, 2, 4}, {256, 2, 2}, {1024, 1, 4}, {512, 1, 8}, {256, 2, 8}};
+constexpr int N_SKEW_CFGS = sizeof(SKEW_CFGS) / sizeof(SKEW_CFGS[0]);
+
+template <int CT>
+static KernelFn skew_cfg(int cfg) {
+  switch (cfg) {
+    case 0: return forest_skew_kernel<CT, 512, 1, 4>;
+    case 1: return forest_skew_kernel<CT, 256, 2, 4>;
+    case 2: return forest_skew_kernel<CT, 256, 2, 2>;
+    case 3: return forest_skew_kernel<CT, 1024, 1, 4>;
+    case 4: return forest_skew_kernel<CT, 512, 1, 8>;
+    case 5: return forest_skew_kernel<CT, 256, 2, 8>;
+    default: return nullptr;
+  }
+}
+
+static KernelFn skew_for(const cmlb_forest& f) {
+  switch (f.CT) {
+    case 1: return skew_cfg<1>(f.rcfg);
+    case 2: return skew_cfg<2>(f.rcfg);
+    case 4: return skew_cfg<4>(f.rcfg);
+    default: return nullptr;
+  }
+}
+
 static KernelFn mma_for(const cmlb_forest& f) {
   const bool pw = f.C == 1 && f.agg != CMLB_AGG_NONE;
   switch (f.CT) {
@@ -1227,6 +1438,7 @@ static KernelFn mma_for(const cmlb_forest& f) {
 
 static KernelFn kernel_for(const cmlb_forest& f) {
   if (f.variant == CMLB_FOREST_RANKED) return ranked_for(f);
+  if (f.variant == CMLB_FOREST_SKEW) return skew_for(f);
   if (f.variant == CMLB_FOREST_MMA) return mma_for(f);
   const bool perfect = f.variant == CMLB_FOREST_PERFECT;
   const bool pw = f.C == 1 && f.agg != CMLB_AGG_NONE;
@@ -1400,6 +1612,35 @@ static void fill_mma(const cmlb_forest_desc* d, int t, int K, int N, int CT, int
     for (int c = 0; c < d->n_outputs; ++c) pay[n * CT + c] = d->payload[(lb + n) * d->n_outputs + c];
 }
 
+// True when the float64 sums over trees are exact in ANY order: every payload
+// value is an integer multiple of 2^-q and the sum over trees of each tree's
+// largest |payload| is below 2^(53-q), so every partial sum (any subset of
+// trees, any order) is an integer multiple of 2^-q smaller than 2^53 units --
+// representable exactly, never rounded.  Then numpy's sequential (C >= 2) and
+// pairwise (C == 1) float64 reductions both equal the exact sum, and so does
+// any other order: the condition for the SKEW variant's rotated tree order.
+static bool sums_order_free(const cmlb_forest_desc* d) {
+  int q = -2000;
+  double bound = 0.0;
+  for (int t = 0; t < d->n_trees; ++t) {
+    double mx = 0.0;
+    for (int64_t l = d->leaf_offset[t]; l < d->leaf_offset[t + 1]; ++l)
+      for (int c = 0; c < d->n_outputs; ++c) {
+        const float v = d->payload[l * d->n_outputs + c];
+        if (!std::isfinite(v)) return false;
+        if (v == 0.0f) continue;
+        int e = 0;
+        std::frexp(v, &e);  // |v| = m * 2^e, m in [0.5, 1)
+        const int qv = std::fabs(v) >= std::numeric_limits<float>::min() ? 24 - e : 149;
+        q = std::max(q, qv);
+        mx = std::max(mx, (double)std::fabs(v));
+      }
+    bound += mx;
+  }
+  if (bound == 0.0) return true;
+  return std::ldexp(bound * (1.0 + 1e-12), q) < 9007199254740992.0;  // 2^53
+}
+
 static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out) {
   if (int s = validate(d)) return s;
   std::unique_ptr<cmlb_forest> f(new cmlb_forest());
@@ -1531,19 +1772,59 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
     ranked_ok = ranked_ok && found;
   }
 
+  // skew plan: as ranked, but 32-tree groups interleaved across the banks;
+  // needs the order-free certificate and a whole group per TMA buffer
+  bool skew_ok = ranked_ok && f->CT <= 4 && sums_order_free(d);
+  int s_cfg = 0, s_ntt = 0, s_rpt = 0, s_groups = 0, s_gbytes = 0, s_node_off = 0, s_stage = 0, s_stage_off = 0,
+      s_stage_bufs = 2;
+  size_t s_smem = 0;
+  if (skew_ok) {
+    const int ni_r = (1 << D) - 1, ns_r = 1 << D;
+    s_node_off = ns_r * 32 * f->CT * 4;
+    s_gbytes = s_node_off + ni_r * 32 * 4;
+    size_t max_nf = 0;
+    for (auto& u : U) max_nf = std::max(max_nf, u.size());
+    std::vector<int> order = {0, 1, 4, 5, 2, 3};
+    if (const char* env = getenv("CMLB_SKEW_CFG")) order = {atoi(env)};
+    bool found = false;
+    for (size_t oi = 0; oi < order.size() && !found; ++oi) {
+      const int ci = order[oi];
+      if (ci < 0 || ci >= N_SKEW_CFGS) continue;
+      const int rows = SKEW_CFGS[ci].ntt * SKEW_CFGS[ci].rpt;
+      if ((size_t)f->F * rows / 2 > 65535) continue;
+      const size_t cap = (max_nf + 7) / 8 * 8;
+      const size_t xr = ((size_t)f->F * rows * 2 + 15) / 16 * 16;
+      if (xr + cap * 6 > SMEM_LIMIT || xr + 2 * (size_t)s_gbytes > SMEM_LIMIT) continue;
+      const int G = (f->T + 31) / 32;
+      const int groups = std::min<int>((int)((SMEM_LIMIT - xr) / (2 * (size_t)s_gbytes)), G);
+      const size_t buf = (size_t)groups * s_gbytes;
+      const int nbufs = xr + std::max(2 * buf, 2 * cap * 6) <= SMEM_LIMIT ? 2 : 1;
+      const size_t stage_bytes = (size_t)nbufs * cap * 6;
+      if (xr + std::max(2 * buf, stage_bytes) > SMEM_LIMIT) continue;
+      s_cfg = ci; s_ntt = SKEW_CFGS[ci].ntt; s_rpt = SKEW_CFGS[ci].rpt; s_groups = groups;
+      s_stage = (int)cap; s_stage_bufs = nbufs; s_stage_off = stage_bytes <= buf ? (int)buf : 0;
+      s_smem = xr + std::max(2 * buf, stage_bytes);
+      found = true;
+    }
+    skew_ok = found;
+  }
+
   f->rpt = saved_rpt;
   // AUTO: measured on B200 (tools/variant_table.py -> profiles/r1_variant_table.json):
   // ranked wins from ~64 trees up (its per-row ranking pass amortizes over the
   // trees), the f32 perfect layout below that, general for deep trees; the
   // tcgen05 path-matrix form never wins (>= 10x slower at every shape).
   if (want == CMLB_FOREST_AUTO) {
-    if (ranked_ok && (f->T >= 64 || !perfect_ok)) want = CMLB_FOREST_RANKED;
+    if (skew_ok && f->T >= 64) want = CMLB_FOREST_SKEW;
+    else if (ranked_ok && (f->T >= 64 || !perfect_ok)) want = CMLB_FOREST_RANKED;
     else want = perfect_ok ? CMLB_FOREST_PERFECT : CMLB_FOREST_GENERAL;
   }
   if (want == CMLB_FOREST_PERFECT && !perfect_ok)
     return fail(CMLB_E_UNRESOLVED, "perfect layout does not fit (depth/outputs/features)");
   if (want == CMLB_FOREST_RANKED && !ranked_ok)
     return fail(CMLB_E_UNRESOLVED, "ranked layout does not fit (depth/outputs/thresholds)");
+  if (want == CMLB_FOREST_SKEW && !skew_ok)
+    return fail(CMLB_E_UNRESOLVED, "skew layout needs order-free (certified exact) sums and a fitting group");
   f->variant = want;
 
   if (f->variant == CMLB_FOREST_MMA) {
@@ -1580,6 +1861,10 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
     for (int t = 0; t < f->T; ++t)
       fill_ranked(d, t, D, f->CT, f->node_off_bytes, f->ntt * f->rpt, U, blob.data() + (size_t)t * f->tree_bytes,
                   slot_leaf.data() + (size_t)t * f->ns);
+    if (int st = upload(&f->blob, blob.data(), blob.size())) return st;
+    if (int st = upload(&f->slot_leaf, slot_leaf.data(), slot_leaf.size())) return st;
+  }
+  if (f->variant == CMLB_FOREST_RANKED || f->variant == CMLB_FOREST_SKEW) {
     // per feature: Eytzinger order of the sorted unique thresholds + the map
     // from Eytzinger position back to sorted index
     std::vector<float> uthr;
@@ -1614,8 +1899,6 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
       while (umap.size() % 8) umap.push_back(0);
     }
     moff[f->F] = (int32_t)umap.size();
-    if (int st = upload(&f->blob, blob.data(), blob.size())) return st;
-    if (int st = upload(&f->slot_leaf, slot_leaf.data(), slot_leaf.size())) return st;
     if (int st = upload(&f->uthr, uthr.data(), uthr.size())) return st;
     if (int st = upload(&f->uoff, uoff.data(), uoff.size())) return st;
     if (int st = upload(&f->umap, umap.data(), umap.size())) return st;
@@ -1623,7 +1906,39 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
     if (int st = upload(&f->unf, unf.data(), unf.size())) return st;
   }
 
-  if (f->variant == CMLB_FOREST_RANKED || f->variant == CMLB_FOREST_MMA) {
+  if (f->variant == CMLB_FOREST_SKEW) {
+    f->rcfg = s_cfg; f->ntt = s_ntt; f->rpt = s_rpt; f->chunk_trees = s_groups; f->tree_bytes = s_gbytes;
+    f->node_off_bytes = s_node_off; f->stage_cap = s_stage; f->smem = s_smem; f->stage_off = s_stage_off;
+    f->stage_bufs = s_stage_bufs;
+    f->ni = (1 << D) - 1; f->ns = 1 << D;
+    const int rows = s_ntt * s_rpt, G = (f->T + 31) / 32;
+    const int t_node_off = f->ns * f->CT * 4;
+    const int t_bytes = (int)(((size_t)t_node_off + (size_t)f->ni * 4 + 15) / 16 * 16);
+    std::vector<uint8_t> blob((size_t)G * s_gbytes, 0), one((size_t)t_bytes);
+    std::vector<int32_t> slot_leaf((size_t)f->T * f->ns, 0);
+    for (int g = 0; g < G; ++g) {
+      float* gp = reinterpret_cast<float*>(blob.data() + (size_t)g * s_gbytes);
+      uint32_t* gn = reinterpret_cast<uint32_t*>(blob.data() + (size_t)g * s_gbytes + s_node_off);
+      for (int t = 0; t < 32; ++t) {
+        const int tt = g * 32 + t;
+        if (tt >= f->T) {  // padding: always left (rank 16383 is never exceeded) onto a zero payload
+          for (int j = 0; j < f->ni; ++j) gn[j * 32 + t] = 0x3FFFu;
+          continue;
+        }
+        std::fill(one.begin(), one.end(), 0);
+        fill_ranked(d, tt, D, f->CT, t_node_off, rows, U, one.data(), slot_leaf.data() + (size_t)tt * f->ns);
+        const float* tp = reinterpret_cast<const float*>(one.data());
+        const uint32_t* tn = reinterpret_cast<const uint32_t*>(one.data() + t_node_off);
+        for (int sl = 0; sl < f->ns; ++sl)
+          for (int c = 0; c < f->CT; ++c) gp[((size_t)sl * 32 + t) * f->CT + c] = tp[sl * f->CT + c];
+        for (int j = 0; j < f->ni; ++j) gn[j * 32 + t] = tn[j];
+      }
+    }
+    if (int st = upload(&f->blob, blob.data(), blob.size())) return st;
+    if (int st = upload(&f->slot_leaf, slot_leaf.data(), slot_leaf.size())) return st;
+  }
+
+  if (f->variant == CMLB_FOREST_RANKED || f->variant == CMLB_FOREST_MMA || f->variant == CMLB_FOREST_SKEW) {
     // built above
   } else if (f->variant == CMLB_FOREST_PERFECT) {
     std::vector<uint8_t> blob((size_t)f->T * f->tree_bytes, 0);
@@ -1675,7 +1990,8 @@ static int run_forest(const cmlb_forest* f, const float* x, int64_t n_rows, int6
     return pe ? atoi(pe) : 0;
   }();
   a.probe = mma_probe;
-  const int threads = f->variant == CMLB_FOREST_RANKED ? f->ntt : (f->variant == CMLB_FOREST_MMA ? MMA2_THREADS : NT);
+  const bool rk = f->variant == CMLB_FOREST_RANKED || f->variant == CMLB_FOREST_SKEW;
+  const int threads = rk ? f->ntt : (f->variant == CMLB_FOREST_MMA ? MMA2_THREADS : NT);
   const int64_t rows = f->variant == CMLB_FOREST_MMA ? (int64_t)MMA_M : (int64_t)threads * f->rpt;
   const int64_t grid = ceil_div(n_rows, rows);
   if (grid > 0x7fffffff) return fail(CMLB_E_INPUT, "too many rows for one launch");
@@ -1761,13 +2077,19 @@ int cmlb_forest_info(const cmlb_forest* f, int32_t* variant, int32_t* depth, int
   if (depth) *depth = f->depth;
   if (chunk_trees) *chunk_trees = f->chunk_trees;
   if (rows_per_cta)
-    *rows_per_cta = (f->variant == CMLB_FOREST_RANKED ? f->ntt : (f->variant == CMLB_FOREST_MMA ? cmlb::MMA_M : cmlb::NT)) * f->rpt;
+    *rows_per_cta = (f->variant == CMLB_FOREST_RANKED || f->variant == CMLB_FOREST_SKEW
+                         ? f->ntt : (f->variant == CMLB_FOREST_MMA ? cmlb::MMA_M : cmlb::NT)) * f->rpt;
   return CMLB_OK;
 }
 
 void cmlb_forest_destroy(cmlb_forest* f) { delete f; }
 
 // Host-only helper exported for tests: the pairwise schedule codes.
+int cmlb_debug_sums_order_free(const cmlb_forest_desc* desc) {
+  if (!desc || desc->n_trees < 1 || desc->n_outputs < 1 || !desc->leaf_offset || !desc->payload) return -1;
+  return cmlb::sums_order_free(desc) ? 1 : 0;
+}
+
 int cmlb_debug_pairwise_schedule(int64_t n, uint32_t* codes) {
   std::vector<uint32_t> v;
   int depth = cmlb::build_schedule(n, v);

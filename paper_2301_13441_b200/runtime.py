@@ -63,58 +63,65 @@ def compact_features(spec: ForestSpec, feature: np.ndarray):
     return int(used.size), np.ascontiguousarray(base[used]), n_in
 
 
+def forest_desc(spec: ForestSpec, variant: int = N.FOREST_AUTO):
+    """cmlb_forest_desc for a lowered forest; returns (desc, buffers to keep
+    alive until the C call that reads it returns)."""
+    trees = spec.trees
+    T = len(trees)
+    node_off = np.zeros(T + 1, np.int64)
+    leaf_off = np.zeros(T + 1, np.int64)
+    for i, t in enumerate(trees):
+        node_off[i + 1] = node_off[i] + t.n_internal
+        leaf_off[i + 1] = leaf_off[i] + t.n_leaves
+    cat = lambda xs, dt: np.ascontiguousarray(np.concatenate(xs).astype(dt)) if xs else np.zeros(0, dt)
+    feature = cat([t.feature for t in trees], np.int32)
+    threshold = cat([t.threshold for t in trees], np.float32)
+    left = cat([t.left for t in trees], np.int32)
+    right = cat([t.right for t in trees], np.int32)
+    payload = np.ascontiguousarray(np.concatenate([t.payload for t in trees]).astype(np.float32))
+    classes = np.ascontiguousarray(np.asarray(spec.classes, np.float64))
+    n_features, prologue, n_inputs = compact_features(spec, feature)
+    if prologue is not spec.prologue:
+        feature = np.ascontiguousarray(np.searchsorted(np.unique(feature), feature).astype(np.int32))
+    keep = [node_off, leaf_off, feature, threshold, left, right, payload, classes]
+    d = N.ForestDesc()
+    d.n_trees, d.n_features, d.n_outputs = T, n_features, spec.n_outputs
+    d.node_offset = N.ptr(node_off, N.c_i64)
+    d.leaf_offset = N.ptr(leaf_off, N.c_i64)
+    d.feature = N.ptr(feature, N.c_i32)
+    d.threshold = N.ptr(threshold, N.c_f32)
+    d.left = N.ptr(left, N.c_i32)
+    d.right = N.ptr(right, N.c_i32)
+    d.payload = N.ptr(payload, N.c_f32)
+    d.aggregation, d.tail = spec.aggregation, spec.tail
+    d.learning_rate, d.base_score = spec.learning_rate, spec.base_score
+    d.classes = N.ptr(classes, N.c_f64)
+    d.n_classes = len(spec.classes)
+    d.out_dtype = OUT_CODE[spec.out_dtype]
+    d.dense_selector = int(spec.dense_selector)
+    d.variant = variant
+    d.n_trees_total = int(spec.n_trees_total)
+    if prologue is not None:
+        pro = np.ascontiguousarray(prologue)
+        keep.append(pro)
+        d.prologue, d.n_inputs = pro.ctypes.data, int(n_inputs)
+    return d, keep
+
+
 class _Forest:
     def __init__(self, spec: ForestSpec, device: int, variant: int = N.FOREST_AUTO):
         self.spec = spec
-        trees = spec.trees
-        T = len(trees)
-        node_off = np.zeros(T + 1, np.int64)
-        leaf_off = np.zeros(T + 1, np.int64)
-        for i, t in enumerate(trees):
-            node_off[i + 1] = node_off[i] + t.n_internal
-            leaf_off[i + 1] = leaf_off[i] + t.n_leaves
-        cat = lambda xs, dt: np.ascontiguousarray(np.concatenate(xs).astype(dt)) if xs else np.zeros(0, dt)
-        feature = cat([t.feature for t in trees], np.int32)
-        threshold = cat([t.threshold for t in trees], np.float32)
-        left = cat([t.left for t in trees], np.int32)
-        right = cat([t.right for t in trees], np.int32)
-        payload = np.ascontiguousarray(np.concatenate([t.payload for t in trees]).astype(np.float32))
-        classes = np.ascontiguousarray(np.asarray(spec.classes, np.float64))
-        n_features, prologue, n_inputs = compact_features(spec, feature)
-        if prologue is not spec.prologue:
-            feature = np.ascontiguousarray(np.searchsorted(np.unique(feature), feature).astype(np.int32))
-        keep = (node_off, leaf_off, feature, threshold, left, right, payload, classes)
-        d = N.ForestDesc()
-        d.n_trees, d.n_features, d.n_outputs = T, n_features, spec.n_outputs
-        d.node_offset = N.ptr(node_off, N.c_i64)
-        d.leaf_offset = N.ptr(leaf_off, N.c_i64)
-        d.feature = N.ptr(feature, N.c_i32)
-        d.threshold = N.ptr(threshold, N.c_f32)
-        d.left = N.ptr(left, N.c_i32)
-        d.right = N.ptr(right, N.c_i32)
-        d.payload = N.ptr(payload, N.c_f32)
-        d.aggregation, d.tail = spec.aggregation, spec.tail
-        d.learning_rate, d.base_score = spec.learning_rate, spec.base_score
-        d.classes = N.ptr(classes, N.c_f64)
-        d.n_classes = len(spec.classes)
-        d.out_dtype = OUT_CODE[spec.out_dtype]
-        d.dense_selector = int(spec.dense_selector)
-        d.variant = variant
-        d.n_trees_total = int(spec.n_trees_total)
-        pro = None
-        if prologue is not None:
-            pro = np.ascontiguousarray(prologue)
-            d.prologue, d.n_inputs = pro.ctypes.data, int(n_inputs)
+        d, keep = forest_desc(spec, variant)
         h = N.c_vp()
         N.check(N.lib().cmlb_forest_create(C.byref(d), device, C.byref(h)))
-        del keep, pro
+        del keep
         self.handle = h
-        self.n_trees = T
+        self.n_trees = len(spec.trees)
 
     def info(self) -> dict:
         v, dep, ch, rows = (N.c_i32() for _ in range(4))
         N.check(N.lib().cmlb_forest_info(self.handle, C.byref(v), C.byref(dep), C.byref(ch), C.byref(rows)))
-        return {"variant": {1: "perfect", 2: "general", 3: "ranked", 4: "mma"}[v.value], "depth": dep.value,
+        return {"variant": {1: "perfect", 2: "general", 3: "ranked", 4: "mma", 5: "skew"}[v.value], "depth": dep.value,
                 "chunk_trees": ch.value, "rows_per_cta": rows.value}
 
     def run(self, x, y, n, ldx, stream, leaf_out=None):

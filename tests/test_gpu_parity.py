@@ -45,20 +45,21 @@ def test_execute_reference_plan(name):
     assert _same(got.astype(np.float64), case.want)
 
 
-@pytest.mark.parametrize("variant", [N.FOREST_PERFECT, N.FOREST_GENERAL, N.FOREST_RANKED, N.FOREST_MMA])
+@pytest.mark.parametrize("variant", [N.FOREST_PERFECT, N.FOREST_GENERAL, N.FOREST_RANKED, N.FOREST_MMA,
+                                     N.FOREST_SKEW])
 @pytest.mark.parametrize("name", [n for n in gc.case_names() if gc.get(n).leaves is not None])
 def test_leaf_indices_and_variants(name, variant):
     case = gc.get(name)
     spec = lower.lower_model(case.model, case.profile, case.passes)
     st = spec.stages[0]
-    if variant in (N.FOREST_PERFECT, N.FOREST_RANKED, N.FOREST_MMA) and (max(t.depth() for t in st.trees) > 11
-                                                                          or max(t.depth() for t in st.trees) == 0):
+    layouts = (N.FOREST_PERFECT, N.FOREST_RANKED, N.FOREST_MMA, N.FOREST_SKEW)
+    if variant in layouts and (max(t.depth() for t in st.trees) > 11 or max(t.depth() for t in st.trees) == 0):
         pytest.skip("too deep / no internal node for the perfect layout")
     try:
         prog = DeviceProgram(spec, 0, forest_variant=variant)
     except UnresolvedKernel:
-        assert variant in (N.FOREST_PERFECT, N.FOREST_RANKED, N.FOREST_MMA)
-        pytest.skip("perfect/ranked/mma layout does not fit this forest")
+        assert variant in layouts
+        pytest.skip("perfect/ranked/mma/skew layout does not fit this forest (or its sums are not order-free)")
     x = torch.from_numpy(case.x).cuda()
     leaves = torch.full((x.shape[0], len(st.trees)), -7, dtype=torch.int32, device="cuda")
     y = prog.run(x, leaf_out=leaves)
@@ -251,3 +252,42 @@ def test_tree_sharded_gbr_is_bit_exact(world):
     single = full.run(xd)
     assert torch.equal(y, single)
     assert _same(y.cpu().numpy().astype(np.float64), want)
+
+
+@pytest.mark.parametrize("cfg", range(6))
+def test_skew_launch_configs(cfg, monkeypatch):
+    """Every SKEW launch configuration (CMLB_SKEW_CFG) is bit-exact, leaves
+    included, on certified (order-free) forests of 1, 2 and 3 outputs, with
+    ragged last groups (T not a multiple of 32) and NaN rows."""
+    monkeypatch.setenv("CMLB_SKEW_CFG", str(cfg))
+    from paper_2301_13441_b200.models import ForestModel
+    rng = np.random.default_rng(300 + cfg)
+    rf2 = _synthetic_forest(rng, 77, 8, 28, 2)
+    rf3 = _synthetic_forest(rng, 40, 6, 12, 3)
+    g = _synthetic_forest(rng, 70, 7, 20, 1, True)
+    reg = ForestModel("random_forest_regressor", 20, g.trees, "mean_probability", 1.0, 0.0, None)
+    ran = 0
+    for m, F in ((rf2, 28), (rf3, 12), (reg, 20)):
+        x = rng.standard_normal((30_000, F)).astype(np.float32)
+        x[::101, 2] = np.nan
+        x[::103, 1] = np.inf
+        want, want_leaves = fast.forest_predict(fast.PackedForest(m), x, want_leaves=True)
+        try:
+            prog = DeviceProgram(lower.lower_model(m), 0, forest_variant=N.FOREST_SKEW)
+        except UnresolvedKernel:
+            continue  # not certified order-free, or the configuration does not fit
+        ran += 1
+        leaves = torch.empty((x.shape[0], len(m.trees)), dtype=torch.int32, device="cuda")
+        y = prog.run(torch.from_numpy(x).cuda(), leaf_out=leaves).cpu().numpy().astype(np.float64)
+        np.testing.assert_array_equal(leaves.cpu().numpy(), want_leaves)
+        assert _same(y, want), (cfg, prog.forest().info())
+        y2 = prog.run(torch.from_numpy(x).cuda()).cpu().numpy().astype(np.float64)
+        assert _same(y2, want)
+        prog.close()
+    assert ran >= 2
+
+
+def test_auto_picks_skew_for_certified_large_forests():
+    import bench
+    model, _, _ = bench.load_model()
+    assert api.compile_model(model).program(0).forest().info()["variant"] == "skew"
