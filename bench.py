@@ -1,20 +1,37 @@
-"""North-star benchmark: RandomForestClassifier 500 x depth-8 on 10M x 28 fp32 rows per GPU.
+"""Benchmarks of the BASELINE configs; the default is the north star.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--rows R]
+    python bench.py [--config rf500|dt6|gbr1000|lr784|svc10k|pipe5] [--gpus N] [--steps K]
+                    [--warmup W] [--impl ours|reference] [--rows R] [--variant ...]
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N
 
-One step = one pass of the fused forest kernel (tree operator representation
-+ ensemble tail, ``libcmlb.so``) over this rank's 10M-row shard, inputs
-resident in HBM (1.12 GB per step, larger than the 126 MB L2, so no flush is
-needed).  Ranks shard rows with no data-path collective (weak scaling);
-``value`` = rows of all ranks / max-over-ranks device time.  ``e2e`` is the
-same metric through the public API from pinned host memory, with the H2D copy
-of X and the D2H copy of the class labels inside the timed region.
+Default (``--config rf500``): RandomForestClassifier 500 x depth-8 on 10M x 28
+fp32 rows per GPU (BASELINE.json's metric and config 2).  One step = one pass
+of the fused forest kernel (tree operator representation + ensemble tail,
+``libcmlb.so``) over this rank's shard, inputs resident in HBM (1.12 GB per
+step, larger than the 126 MB L2, so no flush is needed).  Ranks shard rows with
+no data-path collective (weak scaling); ``value`` = rows of all ranks /
+max-over-ranks device time.  ``--gpus N`` without a launcher starts the N
+ranks itself.  ``e2e`` is the same metric through the public API from pinned
+host memory, with the H2D copy of X and the D2H copy of the outputs inside the
+timed region.  The other configs print the
+same line for their own workload.
 
-``--impl reference`` times the CPU restatement of the reference path
-(``oracle/liboracle.so``, all host threads) on a bounded row sample per step;
-the reference itself (``mlower``, pure Python, 25.8 rows/s measured in
-SURVEY 6) is not on the GPU box.
+``roofline`` is the dominant kernel against the resource that bounds it:
+  * forest walks (rf500, dt6, gbr1000, pipe5): shared-memory load wavefronts.
+    ``achieved`` = ALGORITHMIC wavefronts per row (every node, rank and payload
+    load of the walk and the ranking search at one wavefront per warp-wide
+    conflict-free access) x the live rows/s; ``peak`` = the
+    measured conflict-free wavefront rate (profiles/peaks_smem.json) x SMs x
+    the sampled SM clock.  ``traffic`` = ncu-measured wavefronts per launch
+    when a committed profile of the same kernel exists (conflict replays show
+    up as traffic above the algorithmic count).  HBM and the reference's
+    GEMM-equivalent int8 work are reported beside it (``hbm``, ``gemm_equivalent``).
+  * lr784: HBM bytes (X read + labels written) against MEASURED_PEAKS.json.
+  * svc10k: TF32 tensor flops (2 F n_SV per row) against the measured TF32 peak.
+
+``--impl reference`` times the CPU restatement of the reference path (the
+oracle: ``oracle/liboracle.so`` / numpy; the reference itself is pure Python,
+25.8 rows/s on RF500) on a bounded row sample per step.
 """
 
 from __future__ import annotations
@@ -35,7 +52,6 @@ sys.path.insert(0, ROOT)
 
 ASSET = os.path.join(ROOT, "bench_assets", "rf500_d8.npz")
 METRIC = "samples/sec (RandomForest 500x d8, 10M x 28) at 1/2/4/8 B200; % roofline"
-BYTES_ROW = 28 * 4 + 1      # X row in, uint8 class out
 
 
 def load_model():
@@ -55,27 +71,33 @@ def gemm_equivalent_ops(model) -> int:
     return tot
 
 
+def _json(path):
+    p = os.path.join(ROOT, path)
+    if os.path.exists(p):
+        with open(p) as fh:
+            return json.load(fh)
+    return None
+
+
 def peaks():
-    out = {"hbm_gbs": None, "int8_tops": None, "source": {}}
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-            mp = json.load(fh)
+    out = {"source": {}}
+    mp = _json("MEASURED_PEAKS.json")
+    if mp:
         out["hbm_gbs"] = float(mp["hbm_gbs"])
         out["source"]["hbm"] = "MEASURED_PEAKS.json (measured copy)"
-        bf16 = float(mp["bf16_tflops"])
-    except Exception:
+    else:
         out["hbm_gbs"] = 6650.0
         out["source"]["hbm"] = "fallback 6.65 TB/s (B200_PROFILING.md)"
-        bf16 = 1590.0
-    p8 = os.path.join(ROOT, "profiles", "peaks_int8.json")
-    if os.path.exists(p8):
-        with open(p8) as fh:
-            d = json.load(fh)
-        out["int8_tops"] = float(d["int8_tops_burst"])
-        out["source"]["int8"] = "profiles/peaks_int8.json (measured torch._int_mm 8192^3)"
-    else:
-        out["int8_tops"] = 2.0 * bf16
-        out["source"]["int8"] = "proxy 2x measured bf16 (int8 not measured)"
+    p8 = _json("profiles/peaks_int8.json")
+    out["int8_tops"] = float(p8["int8_tops_burst"]) if p8 else 2.0 * float((mp or {}).get("bf16_tflops", 1590.0))
+    out["source"]["int8"] = "profiles/peaks_int8.json (measured torch._int_mm 8192^3)" if p8 else "proxy 2x bf16"
+    tf = _json("profiles/peaks_tf32.json")
+    out["tf32_tflops"] = float(tf["tf32_tflops_burst"]) if tf else 1100.0
+    out["source"]["tf32"] = "profiles/peaks_tf32.json (measured cuBLAS TF32)" if tf else "nominal 1.1 PF (guide)"
+    sm = _json("profiles/peaks_smem.json")
+    out["smem_wf_per_sm_clk"] = float(sm["wavefronts_per_sm_clk"]) if sm else 1.0
+    out["source"]["smem"] = ("profiles/peaks_smem.json (measured conflict-free LDS wavefronts per SM per clock)"
+                             if sm else "architectural 1 wavefront/clk/SM (not measured)")
     return out
 
 
@@ -135,28 +157,421 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_baseline(model, mu, sigma, target_s: float = 10.0):
-    """C oracle on this host's cores over a bounded sample of the workload."""
-    from oracle import fast
-    packed = fast.PackedForest(model)
-    threads = os.cpu_count() or 1
-    rng = np.random.default_rng(11)
-    cal = (rng.standard_normal((2000, 28)) * sigma + mu).astype(np.float32)
+# ---------------------------------------------------------------------------
+# workloads
+# ---------------------------------------------------------------------------
+
+
+def _class_width(c: int) -> int:
+    for w in (1, 2, 4, 8, 16):
+        if c <= w:
+            return w
+    return 32
+
+
+def forest_wavefronts_row(spec, info) -> dict:
+    """Algorithmic shared-memory wavefronts per row of the ranked/skew walk:
+    per tree D node-word loads + D rank loads + the payload load (CT floats,
+    CT wavefronts per warp of 32), per feature the Eytzinger search
+    (floor(log2 n_f) + 1 levels + the index-map load) and the rank store, all
+    at one wavefront per warp-wide conflict-free access, / 32 rows."""
+    if info["variant"] not in ("ranked", "skew"):
+        return None
+    D = int(info["depth"])
+    CT = _class_width(spec.n_outputs)
+    T = len(spec.trees)
+    T_walked = (T + 31) // 32 * 32 if info["variant"] == "skew" else T
+    feats = np.concatenate([t.feature for t in spec.trees]) if T else np.zeros(0, np.int64)
+    thr = np.concatenate([t.threshold for t in spec.trees]) if T else np.zeros(0, np.float32)
+    search = 0
+    for f in np.unique(feats):
+        nf = np.unique(thr[feats == f]).size
+        search += int(np.floor(np.log2(nf))) + 1 + 1 + 1
+    walk = T_walked * (2 * D + CT)
+    return {"walk": walk / 32.0, "rank": search / 32.0, "total": (walk + search) / 32.0,
+            "trees_walked": T_walked, "depth": D, "payload_floats": CT}
+
+
+class Workload:
+    name = ""
+    metric = ""
+    features = 0
+    default_rows = 0
+    out_bytes = 1
+
+    def model(self):
+        raise NotImplementedError
+
+    def device_input(self, dev, rank: int, n: int):
+        import torch
+        g = torch.Generator(device=dev)
+        g.manual_seed(self.seed + rank)
+        return torch.randn((n, self.features), generator=g, device=dev, dtype=torch.float32)
+
+    def config(self, n: int, world: int, info) -> dict:
+        return {"workload": self.describe(n), "rows_per_gpu": n, "features": self.features,
+                "parallelism": f"row-shard dp{world}",
+                "l2": f"inputs {n * self.features * 4 / 1e9:.2f} GB per step vs 126 MB L2"
+                      + (" (no flush needed)" if n * self.features * 4 > 126e6 else
+                         " (inputs re-read from L2 between steps)")}
+
+    def describe(self, n):
+        return self.name
+
+    def roofline(self, prog, spec, info, rows_per_s: float, kern_ms: float, n: int, pk, clocks, sms) -> dict:
+        return None
+
+    def parity(self, prog, x) -> dict:
+        return None
+
+    def cpu_baseline(self, x_sample: np.ndarray, threads: int):
+        """(callable on a host array, description)."""
+        raise NotImplementedError
+
+
+class ForestWorkload(Workload):
+    seed = 1
+    variant = "auto"
+
+    def describe(self, n):
+        return f"{self.title} on {n} x {self.features} fp32 rows per GPU"
+
+    def roofline(self, prog, spec, info, rows_per_s, kern_ms, n, pk, clocks, sms):
+        model = self.model()
+        bytes_row = self.features * 4 + self.out_bytes
+        hbm = rows_per_s * bytes_row / 1e9
+        ops_row = gemm_equivalent_ops(model) if hasattr(model, "trees") else None
+        wf = forest_wavefronts_row(spec, info)
+        mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965.0
+        out = {"kernel_ms": kern_ms}
+        if wf is not None:
+            peak = pk["smem_wf_per_sm_clk"] * sms * mhz * 1e6 / 1e9
+            ach = rows_per_s * wf["total"] / 1e9
+            traffic = None
+            prof = _json(f"profiles/wavefronts_{self.name}_{info['variant']}.json")
+            if prof:
+                traffic = float(prof["wavefronts_per_row"]) * n
+            out.update({"bound": "smem", "achieved": ach, "peak": peak, "unit": "Gwavefronts/s",
+                        "frac": ach / peak, "traffic": traffic,
+                        "traffic_unit": "shared-memory load wavefronts per launch (ncu, committed profile)",
+                        "basis": f"algorithmic wavefronts per row = {wf['total']:.1f} ({info['variant']} walk "
+                                 f"{wf['walk']:.1f} over {wf['trees_walked']} trees x depth {wf['depth']} + ranking "
+                                 f"{wf['rank']:.1f}) x live rows/s; peak = measured rate x {sms} SMs x "
+                                 f"{mhz:.0f} MHz sampled", "peak_source": pk["source"]["smem"],
+                        "wavefronts_row": wf})
+        else:
+            out.update({"bound": "hbm", "achieved": hbm, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                        "frac": hbm / pk["hbm_gbs"], "traffic": None})
+        out["hbm"] = {"achieved": hbm, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": hbm / pk["hbm_gbs"],
+                      "bytes_row": bytes_row, "peak_source": pk["source"]["hbm"]}
+        if ops_row:
+            tops = rows_per_s * ops_row / 1e12
+            out["gemm_equivalent"] = {
+                "achieved": tops, "peak": pk["int8_tops"], "unit": "TOPS", "ratio": tops / pk["int8_tops"],
+                "ops_row": ops_row, "peak_source": pk["source"]["int8"],
+                "note": "informational: the reference's GEMM-form int8 work (sum_t 2 I_t L_t) the walk avoids; "
+                        "a ratio above 1 means the walk does less work than the GEMM, not a roofline fraction"}
+        return out
+
+    def parity(self, prog, x):
+        from oracle import fast  # checker only, outside the timed region
+        model = self.model()
+        k = min(int(x.shape[0]), 20_000)
+        xs = x[:k]
+        got = prog.run(xs).cpu().numpy().astype(np.float64)
+        want, _ = fast.forest_predict(fast.PackedForest(model), xs.cpu().numpy())
+        return {"rows": k, "bit_exact": bool(np.array_equal(got, want)), "oracle": "oracle/liboracle.so"}
+
+    def cpu_baseline(self, x_sample, threads):
+        from oracle import fast
+        packed = fast.PackedForest(self.model())
+        return (lambda xs: fast.forest_predict(packed, xs, threads=threads)), "oracle/liboracle.so (C restatement)"
+
+
+class RF500(ForestWorkload):
+    name = "rf500"
+    metric = METRIC
+    features = 28
+    default_rows = 10_000_000
+    title = "RandomForestClassifier 500 trees depth 8"
+
+    def __init__(self):
+        self._m = None
+
+    def model(self):
+        if self._m is None:
+            self._m, self.mu, self.sigma = load_model()
+        return self._m
+
+    def device_input(self, dev, rank, n):
+        import torch
+        self.model()
+        x = super().device_input(dev, rank, n)
+        return x.mul_(torch.from_numpy(self.sigma).to(dev)).add_(torch.from_numpy(self.mu).to(dev))
+
+    def config(self, n, world, info):
+        c = super().config(n, world, info)
+        c.update({"forest_source": "sklearn RF500 max_depth=8 fit on make_classification(200k x 28), "
+                                   "bench_assets/rf500_d8.npz", "trees": 500})
+        return c
+
+
+class DT6(ForestWorkload):
+    name = "dt6"
+    metric = "samples/sec (DecisionTreeClassifier depth 6, 100k x 28)"
+    features = 28
+    default_rows = 100_000
+    title = "DecisionTreeClassifier depth 6 (sklearn, make_classification 100k x 28)"
+    seed = 11
+
+    def model(self):
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import golden_cases as gc
+        return gc.get("sk_dt_d6").model
+
+    def device_input(self, dev, rank, n):
+        return super().device_input(dev, rank, n).mul_(2.0)
+
+    def parity(self, prog, x):
+        from oracle import semantics as sem  # single trees: the numpy restatement
+        k = min(int(x.shape[0]), 20_000)
+        got = prog.run(x[:k]).cpu().numpy().astype(np.float64)
+        want, _ = sem.predict(self.model(), x[:k].cpu().numpy())
+        return {"rows": k, "bit_exact": bool(np.array_equal(got, want)), "oracle": "oracle/semantics.py"}
+
+    def cpu_baseline(self, x_sample, threads):
+        from oracle import semantics as sem
+        m = self.model()
+        return (lambda xs: sem.predict(m, xs)), "oracle/semantics.py (numpy restatement of execute, 1 thread)"
+
+
+class GBR1000(ForestWorkload):
+    name = "gbr1000"
+    metric = "samples/sec (GradientBoostingRegressor 1000x d10, 1M x 90)"
+    features = 90
+    default_rows = 1_000_000
+    out_bytes = 4
+    title = "GradientBoostingRegressor 1000 perfect depth-10 trees (SURVEY 8d throughput model)"
+    seed = 2
+
+    def __init__(self):
+        self._m = None
+
+    def model(self):
+        if self._m is None:
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            from bench_configs import perfect_gbdt
+            self._m = perfect_gbdt()
+        return self._m
+
+
+class Pipe5(ForestWorkload):
+    name = "pipe5"
+    metric = "samples/sec (StandardScaler + OneHotEncoder + RandomForest 500x d8, 5M x 64)"
+    features = 64
+    default_rows = 5_000_000
+    title = "ColumnTransformer(StandardScaler 56 + OneHotEncoder 8 x 16) -> RF500 d8, fused"
+
+    def __init__(self):
+        self._m = None
+
+    def _build(self, n):
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from workloads import config5_pipeline
+        self._m, self._x = config5_pipeline(rows=n)
+
+    def model(self):
+        if self._m is None:
+            self._build(16)
+        return self._m
+
+    def device_input(self, dev, rank, n):
+        import torch
+        self._build(n)
+        return torch.from_numpy(self._x).to(dev)
+
+    def parity(self, prog, x):
+        from oracle import ext_semantics as ext
+        k = min(int(x.shape[0]), 5000)
+        got = prog.run(x[:k]).cpu().numpy().astype(np.float64)
+        want, _ = ext.predict(self.model(), x[:k].cpu().numpy())
+        return {"rows": k, "bit_exact": bool(np.array_equal(got, want)),
+                "oracle": "reference scaler semantics + scikit-learn one-hot + C forest oracle"}
+
+    def cpu_baseline(self, x_sample, threads):
+        from oracle import ext_semantics as ext, fast
+        ct, forest = self.model().steps
+        packed = fast.PackedForest(forest)
+        return (lambda xs: fast.forest_predict(packed, ext.transform(ct, xs), threads=threads)), \
+            "numpy column transform + oracle/liboracle.so forest"
+
+    def roofline(self, prog, spec, info, rows_per_s, kern_ms, n, pk, clocks, sms):
+        return super().roofline(prog, spec, info, rows_per_s, kern_ms, n, pk, clocks, sms)
+
+
+class LR784(Workload):
+    name = "lr784"
+    metric = "samples/sec (LogisticRegression 784->10, 1M x 784)"
+    features = 784
+    default_rows = 1_000_000
+    seed = 3
+
+    def __init__(self):
+        self._m = None
+
+    def describe(self, n):
+        return f"LogisticRegression 784 -> 10 classes on {n} x 784 fp32 rows per GPU"
+
+    def model(self):
+        if self._m is None:
+            from paper_2301_13441_b200.models import LinearModel
+            rng = np.random.default_rng(3)
+            self._m = LinearModel(
+                "logistic_regression", 784,
+                tuple(tuple(float(v) for v in r) for r in rng.standard_normal((10, 784)).astype(np.float32) * 0.05),
+                tuple(float(v) for v in rng.standard_normal(10).astype(np.float32)), tuple(float(c) for c in range(10)))
+        return self._m
+
+    def roofline(self, prog, spec, info, rows_per_s, kern_ms, n, pk, clocks, sms):
+        bytes_row = 784 * 4 + 1
+        gbs = rows_per_s * bytes_row / 1e9
+        return {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": gbs / pk["hbm_gbs"],
+                "traffic": None, "basis": f"algorithmic bytes per row {bytes_row} (X row read + int8 label)",
+                "peak_source": pk["source"]["hbm"], "kernel_ms": kern_ms}
+
+    def parity(self, prog, x):
+        from oracle import semantics as sem
+        k = min(int(x.shape[0]), 4000)
+        got = prog.run(x[:k]).cpu().numpy().astype(np.float64)
+        want, _ = sem.predict(self.model(), x[:k].cpu().numpy())
+        return {"rows": k, "bit_exact": bool(np.array_equal(got, want)), "oracle": "oracle/semantics.py (numpy)"}
+
+    def cpu_baseline(self, x_sample, threads):
+        from oracle import semantics as sem
+        m = self.model()
+        return (lambda xs: sem.predict(m, xs)), "oracle/semantics.py (numpy float64 ascending-k, 1 thread)"
+
+
+class SVC10k(Workload):
+    name = "svc10k"
+    metric = "samples/sec (SVC RBF 10k SVs, 1M x 784)"
+    features = 784
+    default_rows = 1_000_000
+    seed = 3
+
+    def __init__(self):
+        self._m = None
+
+    def describe(self, n):
+        return f"SVC RBF, {self.model().n_sv} support vectors, 10 classes, on {n} x 784 fp32 rows per GPU"
+
+    def model(self):
+        if self._m is None:
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            from bench_configs import svc_model
+            self._m = svc_model()
+        return self._m
+
+    def device_input(self, dev, rank, n):
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        from bench_configs import svc_inputs
+        return svc_inputs(dev, rank, n)
+
+    def roofline(self, prog, spec, info, rows_per_s, kern_ms, n, pk, clocks, sms):
+        m = self.model()
+        flops_row = 2.0 * m.n_features * m.n_sv
+        tf = rows_per_s * flops_row / 1e12
+        return {"bound": "tensor", "achieved": tf, "peak": pk["tf32_tflops"], "unit": "TFLOP/s",
+                "frac": tf / pk["tf32_tflops"], "traffic": None,
+                "basis": f"algorithmic Gram flops per row 2 F n_SV = {flops_row:.3g} (the tcgen05 kernel issues "
+                         "3 split-TF32 products per term, 3x this on the tensor pipe)",
+                "peak_source": pk["source"]["tf32"], "kernel_ms": kern_ms}
+
+    def parity(self, prog, x):
+        from oracle import ext_semantics as ext
+        k = min(int(x.shape[0]), 2048)
+        got = prog.run(x[:k]).cpu().numpy().astype(np.float64).ravel()
+        _, vote = ext.svm_decision(self.model(), x[:k].cpu().numpy())
+        want = np.asarray(self.model().classes)[vote]
+        return {"rows": k, "bit_exact": bool(np.array_equal(got, want)), "oracle": "oracle/svm_oracle.c (libsvm order)"}
+
+    def cpu_baseline(self, x_sample, threads):
+        from oracle import ext_semantics as ext
+        m = self.model()
+        return (lambda xs: ext.svm_decision(m, xs, threads=threads)), "oracle/svm_oracle.c (libsvm order, C)"
+
+
+WORKLOADS = {"rf500": RF500, "dt6": DT6, "gbr1000": GBR1000, "lr784": LR784, "svc10k": SVC10k, "pipe5": Pipe5}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline / reference arm
+# ---------------------------------------------------------------------------
+
+
+def _host_sample(wl, n: int, seed: int) -> np.ndarray:
+    """A host copy of the workload's input distribution (same generator family)."""
+    import torch
+    x = wl.device_input(torch.device("cpu"), seed, n) if not isinstance(wl, Pipe5) else None
+    if x is None:
+        wl._build(n)
+        return wl._x
+    return x.numpy()
+
+
+def time_cpu(wl, target_s: float, threads: int, steps: int = 1, warmup: int = 0):
+    """Run the oracle on a bounded host sample sized to ~target_s per step."""
+    fn, what = wl.cpu_baseline(None, threads)
+    cal = _host_sample(wl, 512, 97)
     t0 = time.perf_counter()
-    fast.forest_predict(packed, cal, threads=threads)
-    rate = 2000 / max(time.perf_counter() - t0, 1e-6)
-    n = int(min(max(rate * target_s, 4000), 5_000_000))
-    x = (rng.standard_normal((n, 28)) * sigma + mu).astype(np.float32)
+    fn(cal)
+    rate = cal.shape[0] / max(time.perf_counter() - t0, 1e-6)
+    n = int(min(max(rate * target_s, 256), 5_000_000))
+    x = _host_sample(wl, n, 98)
+    for _ in range(warmup):
+        fn(x[: max(n // 10, 64)])
     t0 = time.perf_counter()
-    fast.forest_predict(packed, x, threads=threads)
+    for _ in range(steps):
+        fn(x)
     dt = time.perf_counter() - t0
+    return n, dt, what
+
+
+def cpu_baseline(wl, threads: int, target_s: float = 10.0) -> dict:
+    n, dt, what = time_cpu(wl, target_s, threads)
     return {"value": n / dt, "unit": "samples/s", "cores": threads, "kind": "port",
-            "sample": f"{n} rows x 28 (randn*sigma+mu), {dt:.1f} s, oracle/liboracle.so "
-                      f"(C restatement of mlower execute semantics)"}
+            "sample": f"{n} rows x {wl.features} of the workload's input distribution, {dt:.1f} s, {what}"}
+
+
+def run_reference(args, wl):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    n, dt, what = time_cpu(wl, 5.0, threads, steps=args.steps, warmup=args.warmup)
+    value = n * args.steps / dt
+    line = {
+        "impl": "reference", "metric": wl.metric, "value": value, "unit": "samples/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": wl.describe(wl.default_rows) if not isinstance(wl, SVC10k) else wl.name,
+                   "rows_per_step": n, "sample": "bounded host sample of the workload"},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": "port",
+                         "sample": f"{n} rows per step x {args.steps} steps, {what}"},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
 
 
 def launch_ranks(n: int, argv) -> int:
-    """``--gpus N`` without a launcher: start N ranks (one per GPU) under
+    """``--gpus N`` without a launcher: start the N ranks (one per GPU) under
     torch.distributed.run ourselves, as the driver would."""
     import socket
 
@@ -189,60 +604,25 @@ def init_dist(gpus: int):
     return rank, world, local
 
 
-def run_reference(args):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return 0
-    from oracle import fast
-    model, mu, sigma = load_model()
-    packed = fast.PackedForest(model)
-    threads = os.cpu_count() or 1
-    rng = np.random.default_rng(1)
-    # size one step to ~5 s of host work
-    cal = (rng.standard_normal((2000, 28)) * sigma + mu).astype(np.float32)
-    t0 = time.perf_counter()
-    fast.forest_predict(packed, cal, threads=threads)
-    rate = 2000 / max(time.perf_counter() - t0, 1e-6)
-    n = int(min(max(rate * 5.0, 4000), 5_000_000))
-    x = (rng.standard_normal((n, 28)) * sigma + mu).astype(np.float32)
-    for _ in range(args.warmup):
-        fast.forest_predict(packed, x[: max(n // 10, 1000)], threads=threads)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        fast.forest_predict(packed, x, threads=threads)
-    dt = time.perf_counter() - t0
-    value = n * args.steps / dt
-    line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "RandomForestClassifier 500 trees depth 8, x28 fp32 rows",
-                   "rows_per_step": n, "sample": "bounded host sample of the 10M-row workload"},
-        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": "port",
-                         "sample": f"{n} rows per step x {args.steps} steps, oracle/liboracle.so"},
-        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
-    return 0
-
-
 def main(argv=None):
     ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="rf500", choices=list(WORKLOADS))
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--rows", type=int, default=10_000_000)
+    ap.add_argument("--rows", type=int, default=None)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--variant", default="auto", choices=["auto", "ranked", "skew", "perfect", "general", "mma"],
                     help="force a forest kernel variant (measurement; default: the measured AUTO choice)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
+    wl = WORKLOADS[args.config]()
     if args.impl == "reference":
-        return run_reference(args)
+        return run_reference(args, wl)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         return launch_ranks(args.gpus, sys.argv[1:] if argv is None else argv)
 
@@ -251,31 +631,33 @@ def main(argv=None):
 
     from paper_2301_13441_b200 import _native as N
     from paper_2301_13441_b200 import api
-    from paper_2301_13441_b200.runtime import run_host
+    from paper_2301_13441_b200.runtime import DeviceProgram, run_host
 
     rank, world, local = init_dist(args.gpus)
     dev = torch.device("cuda", torch.cuda.current_device())
-    model, mu, sigma = load_model()
+    n = args.rows or wl.default_rows
+    model = wl.model()
     compiled = api.compile_model(model)
     if args.variant == "auto":
         prog = compiled.program(dev.index)
     else:
-        from paper_2301_13441_b200.runtime import DeviceProgram
         prog = DeviceProgram(compiled.spec, dev.index, forest_variant={
-            "ranked": N.FOREST_RANKED, "skew": N.FOREST_SKEW, "perfect": N.FOREST_PERFECT, "general": N.FOREST_GENERAL,
-            "mma": N.FOREST_MMA}[args.variant])
-    info = prog.forest().info()
-    n = args.rows
+            "ranked": N.FOREST_RANKED, "skew": N.FOREST_SKEW, "perfect": N.FOREST_PERFECT,
+            "general": N.FOREST_GENERAL, "mma": N.FOREST_MMA}[args.variant])
+    fstage = next((st for st in prog.stages if hasattr(st, "info")), None)
+    info = fstage.info() if fstage is not None else None
+    fspec = fstage.spec if fstage is not None else None
 
-    g = torch.Generator(device=dev)
-    g.manual_seed(1 + rank)
-    x = torch.randn((n, 28), generator=g, device=dev, dtype=torch.float32)
-    x.mul_(torch.from_numpy(sigma).to(dev)).add_(torch.from_numpy(mu).to(dev))
-    y = torch.empty((n, 1), dtype=torch.uint8, device=dev)
+    x = wl.device_input(dev, rank, n)
+    y = torch.empty((n, prog.out_cols), dtype=prog_dtype(prog), device=dev)
+    bad = torch.full((1,), -1, dtype=torch.int64, device=dev) if prog.has_checks else None
     stream = torch.cuda.current_stream(dev)
 
+    def step():
+        prog.run(x, out=y, stream=stream, bad=bad)
+
     for _ in range(args.warmup):
-        prog.run(x, out=y, stream=stream)
+        step()
     torch.cuda.synchronize()
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -289,7 +671,7 @@ def main(argv=None):
         t_start.record(stream)
         for i in range(args.steps):
             ev[i][0].record(stream)
-            prog.run(x, out=y, stream=stream)
+            step()
             ev[i][1].record(stream)
         t_end.record(stream)
         torch.cuda.synchronize()
@@ -304,9 +686,9 @@ def main(argv=None):
     max_ms = float(t.item())
     value = world * n * args.steps / (max_ms / 1e3)
 
-    # ---- end to end through the public API: pinned host X -> classes on host ----
+    # ---- end to end through the public API: pinned host X -> outputs on host ----
     xh = x.cpu().pin_memory()
-    yh = torch.empty((n, 1), dtype=torch.uint8).pin_memory()
+    yh = torch.empty((n, prog.out_cols), dtype=y.dtype).pin_memory()
     run_host(prog, xh[: 1 << 20], out_host=yh[: 1 << 20])  # warm the streams
     torch.cuda.synchronize()
     if world > 1:
@@ -322,70 +704,43 @@ def main(argv=None):
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = world * n * args.e2e_steps / (float(te.item()) / 1e3)
-    parity_ok = bool(torch.equal(yh.to(dev), y))
+    same_as_device = bool(torch.equal(yh.to(dev), y))
 
     if rank == 0:
         pk = peaks()
-        ops_row = gemm_equivalent_ops(model)
-        kern_s = statistics.mean(kernel_ms) / 1e3
-        rows_per_s_kernel = n / kern_s
-        achieved_tops = rows_per_s_kernel * ops_row / 1e12
-        achieved_gbs = rows_per_s_kernel * BYTES_ROW / 1e9
-        traffic = None
-        tpath = os.path.join(ROOT, "profiles", "traffic_rf500.json")
-        if os.path.exists(tpath):  # ncu dram__bytes_read+write per row, scaled to this launch
-            with open(tpath) as fh:
-                traffic = json.load(fh)["dram_bytes_per_row"] * n
         clocks = clk.summary()
-        smem = None  # the traversal's binding resource: shared-memory load wavefronts
-        spath = os.path.join(ROOT, "profiles", "r1_forest_ranked_ncu_summary.json")
-        if info["variant"] == "ranked" and os.path.exists(spath):
-            with open(spath) as fh:
-                js = json.load(fh)
-            wf_row = float(str(js["l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum"]).split()[0]) / js["rows"]
-            sms = torch.cuda.get_device_properties(dev).multi_processor_count
-            mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965.0
-            ach = rows_per_s_kernel * wf_row / 1e9
-            pk_w = sms * mhz * 1e6 / 1e9
-            smem = {"achieved": ach, "peak": pk_w, "unit": "Gwavefronts/s", "frac": ach / pk_w,
-                    "wavefronts_row": wf_row,
-                    "basis": "shared-memory load wavefronts per row (ncu, profiles/r1_forest_ranked_ncu_summary.json) "
-                             "x live rows/s; peak = 1 wavefront/clk/SM at the measured SM clock"}
+        kern_ms = statistics.mean(kernel_ms)
+        rows_per_s_kernel = n / (kern_ms / 1e3)
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        roof = wl.roofline(prog, fspec, info, rows_per_s_kernel, kern_ms, n, pk, clocks, sms)
+        cfg = wl.config(n, world, info)
+        if info is not None:
+            cfg.update({"variant": info["variant"], "chunk": info["chunk_trees"], "rows_per_cta": info["rows_per_cta"]})
         line = {
-            "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+            "metric": wl.metric, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {
-                "workload": f"RandomForestClassifier 500 trees depth 8 on {n} x 28 fp32 rows per GPU",
-                "forest_source": "sklearn RF500 max_depth=8 fit on make_classification(200k x 28), "
-                                 "bench_assets/rf500_d8.npz",
-                "rows_per_gpu": n, "trees": len(model.trees), "features": 28,
-                "parallelism": f"row-shard dp{world}", "variant": info['variant'] + ("-path-matrix" if info['variant'] == "mma" else "-traversal"),
-                "chunk_trees": info["chunk_trees"], "rows_per_cta": info["rows_per_cta"],
-                "l2": "inputs 1.12 GB per step > 126 MB L2 (no flush needed)"},
-            "roofline": {
-                "bound": "tensor", "achieved": achieved_tops, "peak": pk["int8_tops"], "unit": "TOPS",
-                "frac": achieved_tops / pk["int8_tops"], "traffic": traffic,
-                "basis": "GEMM-equivalent int8 work of the reference encoding, ops_row = sum_t 2*I_t*L_t "
-                         f"= {ops_row} (SURVEY 8d); kernel = {info['variant']} variant",
-                "peak_source": pk["source"]["int8"],
-                "hbm": {"achieved": achieved_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                        "frac": achieved_gbs / pk["hbm_gbs"], "bytes_row": BYTES_ROW,
-                        "peak_source": pk["source"]["hbm"]},
-                "smem": smem,
-                "kernel_ms": statistics.mean(kernel_ms)},
-            "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": n * 28 * 4,
-                    "d2h_bytes_per_step": n * 1, "steps": args.e2e_steps, "parity_vs_device": parity_ok},
+            "config": cfg, "roofline": roof,
+            "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": n * wl.features * 4,
+                    "d2h_bytes_per_step": n * prog.out_cols * y.element_size(), "steps": args.e2e_steps,
+                    "same_as_device_path": same_as_device},
             "gpu_launches": int(launches),
             "clocks": clocks,
         }
+        if not args.no_parity:
+            line["parity"] = wl.parity(prog, x)
         if not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(model, mu, sigma)
+            line["cpu_baseline"] = cpu_baseline(wl, os.cpu_count() or 1)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def prog_dtype(prog):
+    from paper_2301_13441_b200.runtime import TORCH_DTYPE
+    return TORCH_DTYPE[prog.out_dtype]
 
 
 if __name__ == "__main__":

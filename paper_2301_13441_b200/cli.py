@@ -81,9 +81,9 @@ def _passes(spec):
 def _compile(args):
     from .api import compile_model
     from .models import parse_model
-    if args.profile not in ("cpu-avx2", "plain"):
-        raise ValidationError(f"unknown profile {args.profile!r} (builtin: cpu-avx2, plain)")
-    return compile_model(parse_model(_read_text(args.model)), args.profile, _passes(args.passes))
+    from .lower import load_profile
+    profile = load_profile(args.profile)  # builtin name or JSON profile file (graph.py:146-168)
+    return compile_model(parse_model(_read_text(args.model)), profile, _passes(args.passes))
 
 
 def cmd_compile(args) -> int:
@@ -159,7 +159,7 @@ def build_parser() -> argparse.ArgumentParser:
 
     def common(p):
         p.add_argument("--model", required=True, help="model JSON path")
-        p.add_argument("--profile", default="cpu-avx2", help="builtin profile name")
+        p.add_argument("--profile", default="cpu-avx2", help="builtin profile name or JSON profile path")
         p.add_argument("--passes", default=None, help="comma-separated subset of re,dr,sor")
 
     p = sub.add_parser("compile", help="lower a model, print the fused device program")

@@ -556,6 +556,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// Shared-memory loads at absolute shared-window addresses (one LDS, no
+// generic-to-shared base add per access).  volatile keeps them in the order
+// written, which the walks use to batch independent loads.
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];\n" : "=h"(v) : "r"(addr));
+  return v;
+}
+
 template <int CT>
 __device__ __forceinline__ void load_payload_shared(uint32_t addr, float (&v)[CT]) {
   if constexpr (CT == 1) {
@@ -877,19 +891,25 @@ __global__ void __launch_bounds__(NTT, 1) forest_ranked_kernel(const ForestArgs 
 // below 2^(53-q), so every float64 partial sum in ANY order is exact and equals
 // numpy's sequential or pairwise result bit for bit).  Padding trees of the
 // last group go always-left onto a zero payload (+0.0 changes no exact sum).
-template <int CT, int NTT, int RPT, int TI>
+template <int CT, int NTT, int RPT, int TI, int DT>
 __global__ void __launch_bounds__(NTT, 1) forest_skew_kernel(const ForestArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int ROWS = NTT * RPT;
   constexpr int STEPS = 32 / TI;
+  constexpr int WARPS = NTT / 32;
   static_assert(ROWS % 64 == 0, "rank tile interleave needs 64-row groups");
-  static_assert(TI == 1 || TI == 2 || TI == 4 || TI == 8, "walks per step");
+  static_assert(TI == 2 || TI == 4 || TI == 8 || TI == 16, "walks per step");
   const int tid = threadIdx.x, lane = tid & 31;
   const int64_t tile = (int64_t)blockIdx.x * ROWS;
   const int F = a.F;
   const uint32_t chunk_off = (uint32_t)(((size_t)F * ROWS * 2 + 15) & ~(size_t)15);
   uint8_t* chunk = smem + chunk_off;
+  // full: chunk landed (TMA tx count); empty: every warp is done with it.  The
+  // buffers are released per warp (no CTA-wide barrier between chunks), so
+  // warps drift freely across chunk boundaries; thread 0 refills a buffer once
+  // its empty barrier completes.
   __shared__ __align__(8) uint64_t tree_bar[2];
+  __shared__ __align__(8) uint64_t empty_bar[2];
   __shared__ __align__(8) uint64_t stage_bar[2];
   const uint32_t gbytes = (uint32_t)a.tree_bytes;              // one 32-tree group
   const uint32_t buf_bytes = (uint32_t)a.chunk_trees * gbytes;  // chunk_trees = groups per buffer here
@@ -909,6 +929,8 @@ __global__ void __launch_bounds__(NTT, 1) forest_skew_kernel(const ForestArgs a)
   if (tid == 0) {
     mbar_init(&tree_bar[0], 1);
     mbar_init(&tree_bar[1], 1);
+    mbar_init(&empty_bar[0], WARPS);
+    mbar_init(&empty_bar[1], WARPS);
     mbar_init(&stage_bar[0], 1);
     mbar_init(&stage_bar[1], 1);
     mbar_fence_init();
@@ -938,51 +960,69 @@ __global__ void __launch_bounds__(NTT, 1) forest_skew_kernel(const ForestArgs a)
 #pragma unroll
     for (int c = 0; c < CT; ++c) acc[k][c] = 0.0;
 
-  const int D = a.depth;
+  const int D = DT > 0 ? DT : a.depth;
   const int ni = a.ni;
-  const uint8_t* xrb = smem;
-  const uint32_t smem_base = smem_u32(smem);
+  const uint32_t B = smem_u32(smem);  // all walk addresses are absolute shared-window addresses
+  uint32_t pbs[RPT];
+#pragma unroll
+  for (int k = 0; k < RPT; ++k) pbs[k] = B + pb[k];
 
-  // One step of one group: TI walks per row, tree (lane + s + q*STEPS) & 31.
-  auto walk_step = [&](auto leafconst, uint32_t gofs, int g, int s) {
+  // One step of one group: TI walks per row, tree (lane + s + q*STEPS) & 31,
+  // i.e. byte column rot_q = 4 * tree within each 128-byte node row.  Loads
+  // are issued all-nodes-then-all-ranks so the TI x RPT chains overlap.
+  auto walk_step = [&](auto leafconst, uint32_t gofs, int g, uint32_t rot) {
     constexpr bool LEAF = decltype(leafconst)::value;
-    const uint32_t nb = gofs + (uint32_t)a.node_off_bytes;  // node words of this group
-    uint32_t o[TI][RPT], cst[TI], tq[TI];
+    const uint32_t nb = B + gofs + (uint32_t)a.node_off_bytes;  // node words of this group (128-aligned)
+    uint32_t o[TI][RPT], cst[TI];
 #pragma unroll
     for (int q = 0; q < TI; ++q) {
-      tq[q] = (uint32_t)(lane + s + q * STEPS) & 31u;
-      cst[q] = 128u - nb - 4u * tq[q];  // child j' = 2j+1(+1): o' = 2o + cst (+128)
+      const uint32_t o0 = nb + ((rot + 4u * (uint32_t)(q * STEPS)) & 127u);
+      cst[q] = 128u - o0;  // child j' = 2j+1 (+1): o' = 2o + 128 - o0 (+128)
 #pragma unroll
-      for (int k = 0; k < RPT; ++k) o[q][k] = nb + 4u * tq[q];
+      for (int k = 0; k < RPT; ++k) o[q][k] = o0;
     }
     auto level = [&]() {
+      uint32_t w[TI][RPT], rk[TI][RPT];
 #pragma unroll
-      for (int q = 0; q < TI; ++q) {
+      for (int q = 0; q < TI; ++q)
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) w[q][k] = lds_u32(o[q][k]);
+#pragma unroll
+      for (int q = 0; q < TI; ++q)
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) rk[q][k] = lds_u16(((w[q][k] >> 14) + pbs[k]));
+#pragma unroll
+      for (int q = 0; q < TI; ++q)
 #pragma unroll
         for (int k = 0; k < RPT; ++k) {
-          const uint32_t w = *reinterpret_cast<const uint32_t*>(smem + o[q][k]);
-          const uint32_t rk = *reinterpret_cast<const uint16_t*>(xrb + ((w >> 14) + pb[k]));
           uint32_t nx = 2u * o[q][k] + cst[q];
-          if (rk > (w & 0xFFFFu)) nx += 128u;
+          if (rk[q][k] > (w[q][k] & 0xFFFFu)) nx += 128u;
           o[q][k] = nx;
         }
-      }
     };
-    int lvl = 0;
-    for (; lvl + 2 <= D; lvl += 2) { level(); level(); }
-    if (lvl < D) level();
+    if constexpr (DT > 0) {
+#pragma unroll
+      for (int l = 0; l < DT; ++l) level();
+    } else {
+      int lvl = 0;
+      for (; lvl + 2 <= D; lvl += 2) { level(); level(); }
+      if (lvl < D) level();
+    }
     // leaf: o = nb + 4*(32*j + t), j >= ni; payload at gofs + (32*(j - ni) + t)*CT*4
-    const uint32_t pay_c = smem_base + gofs - (nb + (uint32_t)ni * 128u) * CT;
+    const uint32_t pay_c = B + gofs - (nb + (uint32_t)ni * 128u) * CT;
+    float v[TI][RPT][CT];
+#pragma unroll
+    for (int q = 0; q < TI; ++q)
+#pragma unroll
+      for (int k = 0; k < RPT; ++k) load_payload_shared<CT>(pay_c + o[q][k] * CT, v[q][k]);
 #pragma unroll
     for (int q = 0; q < TI; ++q) {
 #pragma unroll
       for (int k = 0; k < RPT; ++k) {
-        float v[CT];
-        load_payload_shared<CT>(pay_c + o[q][k] * CT, v);
 #pragma unroll
-        for (int c = 0; c < CT; ++c) acc[k][c] += (double)v[c];
+        for (int c = 0; c < CT; ++c) acc[k][c] += (double)v[q][k][c];
         if constexpr (LEAF) {
-          const int t = g * 32 + (int)tq[q];
+          const int t = g * 32 + (int)(((o[q][k] - nb) >> 2) & 31u);
           if (t < T && rowk[k] < a.n_rows) {
             const int slot = (int)(((o[q][k] - nb) >> 2) >> 5) - ni;
             a.leaf_out[rowk[k] * T + t] = __ldg(a.slot_leaf + (int64_t)t * a.ns + slot);
@@ -993,23 +1033,35 @@ __global__ void __launch_bounds__(NTT, 1) forest_skew_kernel(const ForestArgs a)
   };
 
   __syncthreads();  // ranks complete; staging buffers no longer read
-  if (tid == 0 && !a.stage_off) issue_chunk(0);
+  if (tid == 0) {
+    if (!a.stage_off) issue_chunk(0);
+    if (nchunks > 1) issue_chunk(1);
+  }
+  const uint32_t rot0 = 4u * (uint32_t)lane;
   for (int ci = 0; ci < nchunks; ++ci) {
     const int g0 = ci * a.chunk_trees;
     const int ng = min(a.chunk_trees, G - g0);
-    if (tid == 0 && ci + 1 < nchunks) issue_chunk(ci + 1);
     mbar_wait(&tree_bar[ci & 1], (uint32_t)(ci >> 1) & 1u);
     const uint32_t buf_off = chunk_off + (uint32_t)(ci & 1) * buf_bytes;
     for (int gl = 0; gl < ng; ++gl) {
       const uint32_t gofs = buf_off + (uint32_t)gl * gbytes;
+      uint32_t rot = rot0;
       if (a.leaf_out) {
-        for (int s = 0; s < STEPS; ++s) walk_step(std::true_type{}, gofs, g0 + gl, s);
+        for (int st = 0; st < STEPS; ++st, rot += 4u) walk_step(std::true_type{}, gofs, g0 + gl, rot);
       } else {
 #pragma unroll 1
-        for (int s = 0; s < STEPS; ++s) walk_step(std::false_type{}, gofs, g0 + gl, s);
+        for (int st = 0; st < STEPS; ++st, rot += 4u) walk_step(std::false_type{}, gofs, g0 + gl, rot);
       }
     }
-    __syncthreads();  // every thread done with this buffer before it is refilled
+    // release this buffer: one arrive per warp; thread 0 refills it with
+    // chunk ci + 2 once every warp has arrived
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[ci & 1]);
+    if (tid < 32 && ci + 2 < nchunks) {  // warp 0 waits as a whole (no divergent walk)
+      mbar_wait(&empty_bar[ci & 1], (uint32_t)(ci >> 1) & 1u);
+      if (tid == 0) issue_chunk(ci + 2);
+      __syncwarp();
+    }
   }
 
   float none[CT];
@@ -1400,27 +1452,28 @@ static KernelFn ranked_for(const cmlb_forest& f) {
 }
 
 // Skew launch configurations: (threads, rows per thread, walks per step).
-constexpr RankedCfg SKEW_CFGS[] = {{512, 1, 4}, {256, 2, 4}, {256, 2, 2}, {1024, 1, 4}, {512, 1, 8}, {256, 2, 8}};
+constexpr RankedCfg SKEW_CFGS[] = {{512, 1, 8}, {512, 1, 16}, {512, 1, 4}, {256, 2, 8}, {1024, 1, 8}};
 constexpr int N_SKEW_CFGS = sizeof(SKEW_CFGS) / sizeof(SKEW_CFGS[0]);
 
-template <int CT>
+template <int CT, int DT>
 static KernelFn skew_cfg(int cfg) {
   switch (cfg) {
-    case 0: return forest_skew_kernel<CT, 512, 1, 4>;
-    case 1: return forest_skew_kernel<CT, 256, 2, 4>;
-    case 2: return forest_skew_kernel<CT, 256, 2, 2>;
-    case 3: return forest_skew_kernel<CT, 1024, 1, 4>;
-    case 4: return forest_skew_kernel<CT, 512, 1, 8>;
-    case 5: return forest_skew_kernel<CT, 256, 2, 8>;
+    case 0: return forest_skew_kernel<CT, 512, 1, 8, DT>;
+    case 1: return forest_skew_kernel<CT, 512, 1, 16, DT>;
+    case 2: return forest_skew_kernel<CT, 512, 1, 4, DT>;
+    case 3: return forest_skew_kernel<CT, 256, 2, 8, DT>;
+    case 4: return forest_skew_kernel<CT, 1024, 1, 8, DT>;
     default: return nullptr;
   }
 }
 
+// depth 8 (the north star's) gets fully unrolled levels; others loop
 static KernelFn skew_for(const cmlb_forest& f) {
+  const bool d8 = f.depth == 8;
   switch (f.CT) {
-    case 1: return skew_cfg<1>(f.rcfg);
-    case 2: return skew_cfg<2>(f.rcfg);
-    case 4: return skew_cfg<4>(f.rcfg);
+    case 1: return d8 ? skew_cfg<1, 8>(f.rcfg) : skew_cfg<1, 0>(f.rcfg);
+    case 2: return d8 ? skew_cfg<2, 8>(f.rcfg) : skew_cfg<2, 0>(f.rcfg);
+    case 4: return d8 ? skew_cfg<4, 8>(f.rcfg) : skew_cfg<4, 0>(f.rcfg);
     default: return nullptr;
   }
 }
@@ -1784,7 +1837,7 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
     s_gbytes = s_node_off + ni_r * 32 * 4;
     size_t max_nf = 0;
     for (auto& u : U) max_nf = std::max(max_nf, u.size());
-    std::vector<int> order = {0, 1, 4, 5, 2, 3};
+    std::vector<int> order = {0, 1, 2, 3, 4};
     if (const char* env = getenv("CMLB_SKEW_CFG")) order = {atoi(env)};
     bool found = false;
     for (size_t oi = 0; oi < order.size() && !found; ++oi) {

@@ -172,13 +172,57 @@ class ProgramSpec:
 # -- profile handling ----------------------------------------------------------
 
 
+@dataclass(frozen=True)
+class Profile:
+    """Mirror of the reference ``HardwareProfile`` (``graph.py:128-135``).
+    Only ``sparse_threshold`` changes GPU semantics (dense vs CSR selector and
+    linear weights, SOR ``passes.py:201-215``)."""
+
+    name: str
+    preferred_int_dtype: str
+    sparse_threshold: float
+    notes: str = ""
+
+
+BUILTIN_PROFILES = {"cpu-avx2": Profile("cpu-avx2", "int8", 0.3), "plain": Profile("plain", "int32", 0.0)}
+
+
+def load_profile(name_or_path: str) -> Profile:
+    """Builtin name or JSON profile file, validated as ``graph.py:146-168``."""
+    import json
+
+    from .errors import ProfileError
+    if name_or_path in BUILTIN_PROFILES:
+        return BUILTIN_PROFILES[name_or_path]
+    try:
+        with open(name_or_path, "r", encoding="utf-8") as fh:
+            obj = json.load(fh)
+    except OSError as e:
+        raise ProfileError(f"cannot read profile {name_or_path!r}: {e}") from None
+    except json.JSONDecodeError as e:
+        raise ProfileError(f"profile {name_or_path!r}: invalid JSON ({e.msg})") from None
+    if not isinstance(obj, dict):
+        raise ProfileError("profile must be a JSON object")
+    try:
+        name = obj["name"]
+        pref = str(obj["preferred_int_dtype"])
+        threshold = float(obj["sparse_threshold"])
+    except KeyError as e:
+        raise ProfileError(f"profile missing field {e.args[0]!r}") from None
+    except (TypeError, ValueError):
+        raise ProfileError("sparse_threshold must be a number") from None
+    if pref not in ("int8", "int16", "int32"):
+        raise ProfileError("preferred_int_dtype must be int8, int16 or int32")
+    if not 0.0 <= threshold <= 1.0:
+        raise ProfileError("sparse_threshold must lie in [0, 1]")
+    return Profile(str(name), pref, threshold, str(obj.get("notes", "")))
+
+
 def sparse_threshold(profile) -> float:
     if profile is None:
         return _PROFILE_THRESHOLD["cpu-avx2"]
     if isinstance(profile, str):
-        if profile not in _PROFILE_THRESHOLD:
-            raise ValidationError(f"unknown profile {profile!r}")
-        return _PROFILE_THRESHOLD[profile]
+        return load_profile(profile).sparse_threshold
     return float(profile.sparse_threshold)
 
 

@@ -65,3 +65,20 @@ def test_run_matches_golden_and_is_byte_deterministic(name, tmp_path):
     assert outs[0] == outs[1]
     got = read_csv(outs[0].decode(), case.want.shape[1]).astype(np.float64)
     np.testing.assert_array_equal(got, case.want.astype(np.float32).astype(np.float64))
+
+
+def test_json_profile_file(tmp_path, capsys):
+    """--profile also takes a JSON profile (reference graph.py:146-168): a
+    custom sparse_threshold reaches the lowering; a bad one is a ProfileError."""
+    from paper_2301_13441_b200 import lower
+    from paper_2301_13441_b200.errors import ProfileError
+    good = tmp_path / "p.json"
+    good.write_text('{"name": "dense", "preferred_int_dtype": "int16", "sparse_threshold": 0.0}')
+    prof = lower.load_profile(str(good))
+    assert prof.sparse_threshold == 0.0 and lower.sparse_threshold(str(good)) == 0.0
+    bad = tmp_path / "bad.json"
+    bad.write_text('{"name": "x", "preferred_int_dtype": "int16", "sparse_threshold": 1.5}')
+    with pytest.raises(ProfileError):
+        lower.load_profile(str(bad))
+    with pytest.raises(ProfileError):
+        lower.load_profile(str(tmp_path / "missing.json"))

@@ -1,0 +1,37 @@
+"""The reference's own test suite, run with its executor swapped for ours
+(tests/ref_swap_plugin.py): ``mlower.runtime.execute`` -> ``api.execute`` on
+the B200.  Needs the reference installed in baseline/_ref
+(tools/install_reference.sh; git-ignored, it travels with the snapshot)."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = os.path.join(ROOT, "baseline", "_ref")
+REF_TESTS = os.path.join(REF, "mlower_tests")
+
+pytestmark = pytest.mark.gpu
+
+# the reference test files whose assertions go through execute()
+FILES = ["test_runtime.py", "test_acceptance.py", "test_cli.py", "test_passes.py", "test_oracle.py"]
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_TESTS), reason="reference not installed (tools/install_reference.sh)")
+def test_reference_suite_with_b200_executor(tmp_path):
+    report = tmp_path / "swap.json"
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([REF, REF_TESTS, os.path.join(ROOT, "tests"), ROOT]),
+               REF_SWAP_REPORT=str(report), PYTHONHASHSEED="0")
+    cmd = [sys.executable, "-m", "pytest", "-q", "-p", "ref_swap_plugin", "-p", "no:cacheprovider",
+           "--rootdir", REF_TESTS, *[os.path.join(REF_TESTS, f) for f in FILES]]
+    r = subprocess.run(cmd, cwd=REF_TESTS, env=env, capture_output=True, text=True, timeout=3000)
+    tail = "\n".join(r.stdout.splitlines()[-40:])
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", "ref_swap.log"), "w") as fh:
+        fh.write(r.stdout + "\n----\n" + r.stderr)
+    stats = json.loads(report.read_text())
+    assert stats["gpu_executes"] > 1000, (stats, tail)
+    assert r.returncode == 0, tail

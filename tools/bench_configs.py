@@ -179,6 +179,18 @@ def synthetic_svc(F=784, n_sv=10_000, C=10, seed=5):
                     tuple(int(v) for v in n_support), tuple(float(c) for c in range(C)))
 
 
+def svc_model():
+    """The config-4b model bench.py --config svc10k runs (see bench_assets/)."""
+    return synthetic_svc()
+
+
+def svc_inputs(dev, rank: int, n: int):
+    import torch
+    g = torch.Generator(device=dev)
+    g.manual_seed(3 + rank)
+    return torch.randn((n, 784), generator=g, device=dev, dtype=torch.float32)
+
+
 def tf32_peak():
     p = os.path.join(ROOT, "profiles", "peaks_tf32.json")
     if os.path.exists(p):
