@@ -556,6 +556,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// Exact float32 -> float64 of a NONNEGATIVE value on the integer pipe (two
+// ALU ops instead of F2F.F64.F32, which issues at 16 lanes/clk/SM and
+// throttled the walk: ncu math_pipe_throttle 13%).  For a normal (not subnormal)
+// f32 with bits b, the double's high word is (b >> 3) + (896 << 20) and its low
+// word b << 29 -- except +0.0, which maps to 2^-127 instead of 0.  The SKEW
+// kernel only runs certified forests (payloads >= 0, every nonzero sum >= 2^-q),
+// so each stray 2^-127 vanishes in the next rounding against a
+// nonzero partial sum (the host requires T_pad * 2^-127 < 2^(-q-53)), and an
+// all-zero sum (at most T_pad * 2^-127 < 2^-100) is flushed to 0 before the
+// tail (flush_tiny).
+__device__ __forceinline__ double f32_to_f64_nonneg(float v) {
+  const uint32_t b = __float_as_uint(v);
+  return __hiloint2double((int)((b >> 3) + 0x38000000u), (int)(b << 29));
+}
+__device__ __forceinline__ double flush_tiny(double s) { return s < 0x1p-100 ? 0.0 : s; }
+
 // Shared-memory loads at absolute shared-window addresses (one LDS, no
 // generic-to-shared base add per access).  volatile keeps them in the order
 // written, which the walks use to batch independent loads.
@@ -1020,7 +1036,7 @@ __global__ void __launch_bounds__(NTT, 1) forest_skew_kernel(const ForestArgs a)
 #pragma unroll
       for (int k = 0; k < RPT; ++k) {
 #pragma unroll
-        for (int c = 0; c < CT; ++c) acc[k][c] += (double)v[q][k][c];
+        for (int c = 0; c < CT; ++c) acc[k][c] += f32_to_f64_nonneg(v[q][k][c]);
         if constexpr (LEAF) {
           const int t = g * 32 + (int)(((o[q][k] - nb) >> 2) & 31u);
           if (t < T && rowk[k] < a.n_rows) {
@@ -1072,7 +1088,7 @@ __global__ void __launch_bounds__(NTT, 1) forest_skew_kernel(const ForestArgs a)
     if (rowk[k] >= a.n_rows) continue;
     RowAcc<CT, false> r;
 #pragma unroll
-    for (int c = 0; c < CT; ++c) r.acc[c] = acc[k][c];
+    for (int c = 0; c < CT; ++c) r.acc[c] = flush_tiny(acc[k][c]);
     finish_row<CT, false>(a, rowk[k], r, none);
   }
 }
@@ -1672,8 +1688,9 @@ static void fill_mma(const cmlb_forest_desc* d, int t, int K, int N, int CT, int
 // representable exactly, never rounded.  Then numpy's sequential (C >= 2) and
 // pairwise (C == 1) float64 reductions both equal the exact sum, and so does
 // any other order: the condition for the SKEW variant's rotated tree order.
-static bool sums_order_free(const cmlb_forest_desc* d) {
+static bool sums_order_free(const cmlb_forest_desc* d, int* q_out = nullptr, bool* nonneg = nullptr) {
   int q = -2000;
+  if (nonneg) *nonneg = true;
   double bound = 0.0;
   for (int t = 0; t < d->n_trees; ++t) {
     double mx = 0.0;
@@ -1681,6 +1698,7 @@ static bool sums_order_free(const cmlb_forest_desc* d) {
       for (int c = 0; c < d->n_outputs; ++c) {
         const float v = d->payload[l * d->n_outputs + c];
         if (!std::isfinite(v)) return false;
+        if (nonneg && (v < 0.0f || std::signbit(v))) *nonneg = false;
         if (v == 0.0f) continue;
         int e = 0;
         std::frexp(v, &e);  // |v| = m * 2^e, m in [0.5, 1)
@@ -1690,6 +1708,7 @@ static bool sums_order_free(const cmlb_forest_desc* d) {
       }
     bound += mx;
   }
+  if (q_out) *q_out = q;
   if (bound == 0.0) return true;
   return std::ldexp(bound * (1.0 + 1e-12), q) < 9007199254740992.0;  // 2^53
 }
@@ -1827,7 +1846,18 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
 
   // skew plan: as ranked, but 32-tree groups interleaved across the banks;
   // needs the order-free certificate and a whole group per TMA buffer
-  bool skew_ok = ranked_ok && f->CT <= 4 && sums_order_free(d);
+  // (+ nonnegative payloads with every nonzero sum >= 2^-99: the kernel's
+  // integer-pipe float64 conversion, f32_to_f64_nonneg)
+  int cert_q = 0;
+  bool cert_nonneg = false;
+  bool skew_ok = ranked_ok && f->CT <= 4 && sums_order_free(d, &cert_q, &cert_nonneg) && cert_nonneg;
+  {
+    // up to T_pad stray 2^-127 (zero payloads) must stay below half an ulp of
+    // the smallest nonzero sum (2^-q): T_pad * 2^-127 < 2^(-q-53)
+    int lg = 0;
+    while ((1 << lg) < (f->T + 31) / 32 * 32) ++lg;
+    skew_ok = skew_ok && cert_q + lg + 53 < 127;
+  }
   int s_cfg = 0, s_ntt = 0, s_rpt = 0, s_groups = 0, s_gbytes = 0, s_node_off = 0, s_stage = 0, s_stage_off = 0,
       s_stage_bufs = 2;
   size_t s_smem = 0;

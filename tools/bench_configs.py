@@ -180,15 +180,28 @@ def synthetic_svc(F=784, n_sv=10_000, C=10, seed=5):
 
 
 def svc_model():
-    """The config-4b model bench.py --config svc10k runs (see bench_assets/)."""
-    return synthetic_svc()
+    """Config 4b: sklearn SVC(kernel="rbf") fit on synthetic MNIST-shaped 8-bit
+    digits, 9,626 support vectors (tools/make_svc_model.py ->
+    bench_assets/svc_digits.npz); support vectors are exactly u8 / 255 in f32."""
+    from paper_2301_13441_b200.extmodels import SVMModel
+    z = np.load(os.path.join(ROOT, "bench_assets", "svc_digits.npz"))
+    sv = z["sv_u8"].astype(np.float32) / np.float32(255)
+    return SVMModel("svc", 784, "rbf", float(z["gamma"]), 0.0, 3, sv, z["dual_coef"], z["intercept"],
+                    tuple(int(v) for v in z["n_support"]), tuple(float(c) for c in z["classes"]))
 
 
 def svc_inputs(dev, rank: int, n: int):
+    """Inference rows from the model's own distribution: a class prototype at a
+    random contrast plus pixel noise, clipped and quantised to 8 bits, / 255."""
     import torch
+    z = np.load(os.path.join(ROOT, "bench_assets", "svc_digits.npz"))
     g = torch.Generator(device=dev)
     g.manual_seed(3 + rank)
-    return torch.randn((n, 784), generator=g, device=dev, dtype=torch.float32)
+    proto = torch.from_numpy(z["proto"]).to(dev)
+    y = torch.randint(0, proto.shape[0], (n,), generator=g, device=dev)
+    x = proto[y] * (0.5 + 0.7 * torch.rand((n, 1), generator=g, device=dev))
+    x += float(z["noise"]) * torch.randn((n, 784), generator=g, device=dev)
+    return x.round_().clamp_(0, 255).div_(255.0)
 
 
 def tf32_peak():
