@@ -150,6 +150,10 @@ struct ForestArgs {
   // MMA variant
   int mma_k, mma_n, mma_feat_off, mma_thr_off, mma_pay_off;
   int probe;                  // debug (CMLB_MMA_PROBE): 1 skip compares, 2 skip blob TMA, 4 skip epilogue reads
+  // opaque constants (1, 2, 128, 2^29, 0x38000000) the SKEW walk multiplies by, so
+  // ptxas keeps those steps as IMAD on the FMA pipe instead of strength-reducing
+  // them to shifts/adds on the ALU pipe (which bound the walk, ncu alu 65%)
+  uint32_t k1, k2, k128, k2p29, kexp;
 };
 
 constexpr int NT = 256;  // threads per CTA for every forest kernel
@@ -566,9 +570,34 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // nonzero partial sum (the host requires T_pad * 2^-127 < 2^(-q-53)), and an
 // all-zero sum (at most T_pad * 2^-127 < 2^-100) is flushed to 0 before the
 // tail (flush_tiny).
-__device__ __forceinline__ double f32_to_f64_nonneg(float v) {
+struct SkewConsts { uint32_t one, two, c128, c2p29, cexp, ct; };
+
+__device__ __forceinline__ uint32_t imad_u32(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+// One level of the skewed walk: o' = 2 o + cst (+128 when rank > threshold).
+// The two adds are IMADs by opaque constants (FMA pipe); the mask, compare and
+// the rank address (caller) stay on the ALU pipe.
+__device__ __forceinline__ uint32_t skew_next(uint32_t o, uint32_t cst, uint32_t rk, uint32_t w, const SkewConsts& k) {
+  uint32_t nx;
+  asm("{\n .reg .pred p;\n .reg .b32 t;\n"
+      " and.b32 t, %4, 65535;\n"
+      " setp.gt.u32 p, %3, t;\n"
+      " mad.lo.u32 %0, %1, %5, %2;\n"
+      " @p mad.lo.u32 %0, %6, %7, %0;\n}"
+      : "=&r"(nx) : "r"(o), "r"(cst), "r"(rk), "r"(w), "r"(k.two), "r"(k.one), "r"(k.c128));
+  return nx;
+}
+
+__device__ __forceinline__ double f32_to_f64_nonneg(float v, const SkewConsts& k) {
   const uint32_t b = __float_as_uint(v);
-  return __hiloint2double((int)((b >> 3) + 0x38000000u), (int)(b << 29));
+  uint32_t hi, lo;
+  asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(hi) : "r"(b), "r"(k.c2p29), "r"(k.cexp));  // (b >> 3) + 0x38000000
+  asm("mul.lo.u32 %0, %1, %2;" : "=r"(lo) : "r"(b), "r"(k.c2p29));                 // b << 29
+  return __hiloint2double((int)hi, (int)lo);
 }
 __device__ __forceinline__ double flush_tiny(double s) { return s < 0x1p-100 ? 0.0 : s; }
 
@@ -979,6 +1008,7 @@ __global__ void __launch_bounds__(NTT, 1) forest_skew_kernel(const ForestArgs a)
   const int D = DT > 0 ? DT : a.depth;
   const int ni = a.ni;
   const uint32_t B = smem_u32(smem);  // all walk addresses are absolute shared-window addresses
+  const SkewConsts kc{a.k1, a.k2, a.k128, a.k2p29, a.kexp, a.k1 * (uint32_t)CT};
   uint32_t pbs[RPT];
 #pragma unroll
   for (int k = 0; k < RPT; ++k) pbs[k] = B + pb[k];
@@ -1010,11 +1040,7 @@ __global__ void __launch_bounds__(NTT, 1) forest_skew_kernel(const ForestArgs a)
 #pragma unroll
       for (int q = 0; q < TI; ++q)
 #pragma unroll
-        for (int k = 0; k < RPT; ++k) {
-          uint32_t nx = 2u * o[q][k] + cst[q];
-          if (rk[q][k] > (w[q][k] & 0xFFFFu)) nx += 128u;
-          o[q][k] = nx;
-        }
+        for (int k = 0; k < RPT; ++k) o[q][k] = skew_next(o[q][k], cst[q], rk[q][k], w[q][k], kc);
     };
     if constexpr (DT > 0) {
 #pragma unroll
@@ -1030,13 +1056,13 @@ __global__ void __launch_bounds__(NTT, 1) forest_skew_kernel(const ForestArgs a)
 #pragma unroll
     for (int q = 0; q < TI; ++q)
 #pragma unroll
-      for (int k = 0; k < RPT; ++k) load_payload_shared<CT>(pay_c + o[q][k] * CT, v[q][k]);
+      for (int k = 0; k < RPT; ++k) load_payload_shared<CT>(imad_u32(o[q][k], kc.ct, pay_c), v[q][k]);
 #pragma unroll
     for (int q = 0; q < TI; ++q) {
 #pragma unroll
       for (int k = 0; k < RPT; ++k) {
 #pragma unroll
-        for (int c = 0; c < CT; ++c) acc[k][c] += f32_to_f64_nonneg(v[q][k][c]);
+        for (int c = 0; c < CT; ++c) acc[k][c] += f32_to_f64_nonneg(v[q][k][c], kc);
         if constexpr (LEAF) {
           const int t = g * 32 + (int)(((o[q][k] - nb) >> 2) & 31u);
           if (t < T && rowk[k] < a.n_rows) {
@@ -2073,6 +2099,7 @@ static int run_forest(const cmlb_forest* f, const float* x, int64_t n_rows, int6
     return pe ? atoi(pe) : 0;
   }();
   a.probe = mma_probe;
+  a.k1 = 1u; a.k2 = 2u; a.k128 = 128u; a.k2p29 = 1u << 29; a.kexp = 0x38000000u;
   const bool rk = f->variant == CMLB_FOREST_RANKED || f->variant == CMLB_FOREST_SKEW;
   const int threads = rk ? f->ntt : (f->variant == CMLB_FOREST_MMA ? MMA2_THREADS : NT);
   const int64_t rows = f->variant == CMLB_FOREST_MMA ? (int64_t)MMA_M : (int64_t)threads * f->rpt;

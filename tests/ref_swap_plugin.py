@@ -34,6 +34,20 @@ def pytest_configure(config):
     from paper_2301_13441_b200.errors import UnresolvedKernel
 
     reference_execute = mlower.runtime.execute
+    if os.environ.get("REF_SWAP_IMPL") == "binding":
+        # the reference-side ctypes binding of INTEGRATION.md section 2
+        import sys
+        sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "integration"))
+        import mlower_b200
+        bound = mlower_b200.make_execute(reference_execute)
+
+        def execute(plan, x):
+            out = bound(plan, x)
+            STATS["gpu_executes"] = mlower_b200.STATS["b200"]
+            STATS["interpreted"] = mlower_b200.STATS["interpreted"]
+            return out
+        _install(execute, reference_execute, config)
+        return
 
     def execute(plan, x):
         try:
@@ -46,6 +60,13 @@ def pytest_configure(config):
         STATS["gpu_executes"] += 1
         return out
 
+    _install(execute, reference_execute, config)
+
+
+def _install(execute, reference_execute, config):
+    import mlower.cli
+    import mlower.pipeline
+    import mlower.runtime
     execute.__wrapped__ = reference_execute
     for mod in (mlower.runtime, mlower.pipeline, mlower.cli):
         if getattr(mod, "execute", None) is reference_execute:

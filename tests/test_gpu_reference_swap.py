@@ -21,17 +21,22 @@ FILES = ["test_runtime.py", "test_acceptance.py", "test_cli.py", "test_passes.py
 
 
 @pytest.mark.skipif(not os.path.isdir(REF_TESTS), reason="reference not installed (tools/install_reference.sh)")
-def test_reference_suite_with_b200_executor(tmp_path):
+@pytest.mark.parametrize("impl", ["api", "binding"])
+def test_reference_suite_with_b200_executor(tmp_path, impl):
+    """impl "api": mlower.runtime.execute -> paper_2301_13441_b200.api.execute
+    (every plan family on the GPU); impl "binding": the reference-side ctypes
+    binding of INTEGRATION.md section 2 (integration/mlower_b200.py: forest
+    plans on the GPU, the rest interpreted)."""
     report = tmp_path / "swap.json"
     env = dict(os.environ, PYTHONPATH=os.pathsep.join([REF, REF_TESTS, os.path.join(ROOT, "tests"), ROOT]),
-               REF_SWAP_REPORT=str(report), PYTHONHASHSEED="0")
+               REF_SWAP_REPORT=str(report), PYTHONHASHSEED="0", REF_SWAP_IMPL=impl)
     cmd = [sys.executable, "-m", "pytest", "-q", "-p", "ref_swap_plugin", "-p", "no:cacheprovider",
            "--rootdir", REF_TESTS, *[os.path.join(REF_TESTS, f) for f in FILES]]
     r = subprocess.run(cmd, cwd=REF_TESTS, env=env, capture_output=True, text=True, timeout=3000)
     tail = "\n".join(r.stdout.splitlines()[-40:])
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    with open(os.path.join(ROOT, "gpurun_out", "ref_swap.log"), "w") as fh:
+    with open(os.path.join(ROOT, "gpurun_out", f"ref_swap_{impl}.log"), "w") as fh:
         fh.write(r.stdout + "\n----\n" + r.stderr)
     stats = json.loads(report.read_text())
-    assert stats["gpu_executes"] > 1000, (stats, tail)
+    assert stats["gpu_executes"] > (1000 if impl == "api" else 300), (stats, tail)
     assert r.returncode == 0, tail
