@@ -26,12 +26,12 @@ extern "C" {
 
 enum cmlb_status {
   CMLB_OK = 0,
-  CMLB_E_VALIDATION = 1,   /* ValidationError        errors.py:21-24 */
-  CMLB_E_SHAPE = 2,        /* ShapeMismatch          errors.py:35-36 */
-  CMLB_E_INDEX = 3,        /* IndexOutOfBounds       errors.py:55-56 */
-  CMLB_E_OVERFLOW = 4,     /* AccumulatorOverflowRisk errors.py:59-60 */
-  CMLB_E_UNRESOLVED = 5,   /* UnresolvedKernel       errors.py:71-72 */
-  CMLB_E_INPUT = 6,        /* InputMismatch          errors.py:79-80 */
+  CMLB_E_VALIDATION = 1,   /* ValidationError        errors.py:22-25 */
+  CMLB_E_SHAPE = 2,        /* ShapeMismatch          errors.py:36-38 */
+  CMLB_E_INDEX = 3,        /* IndexOutOfBounds       errors.py:56-58 */
+  CMLB_E_OVERFLOW = 4,     /* AccumulatorOverflowRisk errors.py:60-62 */
+  CMLB_E_UNRESOLVED = 5,   /* UnresolvedKernel       errors.py:72-74 */
+  CMLB_E_INPUT = 6,        /* InputMismatch          errors.py:80-82 */
   CMLB_E_DEVICE = 7        /* CUDA failure (no reference analogue) */
 };
 

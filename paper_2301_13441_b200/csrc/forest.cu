@@ -154,6 +154,10 @@ struct ForestArgs {
   // ptxas keeps those steps as IMAD on the FMA pipe instead of strength-reducing
   // them to shifts/adds on the ALU pipe (which bound the walk, ncu alu 65%)
   uint32_t k1, k2, k128, k2p29, kexp;
+  // SKEW: ranks precomputed by forest_rank_kernel, [tile][F][rank_rows] u16 in
+  // the walk's interleaved row order (nullptr: the walk ranks its own tile)
+  uint16_t* ranks;
+  int rank_rows;
 };
 
 constexpr int NT = 256;  // threads per CTA for every forest kernel
@@ -652,10 +656,10 @@ __device__ __forceinline__ void load_payload(const float* p, float (&v)[CT]) {
 // buffer f&1 of the staging area (inside the tree-chunk region) while the CTA
 // searches feature f-1's buffer (double buffering: one barrier per feature).
 // Row values are read eight features at a time.
-template <int NTT, int RPT>
+template <int NTT, int RPT, bool GOUT = false>
 __device__ __forceinline__ void rank_tile(const ForestArgs& a, uint8_t* smem, uint8_t* chunk, uint64_t* stage_bar,
                                           const int64_t (&rowk)[RPT], const uint32_t (&pb)[RPT],
-                                          const int (&nbad)[RPT]) {
+                                          const int (&nbad)[RPT], const int64_t* gidx = nullptr) {
   constexpr int ROWS = NTT * RPT;
   const int tid = threadIdx.x;
   const int F = a.F;
@@ -724,10 +728,19 @@ __device__ __forceinline__ void rank_tile(const ForestArgs& a, uint8_t* smem, ui
         const float* fb = stage_f(f & 1);
         const uint16_t* mb = reinterpret_cast<const uint16_t*>(fb + cap);
         const int nf = __ldg(a.unf + f);
-        uint8_t* xrow = reinterpret_cast<uint8_t*>(xr) + (size_t)f * ROWS * 2;
+        if constexpr (GOUT) {  // rank kernel: straight into the walk tiles in global memory
+          int r[RPT];
 #pragma unroll
-        for (int k = 0; k < RPT; ++k)
-          *reinterpret_cast<uint16_t*>(xrow + pb[k]) = (uint16_t)count_less_eyt(fb, mb, nf, xv[k][j]);
+          for (int k = 0; k < RPT; ++k) r[k] = count_less_eyt(fb, mb, nf, xv[k][j]);
+#pragma unroll
+          for (int k = 0; k < RPT; ++k)
+            if (rowk[k] < a.n_rows) a.ranks[gidx[k] + (int64_t)f * a.rank_rows] = (uint16_t)r[k];
+        } else {
+          uint8_t* xrow = reinterpret_cast<uint8_t*>(xr) + (size_t)f * ROWS * 2;
+#pragma unroll
+          for (int k = 0; k < RPT; ++k)
+            *reinterpret_cast<uint16_t*>(xrow + pb[k]) = (uint16_t)count_less_eyt(fb, mb, nf, xv[k][j]);
+        }
       }
     }
   }
@@ -936,6 +949,46 @@ __global__ void __launch_bounds__(NTT, 1) forest_ranked_kernel(const ForestArgs 
 // below 2^(53-q), so every float64 partial sum in ANY order is exact and equals
 // numpy's sequential or pairwise result bit for bit).  Padding trees of the
 // last group go always-left onto a zero payload (+0.0 changes no exact sum).
+// Ranking as its own pass (SKEW variant).  Fused into the walk, the per-CTA
+// ranking (stage each feature's thresholds, search every row) ran once per
+// 512-row tile and took ~30% of the walk kernel's warp time (ncu stall samples,
+// profiles/r2_skew_v4_ncu_summary.json); here a CTA ranks 2,048 rows per
+// staged feature, 4 independent searches per thread, and writes the u16 ranks
+// straight into the walk tiles' interleaved layout, which the walk then
+// bulk-copies (28 KB per 512-row tile for F = 28).
+constexpr int RANK_THREADS = 512, RANK_RPT = 4;
+__global__ void __launch_bounds__(RANK_THREADS) forest_rank_kernel(const ForestArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ __align__(8) uint64_t stage_bar[2];
+  constexpr int RPT = RANK_RPT, ROWS = RANK_THREADS * RANK_RPT;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(&stage_bar[0], 1);
+    mbar_init(&stage_bar[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int WR = a.rank_rows;
+  int64_t rowk[RPT], gidx[RPT];
+  uint32_t pb[RPT];
+  int nbad[RPT];
+#pragma unroll
+  for (int k = 0; k < RPT; ++k) {
+    rowk[k] = (int64_t)blockIdx.x * ROWS + tid + k * RANK_THREADS;
+    const int r = (int)(rowk[k] % WR);
+    gidx[k] = rowk[k] / WR * (int64_t)a.F * WR + (((r >> 6) << 6) | ((r & 31) << 1) | ((r >> 5) & 1));
+    pb[k] = 0;
+    nbad[k] = 0;
+    if (a.dense_sel && rowk[k] < a.n_rows) {
+      const float* src = a.x + rowk[k] * a.ldx;
+      for (int f = 0; f < a.F; ++f) nbad[k] += !isfinite(load_col(a.pro, src, f));
+    }
+  }
+  ForestArgs ar = a;
+  ar.stage_off = 0;  // staging buffers at the start of this kernel's shared memory
+  rank_tile<RANK_THREADS, RPT, true>(ar, smem, smem, stage_bar, rowk, pb, nbad, gidx);
+}
+
 template <int CT, int NTT, int RPT, int TI, int DT>
 __global__ void __launch_bounds__(NTT, 1) forest_skew_kernel(const ForestArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -997,7 +1050,18 @@ __global__ void __launch_bounds__(NTT, 1) forest_skew_kernel(const ForestArgs a)
       for (int f = 0; f < F; ++f) nbad[k] += !isfinite(load_col(a.pro, src, f));
     }
   }
-  rank_tile<NTT, RPT>(a, smem, chunk, stage_bar, rowk, pb, nbad);
+  if (a.ranks) {  // ranks precomputed (forest_rank_kernel): one bulk copy of this tile
+    if (tid == 0) {
+      const uint32_t bytes = (uint32_t)F * ROWS * 2u;
+      const uint8_t* src = reinterpret_cast<const uint8_t*>(a.ranks + (int64_t)blockIdx.x * F * ROWS);
+      fence_proxy_async();
+      mbar_expect_tx(&stage_bar[0], bytes);
+      for (uint32_t off = 0; off < bytes; off += 32768u) bulk_g2s(smem + off, src + off, min(32768u, bytes - off), &stage_bar[0]);
+    }
+    mbar_wait(&stage_bar[0], 0);
+  } else {
+    rank_tile<NTT, RPT>(a, smem, chunk, stage_bar, rowk, pb, nbad);
+  }
 
   double acc[RPT][CT];
 #pragma unroll
@@ -1403,6 +1467,7 @@ struct cmlb_forest {
   int32_t* moff = nullptr;
   int32_t* unf = nullptr;
   int ntt = 256, stage_cap = 0, node_off_bytes = 0, rcfg = 0, stage_off = 0, stage_bufs = 2;
+  size_t rank_smem = 0;  // SKEW: forest_rank_kernel's two staging buffers
   int mma_k = 0, mma_n = 0, mma_feat_off = 0, mma_thr_off = 0, mma_pay_off = 0;
   cmlb_column_op* pro = nullptr;  // fused preprocessing
   int n_inputs = 0;
@@ -2069,6 +2134,10 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
   KernelFn k = kernel_for(*f);
   if (!k) return fail(CMLB_E_UNRESOLVED, "no kernel instantiation for this forest shape");
   CMLB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f->smem));
+  if (f->variant == CMLB_FOREST_SKEW) {
+    f->rank_smem = 2 * (size_t)f->stage_cap * 6;
+    CMLB_CUDA(cudaFuncSetAttribute(forest_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f->rank_smem));
+  }
   *out = f.release();
   return CMLB_OK;
 }
@@ -2105,9 +2174,32 @@ static int run_forest(const cmlb_forest* f, const float* x, int64_t n_rows, int6
   const int64_t rows = f->variant == CMLB_FOREST_MMA ? (int64_t)MMA_M : (int64_t)threads * f->rpt;
   const int64_t grid = ceil_div(n_rows, rows);
   if (grid > 0x7fffffff) return fail(CMLB_E_INPUT, "too many rows for one launch");
-  k<<<(unsigned)grid, threads, f->smem, (cudaStream_t)stream>>>(a);
+  cudaStream_t s = (cudaStream_t)stream;
+  void* ranks = nullptr;
+  if (f->variant == CMLB_FOREST_SKEW) {
+    // rank pass first (forest_rank_kernel), into stream-ordered scratch laid
+    // out as the walk's tiles; freed in stream order after the walk
+    keep_pool(f->device);
+    const size_t bytes = (size_t)grid * f->F * rows * sizeof(uint16_t);
+    CMLB_CUDA(cudaMallocAsync(&ranks, bytes, s));
+    a.ranks = static_cast<uint16_t*>(ranks);
+    a.rank_rows = (int)rows;
+    ForestArgs ra = a;
+    ra.stage_bufs = 2;
+    const int64_t rgrid = ceil_div(n_rows, (int64_t)RANK_THREADS * RANK_RPT);
+    forest_rank_kernel<<<(unsigned)rgrid, RANK_THREADS, f->rank_smem, s>>>(ra);
+    note_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      cudaFreeAsync(ranks, s);
+      return cuda_fail(e, "forest_rank_kernel");
+    }
+  }
+  k<<<(unsigned)grid, threads, f->smem, s>>>(a);
   note_launch();
-  CMLB_CUDA(cudaGetLastError());
+  cudaError_t e = cudaGetLastError();
+  if (ranks) cudaFreeAsync(ranks, s);
+  if (e != cudaSuccess) return cuda_fail(e, "forest kernel");
   return CMLB_OK;
 }
 

@@ -320,6 +320,10 @@ __global__ void __launch_bounds__(THREADS, 1) svm_tc_kernel(const Args a) {
     double dec[MAXC * (MAXC - 1) / 2];
     for (int p = 0; p < a.pairs; ++p) dec[p] = 0.0;
     float err_sum = 0.0f, err_sq = 0.0f;
+    // per-class share of the bound: pair (i, k) only sums SVs of classes i and k
+    // (libsvm one-vs-one), so its tolerance is 4 (errc[i] + errc[k]), not 4 E
+    float errc[MAXC], err_flushed = 0.0f;
+    for (int c = 0; c < MAXC; ++c) errc[c] = 0.0f;
     int cur = -1;
     const bool rbf = a.kernel == CMLB_SVM_RBF;
     const float neg_gl2 = -a.gamma * 1.4426950408889634f;
@@ -383,6 +387,8 @@ __global__ void __launch_bounds__(THREADS, 1) svm_tc_kernel(const Args a) {
               if (c != cur) {  // uniform: classes are contiguous
                 fold();
                 flush<CP>(a, cur, acc, dec);
+                if (cur >= 0) errc[cur] += err_sum - err_flushed;
+                err_flushed = err_sum;
 #pragma unroll
                 for (int o = 0; o < CP; ++o) acc[o] = 0.0;
                 cur = c;
@@ -404,20 +410,24 @@ __global__ void __launch_bounds__(THREADS, 1) svm_tc_kernel(const Args a) {
       bar_arrive(&tempty_bar[b]);
     }
     flush<CP>(a, cur, acc, dec);
+    if (cur >= 0) errc[cur] += err_sum - err_flushed;
     // combine the two column halves of each row: half 1 hands its sums over
     float* xch = reinterpret_cast<float*>(smem);  // the stages are idle now
     double* xd = reinterpret_cast<double*>(xch);
     named_bar_sync(1, EPI_THREADS);               // every epilogue thread is past its last tile
-    const int stride = a.pairs + 1;
+    const int nc = a.is_svr ? 0 : a.C;
+    const int stride = a.pairs + 1 + nc;
     if (half == 1) {
       for (int p = 0; p < a.pairs; ++p) xd[r * stride + p] = dec[p];
       xd[r * stride + a.pairs] = (double)err_sum;
+      for (int c = 0; c < nc; ++c) xd[r * stride + a.pairs + 1 + c] = (double)errc[c];
       xch[2 * BM * stride + r] = err_sq;
     }
     named_bar_sync(1, EPI_THREADS);
     if (half == 1) return;
     for (int p = 0; p < a.pairs; ++p) dec[p] += xd[r * stride + p];
     err_sum += (float)xd[r * stride + a.pairs];
+    for (int c = 0; c < nc; ++c) errc[c] += (float)xd[r * stride + a.pairs + 1 + c];
     err_sq += xch[2 * BM * stride + r];
     if (valid) {
       // b_j = per-SV error bound and E = sum b_j: the deterministic bound
@@ -449,7 +459,8 @@ __global__ void __launch_bounds__(THREADS, 1) svm_tc_kernel(const Args a) {
           for (int j = i + 1; j < a.C; ++j, ++p) {
             const double v = dec[p] + (double)a.intercept[p];
             dec[p] = v;
-            exact = exact || !(fabs(v) > (double)tol);
+            const float tol_p = a.prob_tol ? tol : 4.0f * (errc[i] + errc[j]) + 1e-30f;
+            exact = exact || !(fabs(v) > (double)tol_p);
             if (v > 0) ++vote[i]; else ++vote[j];
           }
         }

@@ -76,7 +76,6 @@ _STATUS = {
     5: "UnresolvedKernel",
     6: "InputMismatch",
     7: "DeviceError",
-    8: "DivisionByZero",
 }
 
 

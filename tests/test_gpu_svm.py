@@ -119,3 +119,28 @@ def test_svm_zero_rows():
     case = gc.ext_get("svc4_rbf")
     y, dec, n_exact = run_svm(case.model, case.x[:0])
     assert y.shape == (0, 1) and n_exact == 0
+
+
+def test_config4b_fitted_svc_65536_rows_against_libsvm_oracle():
+    """Config 4b at its own shape: the fitted sklearn SVC (9,626 SVs, 784
+    features, 10 classes; bench_assets/svc_digits.npz) on 65,536 rows of its
+    input distribution: every class equals the libsvm-order C oracle, and the
+    rows the fast path decided stay within the certified tolerance."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    from bench_configs import svc_inputs, svc_model
+    m = svc_model()
+    x = svc_inputs(torch.device("cuda"), 7, 65_536)
+    compiled = api.compile_model(m)
+    prog = compiled.program(0)
+    st = prog.stages[0]
+    n = x.shape[0]
+    y = torch.empty((n, 1), dtype=TORCH_DTYPE[st.spec.out_dtype], device="cuda")
+    ex = torch.zeros(1, dtype=torch.int32, device="cuda")
+    st.run(x, y, n, 784, torch.cuda.current_stream().cuda_stream, exact_rows=ex)
+    _, vote = ext.svm_decision(m, x.cpu().numpy())
+    want = np.asarray(m.classes, np.float64)[vote]
+    got = y.cpu().numpy().astype(np.float64).ravel()
+    bad = np.flatnonzero(got != want)
+    assert bad.size == 0, f"{bad.size} of {n} classes differ (exact-path rows {int(ex.item())})"
