@@ -807,9 +807,19 @@ __global__ void __launch_bounds__(NTT, 1) forest_ranked_kernel(const ForestArgs 
     }
   }
 
-  rank_tile<NTT, RPT>(a, smem, chunk, stage_bar, rowk, pb, nbad);
-
-  RowAcc<CT, PW> acc[RPT];
+    if (a.ranks) {  // ranks precomputed (forest_rank_kernel): one bulk copy of this tile
+    if (tid == 0) {
+      const uint32_t bytes = (uint32_t)F * ROWS * 2u;
+      const uint8_t* src = reinterpret_cast<const uint8_t*>(a.ranks + (int64_t)blockIdx.x * F * ROWS);
+      fence_proxy_async();
+      mbar_expect_tx(&stage_bar[0], bytes);
+      for (uint32_t off = 0; off < bytes; off += 32768u) bulk_g2s(smem + off, src + off, min(32768u, bytes - off), &stage_bar[0]);
+    }
+    mbar_wait(&stage_bar[0], 0);
+  } else {
+    rank_tile<NTT, RPT>(a, smem, chunk, stage_bar, rowk, pb, nbad);
+  }
+ RowAcc<CT, PW> acc[RPT];
   double pw_stack[PW ? RPT : 1][PW ? SMAX : 1];
 #pragma unroll
   for (int k = 0; k < RPT; ++k) {
@@ -1467,7 +1477,8 @@ struct cmlb_forest {
   int32_t* moff = nullptr;
   int32_t* unf = nullptr;
   int ntt = 256, stage_cap = 0, node_off_bytes = 0, rcfg = 0, stage_off = 0, stage_bufs = 2;
-  size_t rank_smem = 0;  // SKEW: forest_rank_kernel's two staging buffers
+  size_t rank_smem = 0;  // SKEW / RANKED: forest_rank_kernel's two staging buffers
+  bool rank_pass = true; // RANKED: rank in a separate pass (CMLB_RANK_PASS=0: fused per tile)
   int mma_k = 0, mma_n = 0, mma_feat_off = 0, mma_thr_off = 0, mma_pay_off = 0;
   cmlb_column_op* pro = nullptr;  // fused preprocessing
   int n_inputs = 0;
@@ -1958,7 +1969,9 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
     s_gbytes = s_node_off + ni_r * 32 * 4;
     size_t max_nf = 0;
     for (auto& u : U) max_nf = std::max(max_nf, u.size());
-    std::vector<int> order = {0, 1, 2, 3, 4};
+    // measured on B200, RF500 d8 10M rows: 512x1x16 672M, 512x1x8 656M,
+    // 256x2x8 656M rows/s (profiles/r2_tuning/skew_cfgs.jsonl)
+    std::vector<int> order = {1, 0, 3, 2, 4};
     if (const char* env = getenv("CMLB_SKEW_CFG")) order = {atoi(env)};
     bool found = false;
     for (size_t oi = 0; oi < order.size() && !found; ++oi) {
@@ -2134,7 +2147,11 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
   KernelFn k = kernel_for(*f);
   if (!k) return fail(CMLB_E_UNRESOLVED, "no kernel instantiation for this forest shape");
   CMLB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f->smem));
-  if (f->variant == CMLB_FOREST_SKEW) {
+  if (f->variant == CMLB_FOREST_RANKED) {
+    const char* rp = getenv("CMLB_RANK_PASS");
+    f->rank_pass = !(rp && atoi(rp) == 0) && 2 * (size_t)f->stage_cap * 6 <= SMEM_LIMIT;
+  }
+  if (f->variant == CMLB_FOREST_SKEW || (f->variant == CMLB_FOREST_RANKED && f->rank_pass)) {
     f->rank_smem = 2 * (size_t)f->stage_cap * 6;
     CMLB_CUDA(cudaFuncSetAttribute(forest_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f->rank_smem));
   }
@@ -2176,7 +2193,7 @@ static int run_forest(const cmlb_forest* f, const float* x, int64_t n_rows, int6
   if (grid > 0x7fffffff) return fail(CMLB_E_INPUT, "too many rows for one launch");
   cudaStream_t s = (cudaStream_t)stream;
   void* ranks = nullptr;
-  if (f->variant == CMLB_FOREST_SKEW) {
+  if (f->variant == CMLB_FOREST_SKEW || (f->variant == CMLB_FOREST_RANKED && f->rank_pass)) {
     // rank pass first (forest_rank_kernel), into stream-ordered scratch laid
     // out as the walk's tiles; freed in stream order after the walk
     keep_pool(f->device);

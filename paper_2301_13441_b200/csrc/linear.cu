@@ -659,6 +659,17 @@ __device__ __forceinline__ void stage_w_kmajor(T* dst, int ldw, const float* w, 
   }
 }
 
+// a0 = fma(x, w0, a0), a1 = fma(x, w1, a1) as one FFMA2 (sm_100 packed fp32;
+// ptxas folds the packing moves and the broadcast of x into the operands)
+__device__ __forceinline__ void ffma2(float& a0, float& a1, float x, float w0, float w1) {
+  unsigned long long xp, wp, ap, rp;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(xp) : "f"(x));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(wp) : "f"(w0), "f"(w1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(ap) : "f"(a0), "f"(a1));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(rp) : "l"(xp), "l"(wp), "l"(ap));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(rp));
+}
+
 template <int KC>
 __device__ __forceinline__ int lt_swz(int r, int p) {
   if constexpr (KC == 32) return p ^ (r & 7);        // 128-byte rows
@@ -767,10 +778,12 @@ __global__ void __launch_bounds__(NT, 1) linear_tile_kernel(const LinearArgs a) 
           const float4 w = w4[c4];
 #pragma unroll
           for (int q = 0; q < RPT; ++q) {
-            if (4 * c4 + 0 < CM) acc[q][4 * c4 + 0] = fmaf(xv[q], w.x, acc[q][4 * c4 + 0]);
-            if (4 * c4 + 1 < CM) acc[q][4 * c4 + 1] = fmaf(xv[q], w.y, acc[q][4 * c4 + 1]);
-            if (4 * c4 + 2 < CM) acc[q][4 * c4 + 2] = fmaf(xv[q], w.z, acc[q][4 * c4 + 2]);
-            if (4 * c4 + 3 < CM) acc[q][4 * c4 + 3] = fmaf(xv[q], w.w, acc[q][4 * c4 + 3]);
+            // two outputs per FFMA2 (x broadcast): the same IEEE fma chains,
+            // half the FMA-pipe instructions
+            if (4 * c4 + 1 < CM) ffma2(acc[q][4 * c4 + 0], acc[q][4 * c4 + 1], xv[q], w.x, w.y);
+            else if (4 * c4 + 0 < CM) acc[q][4 * c4 + 0] = fmaf(xv[q], w.x, acc[q][4 * c4 + 0]);
+            if (4 * c4 + 3 < CM) ffma2(acc[q][4 * c4 + 2], acc[q][4 * c4 + 3], xv[q], w.z, w.w);
+            else if (4 * c4 + 2 < CM) acc[q][4 * c4 + 2] = fmaf(xv[q], w.z, acc[q][4 * c4 + 2]);
           }
         }
       }

@@ -62,7 +62,8 @@ __global__ void __launch_bounds__(THREADS, 1) smem_rate(unsigned long long* cycl
   if (acc == 0x12345678u) sink[0] = acc;
 }
 
-// MODE 0: DADD, 1: DFMA, 2: F2F.F64.F32 (+ a cheap FADD to vary the source), 3: FFMA (reference)
+// MODE 0: DADD, 1: DFMA, 2: F2F.F64.F32 (+ a cheap FADD to vary the source), 3: FFMA with
+// immediate operands, 4: FFMA with register operands, 5: FFMA2 (packed fp32x2) register form
 template <int MODE>
 __global__ void __launch_bounds__(THREADS, 1) fp_rate(unsigned long long* cycles, double* sink, float seed) {
   double d[UNROLL];
@@ -77,7 +78,15 @@ __global__ void __launch_bounds__(THREADS, 1) fp_rate(unsigned long long* cycles
       if (MODE == 0) d[u] = d[u] + 1.0000001;
       else if (MODE == 1) d[u] = fma(d[u], 0.9999999, 1e-9);
       else if (MODE == 2) d[u] += (double)__int_as_float(0x3f800000 | ((it * UNROLL + u) & 0x7fffff));
-      else f[u] = fmaf(f[u], 0.9999999f, 1e-9f);
+      else if (MODE == 3) f[u] = fmaf(f[u], 0.9999999f, 1e-9f);
+      else if (MODE == 4) f[u] = fmaf(f[u], f[(u + 1) % UNROLL], f[(u + 3) % UNROLL]);
+      else {
+        unsigned long long a, b, r;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "f"(f[u]), "f"(f[(u + 1) % UNROLL]));
+        asm("mov.b64 %0, {%1, %2};" : "=l"(b) : "f"(f[(u + 2) % UNROLL]), "f"(f[(u + 5) % UNROLL]));
+        asm("fma.rn.f32x2 %0, %1, %2, %1;" : "=l"(r) : "l"(a), "l"(b));
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(f[u]), "=f"(f[(u + 1) % UNROLL]) : "l"(r));
+      }
     }
   }
   __syncthreads();
@@ -122,6 +131,8 @@ int main() {
   const double dfma = per_sm_clk(fp_rate<1>, sms, thread_ops, dsink, 1.0f);
   const double f2f = per_sm_clk(fp_rate<2>, sms, thread_ops, dsink, 1.0f);
   const double ffma = per_sm_clk(fp_rate<3>, sms, thread_ops, dsink, 1.0f);
+  const double ffma_reg = per_sm_clk(fp_rate<4>, sms, thread_ops, dsink, 1.0f);
+  const double ffma2 = per_sm_clk(fp_rate<5>, sms, thread_ops, dsink, 1.0f);  // instructions (2 FMAs each)
   int clk_khz = 0;
   cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev);
   printf("{\"gpu\": \"%s\", \"sms\": %d, \"sm_clock_attr_mhz\": %.0f,\n", p.name, sms, clk_khz / 1e3);
@@ -130,7 +141,8 @@ int main() {
   printf(" \"smem_lds64_conflict_free_warp_instr_per_sm_clk\": %.4f,\n", v2);
   printf(" \"smem_lds32_random256_warp_instr_per_sm_clk\": %.4f,\n", rnd);
   printf(" \"dadd_per_sm_clk\": %.2f, \"dfma_per_sm_clk\": %.2f, \"f2f_f64_f32_plus_dadd_per_sm_clk\": %.2f, "
-         "\"ffma_per_sm_clk\": %.2f,\n", dadd, dfma, f2f, ffma);
+         "\"ffma_per_sm_clk\": %.2f, \"ffma_reg_per_sm_clk\": %.2f, \"ffma2_instr_per_sm_clk\": %.2f,\n",
+         dadd, dfma, f2f, ffma, ffma_reg, ffma2);
   printf(" \"fp64_fma_tflops_at_max_clock\": %.2f}\n", dfma * 2 * sms * 1965e6 / 1e12);
   return cudaDeviceSynchronize() != cudaSuccess;
 }
