@@ -520,11 +520,29 @@ __global__ void __launch_bounds__(NT) forest_kernel(const ForestArgs a) {
 // bank-conflict-free across a warp (a power-of-two binary search over a
 // sorted array sends every lane of a step to the same bank).  The final
 // position is the lower_bound element, mapped back to its sorted index.
-__device__ __forceinline__ int count_less_eyt(const float* ue, const uint16_t* map, int n, float x) {
-  int k = 1;
-  while (k <= n) k = 2 * k + (ue[k - 1] < x ? 1 : 0);
-  k >>= __ffs(~k);
-  return k ? (int)map[k - 1] : n;
+// R searches of one table interleaved (a fixed trip count instead of the
+// data-dependent while loop, so the R dependent load chains overlap).  The
+// implicit tree of n nodes has L = floor(log2 n) + 1 levels, all full but the
+// last: L - 1 unconditional steps, then one step where the node exists.
+template <int R>
+__device__ __forceinline__ void count_less_eyt_n(const float* ue, const uint16_t* map, int n, const float (&x)[R],
+                                                 int (&out)[R]) {
+  const int levels = n > 0 ? 32 - __clz(n) : 0;
+  uint32_t k[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) k[r] = 1u;
+  for (int l = 0; l + 1 < levels; ++l) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) k[r] = 2u * k[r] + (ue[k[r] - 1] < x[r] ? 1u : 0u);
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if ((int)k[r] <= n) k[r] = 2u * k[r] + (ue[k[r] - 1] < x[r] ? 1u : 0u);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const uint32_t kk = k[r] >> __ffs(~k[r]);
+    out[r] = kk ? (int)map[kk - 1] : n;
+  }
 }
 
 __device__ __forceinline__ void cp_async4(void* smem_dst, const void* gmem_src) {
@@ -728,18 +746,19 @@ __device__ __forceinline__ void rank_tile(const ForestArgs& a, uint8_t* smem, ui
         const float* fb = stage_f(f & 1);
         const uint16_t* mb = reinterpret_cast<const uint16_t*>(fb + cap);
         const int nf = __ldg(a.unf + f);
-        if constexpr (GOUT) {  // rank kernel: straight into the walk tiles in global memory
-          int r[RPT];
+        float xq[RPT];
+        int r[RPT];
 #pragma unroll
-          for (int k = 0; k < RPT; ++k) r[k] = count_less_eyt(fb, mb, nf, xv[k][j]);
+        for (int k = 0; k < RPT; ++k) xq[k] = xv[k][j];
+        count_less_eyt_n<RPT>(fb, mb, nf, xq, r);
+        if constexpr (GOUT) {  // rank kernel: straight into the walk tiles in global memory
 #pragma unroll
           for (int k = 0; k < RPT; ++k)
             if (rowk[k] < a.n_rows) a.ranks[gidx[k] + (int64_t)f * a.rank_rows] = (uint16_t)r[k];
         } else {
           uint8_t* xrow = reinterpret_cast<uint8_t*>(xr) + (size_t)f * ROWS * 2;
 #pragma unroll
-          for (int k = 0; k < RPT; ++k)
-            *reinterpret_cast<uint16_t*>(xrow + pb[k]) = (uint16_t)count_less_eyt(fb, mb, nf, xv[k][j]);
+          for (int k = 0; k < RPT; ++k) *reinterpret_cast<uint16_t*>(xrow + pb[k]) = (uint16_t)r[k];
         }
       }
     }

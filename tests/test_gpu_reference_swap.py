@@ -40,7 +40,7 @@ def test_reference_suite_with_b200_executor(tmp_path, impl):
     cmd = [sys.executable, "-m", "pytest", "-q", "-p", "ref_swap_plugin", "-p", "no:cacheprovider",
            "--rootdir", REF_TESTS, *[os.path.join(REF_TESTS, f) for f in FILES]]
     if impl == "api":
-        cmd += [f"--deselect={os.path.join(REF_TESTS, t)}" for t in HAND_BUILT]
+        cmd += ["-k", " and ".join(f"not {t.split('::')[1]}" for t in HAND_BUILT)]
     r = subprocess.run(cmd, cwd=REF_TESTS, env=env, capture_output=True, text=True, timeout=3000)
     tail = "\n".join(r.stdout.splitlines()[-40:])
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)

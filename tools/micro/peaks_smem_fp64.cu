@@ -67,9 +67,14 @@ __global__ void __launch_bounds__(THREADS, 1) smem_rate(unsigned long long* cycl
 template <int MODE>
 __global__ void __launch_bounds__(THREADS, 1) fp_rate(unsigned long long* cycles, double* sink, float seed) {
   double d[UNROLL];
-  float f[UNROLL];
+  float f[UNROLL], g[UNROLL], h[UNROLL];
 #pragma unroll
-  for (int u = 0; u < UNROLL; ++u) { d[u] = seed * (u + 1 + threadIdx.x); f[u] = seed + u; }
+  for (int u = 0; u < UNROLL; ++u) {
+    d[u] = seed * (u + 1 + threadIdx.x);
+    f[u] = seed + u;
+    g[u] = seed * 0.9999f - u * 1e-7f;
+    h[u] = seed * 1e-9f + u;
+  }
   __syncthreads();
   const long long t0 = clock64();
   for (int it = 0; it < ITERS; ++it) {
@@ -79,13 +84,13 @@ __global__ void __launch_bounds__(THREADS, 1) fp_rate(unsigned long long* cycles
       else if (MODE == 1) d[u] = fma(d[u], 0.9999999, 1e-9);
       else if (MODE == 2) d[u] += (double)__int_as_float(0x3f800000 | ((it * UNROLL + u) & 0x7fffff));
       else if (MODE == 3) f[u] = fmaf(f[u], 0.9999999f, 1e-9f);
-      else if (MODE == 4) f[u] = fmaf(f[u], f[(u + 1) % UNROLL], f[(u + 3) % UNROLL]);
-      else {
+      else if (MODE == 4) f[u] = fmaf(f[u], g[u], h[u]);  // independent chains, register operands
+      else {  // FFMA2: chains (f[u], h[u]) x (g[u], g[u]) + (f[u], h[u])
         unsigned long long a, b, r;
-        asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "f"(f[u]), "f"(f[(u + 1) % UNROLL]));
-        asm("mov.b64 %0, {%1, %2};" : "=l"(b) : "f"(f[(u + 2) % UNROLL]), "f"(f[(u + 5) % UNROLL]));
+        asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "f"(f[u]), "f"(h[u]));
+        asm("mov.b64 %0, {%1, %1};" : "=l"(b) : "f"(g[u]));
         asm("fma.rn.f32x2 %0, %1, %2, %1;" : "=l"(r) : "l"(a), "l"(b));
-        asm("mov.b64 {%0, %1}, %2;" : "=f"(f[u]), "=f"(f[(u + 1) % UNROLL]) : "l"(r));
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(f[u]), "=f"(h[u]) : "l"(r));
       }
     }
   }
@@ -94,7 +99,7 @@ __global__ void __launch_bounds__(THREADS, 1) fp_rate(unsigned long long* cycles
   if (threadIdx.x == 0) cycles[blockIdx.x] = (unsigned long long)(t1 - t0);
   double s = 0;
 #pragma unroll
-  for (int u = 0; u < UNROLL; ++u) s += d[u] + f[u];
+  for (int u = 0; u < UNROLL; ++u) s += d[u] + f[u] + h[u];
   if (s == 1.2345) sink[0] = s;
 }
 
@@ -132,7 +137,7 @@ int main() {
   const double f2f = per_sm_clk(fp_rate<2>, sms, thread_ops, dsink, 1.0f);
   const double ffma = per_sm_clk(fp_rate<3>, sms, thread_ops, dsink, 1.0f);
   const double ffma_reg = per_sm_clk(fp_rate<4>, sms, thread_ops, dsink, 1.0f);
-  const double ffma2 = per_sm_clk(fp_rate<5>, sms, thread_ops, dsink, 1.0f);  // instructions (2 FMAs each)
+  const double ffma2 = per_sm_clk(fp_rate<5>, sms, thread_ops, dsink, 1.0f);  // thread instructions (2 FMAs each)
   int clk_khz = 0;
   cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev);
   printf("{\"gpu\": \"%s\", \"sms\": %d, \"sm_clock_attr_mhz\": %.0f,\n", p.name, sms, clk_khz / 1e3);
