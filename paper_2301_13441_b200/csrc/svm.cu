@@ -90,8 +90,11 @@ struct Args {
   int prob_tol;            // opt-in (CMLB_SVM_TOL=hoeffding): probabilistic vote tolerance, NOT a guarantee
   int probe;               // debug: bit 0 skip X loads, bit 1 skip B copies, bit 2 skip epilogue math
   const cmlb_column_op* pro;  // fused preprocessing (nullable)
-  int32_t* queue;          // [n_rows] rows for the exact path
+  int32_t* queue;          // [n_rows] rows the fast path could not certify
   int32_t* queue_len;
+  const double* ns64;      // [n_sv] |sv|^2 in float64 (certifying tier)
+  int32_t* queue2;         // rows the float64 certifying tier could not decide -> libsvm-order exact path
+  int32_t* queue2_len;
 };
 
 __host__ __device__ inline int pair_index(int a, int b, int C) {  // a < b
@@ -569,6 +572,231 @@ __device__ double exact_k(const Args& a, const double* xs, const double* s) {
 
 constexpr int XTHREADS = 256;
 
+// ---------------------------------------------------------------------------
+// certifying tier: float64 Gram for the rows the fast path queued
+// ---------------------------------------------------------------------------
+//
+// The fast path's bound covers the split residuals and kernel-function
+// roundings, but the fp32 accumulation inside the tensor core is modeled, not
+// proved, and a worst-case fp32 bound would flag most rows.  The rows it
+// queues are therefore decided here with float64 arithmetic whose error is
+// bounded RIGOROUSLY against libsvm's own float64 computation:
+//   G = x.s as a sequential float64 FMA chain (|err| <= gamma_F sum|x_k s_k|
+//   <= gamma_F sqrt(nx ns)), d2 = nx + ns - 2G, K = kernel(d2 or G), then the
+//   decision sums in libsvm's order (class-i block, class-k block, - rho).
+//   libsvm computes the same decision with its own float64 roundings; both
+//   differ from the exact value by at most the standard gamma_n bounds, so
+//   |dec_ours - dec_libsvm| <= tol2 = sum|w_j| errK_j + 2 gamma_{n+2} (sum|w_j K_j| + |rho|)
+//   and a pair with |dec_ours| > tol2 votes exactly as libsvm does.
+// Rows with any pair inside tol2 (or a non-finite feature) go on to the
+// libsvm-order exact kernel.  Tile: 64 rows x 64 SVs per CTA step, 4 x 4
+// outputs per thread, K staged in 32-feature float64 chunks (double-buffered);
+// decision sums per (row, pair) task in ascending SV order (deterministic).
+constexpr int CB_ROWS = 64, CB_SV = 64, CB_K = 16, CB_THREADS = 256;
+constexpr int CB_KS = CB_K + 1, CB_SS = CB_SV + 1;              // padded strides (bank-conflict-free)
+constexpr int CB_TPT = 12;                                        // (row, pair) tasks per thread: pairs <= 48
+constexpr int CB_MAXP = CB_TPT * CB_THREADS / CB_ROWS;
+constexpr size_t CB_SMEM = (size_t)2 * (CB_ROWS + CB_SV) * CB_KS * 8 + (size_t)2 * CB_ROWS * CB_SS * 8 + CB_ROWS * 8;
+
+__device__ __forceinline__ double gamma_n(int n) {
+  const double nu = n * 1.1102230246251565e-16;  // n * 2^-53
+  return nu / (1.0 - nu);
+}
+
+__global__ void __launch_bounds__(CB_THREADS, 2) svm_certify_kernel(const Args a, const int* n_sv_start) {
+  extern __shared__ __align__(16) uint8_t csm[];
+  double* xc = reinterpret_cast<double*>(csm);                  // [2][CB_ROWS][CB_KS]
+  double* sc = xc + 2 * CB_ROWS * CB_KS;                          // [2][CB_SV][CB_KS]
+  double* ks = sc + 2 * CB_SV * CB_KS;                            // [CB_ROWS][CB_SS] kernel values
+  double* eks = ks + CB_ROWS * CB_SS;                              // [CB_ROWS][CB_SS] |K_ours - K_libsvm| bounds
+  double* nxs = eks + CB_ROWS * CB_SS;                             // [CB_ROWS] |x|^2
+  __shared__ int32_t rows[CB_ROWS];
+  __shared__ int undecided[CB_ROWS];
+  const int tid = threadIdx.x;
+  const int nq = *a.queue_len;
+  const int F = a.F, C = a.C;
+  const int npairs = a.is_svr ? 1 : a.pairs;
+  const int ntasks = CB_ROWS * npairs;
+  const int tr = tid / 16, ts = tid % 16;                          // 4 rows x 4 SVs: rows tr + 16 i, SVs ts + 16 j
+  const double gF = gamma_n(F + 3);
+  constexpr double U = 1.1102230246251565e-16;
+  for (int b0 = blockIdx.x * CB_ROWS; b0 < nq; b0 += gridDim.x * CB_ROWS) {
+    const int nb = min(CB_ROWS, nq - b0);
+    if (tid < CB_ROWS) rows[tid] = tid < nb ? a.queue[b0 + tid] : -1;
+    __syncthreads();
+    if (tid < CB_ROWS) {  // |x|^2 in float64 and the non-finite check
+      double sacc = 0.0;
+      int nf = 0;
+      if (rows[tid] >= 0) {
+        const float* src = a.x + (int64_t)rows[tid] * a.ldx;
+        for (int k = 0; k < F; ++k) {
+          const double v = (double)load_col(a.pro, src, k);
+          nf |= !isfinite(v);
+          sacc = fma(v, v, sacc);
+        }
+      }
+      nxs[tid] = sacc;
+      undecided[tid] = nf;
+    }
+    double dsum[CB_TPT], esum[CB_TPT];
+    float asum[CB_TPT];  // sum |w K|, rounded up (an upper bound is all the certificate needs)
+#pragma unroll
+    for (int q = 0; q < CB_TPT; ++q) dsum[q] = esum[q] = 0.0, asum[q] = 0.0f;
+    __syncthreads();
+    const int nkc = (F + CB_K - 1) / CB_K;
+    for (int j0 = 0; j0 < a.n_sv; j0 += CB_SV) {
+      const int nj = min(CB_SV, a.n_sv - j0);
+      double g[4][4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) g[i][j] = 0.0;
+      auto stage = [&](int kc, int buf) {
+        const int k0 = kc * CB_K;
+        double* xb = xc + buf * CB_ROWS * CB_KS;
+        double* sb = sc + buf * CB_SV * CB_KS;
+        for (int i = tid; i < CB_ROWS * CB_K; i += CB_THREADS) {
+          const int r = i / CB_K, k = i % CB_K;
+          xb[r * CB_KS + k] = (rows[r] >= 0 && k0 + k < F) ? (double)load_col(a.pro, a.x + (int64_t)rows[r] * a.ldx, k0 + k) : 0.0;
+        }
+        for (int i = tid; i < CB_SV * CB_K; i += CB_THREADS) {
+          const int jj = i / CB_K, k = i % CB_K;
+          sb[jj * CB_KS + k] = (jj < nj && k0 + k < F) ? __ldg(a.sv + (size_t)(j0 + jj) * F + k0 + k) : 0.0;
+        }
+      };
+      stage(0, 0);
+      __syncthreads();
+      for (int kc = 0; kc < nkc; ++kc) {
+        if (kc + 1 < nkc) stage(kc + 1, (kc + 1) & 1);
+        const double* xb = xc + (kc & 1) * CB_ROWS * CB_KS;
+        const double* sb = sc + (kc & 1) * CB_SV * CB_KS;
+#pragma unroll 4
+        for (int k = 0; k < CB_K; ++k) {
+          double xv[4], sv[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) xv[i] = xb[(tr + 16 * i) * CB_KS + k];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) sv[j] = sb[(ts + 16 * j) * CB_KS + k];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) g[i][j] = fma(xv[i], sv[j], g[i][j]);
+        }
+        __syncthreads();
+      }
+      // kernel values of this tile and their error bounds against libsvm's
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int r = tr + 16 * i, jj = ts + 16 * j;
+          double kv = 0.0, ek = 0.0;
+          if (jj < nj) {
+            const double G = g[i][j], nx = nxs[r], ns = __ldg(a.ns64 + j0 + jj);
+            // G: ours and libsvm's float64 dot products each within gamma_{F+3} sum|x s| <= gamma (nx + ns) / 2
+            const double eg = gF * (nx + ns);
+            if (a.kernel == CMLB_SVM_RBF) {
+              // d2 = nx + ns - 2G here, sum (x - s)^2 in libsvm: both within (2 gF + 6u)(nx + ns) of exact
+              const double d2 = fmax(nx + ns - 2.0 * G, 0.0);
+              kv = exp(-a.gamma64 * d2);
+              const double gd = fabs(a.gamma64) * (4.0 * gF + 12.0 * U) * (nx + ns);
+              // + the roundings of exp (<= 1 ulp each side) and of its argument gamma * d2
+              ek = kv * (gd * (1.0 + 2.0 * gd) + 8.0 * U + 4.0 * U * fabs(a.gamma64) * d2) + 1e-300;
+            } else if (a.kernel == CMLB_SVM_LINEAR) {
+              kv = G;
+              ek = 2.0 * eg + 4.0 * U * fabs(G);
+            } else {
+              const double u = a.gamma64 * G + a.coef064;
+              const double eu = fabs(a.gamma64) * 2.0 * eg + 4.0 * U * (fabs(a.gamma64 * G) + fabs(a.coef064));
+              if (a.kernel == CMLB_SVM_SIGMOID) {
+                kv = tanh(u);
+                ek = 2.0 * eu + 8.0 * U;
+              } else {
+                double t = u, ret = 1.0;
+                for (int e = a.degree; e > 0; e /= 2) {
+                  if (e % 2 == 1) ret *= t;
+                  t *= t;
+                }
+                kv = ret;
+                double m = 1.0;  // (|u| + eu)^(deg - 1)
+                for (int e = 1; e < a.degree; ++e) m *= fabs(u) + eu;
+                ek = 2.0 * a.degree * m * eu * (1.0 + eu) + 8.0 * a.degree * U * fabs(kv) + 1e-300;
+              }
+            }
+          }
+          ks[r * CB_SS + jj] = kv;
+          eks[r * CB_SS + jj] = ek;
+        }
+      __syncthreads();
+      // decision sums per (row, pair) task, ascending SV order (libsvm's)
+#pragma unroll
+      for (int q = 0; q < CB_TPT; ++q) {
+        const int task = tid + q * CB_THREADS;
+        if (task >= ntasks) break;
+        const int r = task % CB_ROWS, p = task / CB_ROWS;
+        auto add = [&](const float* coefrow, int lo, int hi) {
+          for (int j = max(lo, j0); j < min(hi, j0 + nj); ++j) {
+            const double w = (double)__ldg(coefrow + j);
+            const double kv = ks[r * CB_SS + (j - j0)];
+            dsum[q] = __dadd_rn(dsum[q], __dmul_rn(w, kv));
+            asum[q] = __fadd_ru(asum[q], __double2float_ru(fabs(w * kv)));
+            esum[q] += fabs(w) * eks[r * CB_SS + (j - j0)];
+          }
+        };
+        if (a.is_svr) {
+          add(a.coef, 0, a.n_sv);
+        } else {
+          int ca = 0, rem = p;
+          while (rem >= C - 1 - ca) { rem -= C - 1 - ca; ++ca; }
+          const int cb = ca + 1 + rem;
+          add(a.coef + (size_t)(cb - 1) * a.n_sv, n_sv_start[ca], n_sv_start[ca + 1]);
+          add(a.coef + (size_t)ca * a.n_sv, n_sv_start[cb], n_sv_start[cb + 1]);
+        }
+      }
+      __syncthreads();  // ks / eks reused by the next tile
+    }
+    // certify: a row is decided when every pair clears its bound
+    double* decs = xc;  // [CB_ROWS][npairs <= 48]: 24.6 KB over the free staging buffers (xc + sc, 34.8 KB)
+#pragma unroll
+    for (int q = 0; q < CB_TPT; ++q) {
+      const int task = tid + q * CB_THREADS;
+      if (task >= ntasks) break;
+      const int r = task % CB_ROWS, p = task / CB_ROWS;
+      const double rho = (double)a.intercept[p];
+      const double dec = __dsub_rn(dsum[q], -rho);
+      const double tol2 = esum[q] + 2.0 * gamma_n(a.n_sv + 2) * (asum[q] + fabs(rho)) + 1e-300;
+      if (!a.is_svr && !(fabs(dec) > tol2)) atomicOr(&undecided[r], 1);
+      decs[r * npairs + p] = dec;
+    }
+    __syncthreads();
+    if (tid < nb) {
+      const int64_t row = rows[tid];
+      const double* d = decs + tid * npairs;
+      if (undecided[tid]) {
+        a.queue2[atomicAdd(a.queue2_len, 1)] = (int32_t)row;
+      } else if (a.is_svr) {
+        store_out(a.y, row, a.out_dt, (double)(float)d[0]);
+        if (a.dec_out) a.dec_out[row] = d[0];
+      } else {
+        int vote[MAXC];
+        for (int c = 0; c < C; ++c) vote[c] = 0;
+        int p = 0;
+        for (int i = 0; i < C; ++i)
+          for (int j = i + 1; j < C; ++j, ++p) {
+            if (d[p] > 0) ++vote[i]; else ++vote[j];
+          }
+        int best = 0;
+        for (int c = 1; c < C; ++c)
+          if (vote[c] > vote[best]) best = c;
+        store_out(a.y, row, a.out_dt, a.classes[best]);
+        if (a.dec_out)
+          for (int q = 0; q < npairs; ++q) a.dec_out[row * npairs + q] = d[q];
+      }
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(XTHREADS) svm_exact_kernel(const Args a, const int* n_sv_start) {
   extern __shared__ __align__(16) uint8_t xsm[];
   const int xstr = a.F + 2;                                           // padded row stride (doubles)
@@ -742,6 +970,7 @@ static int make_svm(const cmlb_svm_desc* d, int device, cmlb_svm** out) {
   // per-SV coefficient toward each other class (libsvm: SV of class c in
   // pair (c, o) uses coef[o-1] if c < o, else coef[o])
   std::vector<float> w((size_t)NP * CPS, 0.0f), wmax(NP, 0.0f), ns(NP, 0.0f), qerr(NP, 0.0f);
+  std::vector<double> ns64(std::max(NSV, 1), 0.0);
   for (int j = 0; j < NSV; ++j) {
     const int c = cls[j];
     for (int o = 0; o < C; ++o) {
@@ -758,6 +987,7 @@ static int make_svm(const cmlb_svm_desc* d, int device, cmlb_svm** out) {
       s += v * v;
     }
     ns[j] = (float)s;
+    ns64[j] = s;
     qerr[j] = (float)((double)wmax[j] * d->gamma * 1.075e-6 * s * (1.0 + 1e-6));
   }
   // SV splits in the UMMA core-matrix layout: [tile][kb][big|small][c][row][4]
@@ -798,7 +1028,7 @@ static int make_svm(const cmlb_svm_desc* d, int device, cmlb_svm** out) {
   if ((st = upload(m, bsplit, &bs)) || (st = upload(m, ns, &a.ns)) || (st = upload(m, w, &a.w)) ||
       (st = upload(m, wmax, &a.wmax)) || (st = upload(m, qerr, &a.qerr)) || (st = upload(m, cls, &a.cls)) || (st = upload(m, svv, &a.sv)) ||
       (st = upload(m, coef, &a.coef)) || (st = upload(m, ic, &a.intercept)) ||
-      (st = upload(m, classes, &a.classes)) || (st = upload(m, start, &ss))) {
+      (st = upload(m, classes, &a.classes)) || (st = upload(m, start, &ss)) || (st = upload(m, ns64, &a.ns64))) {
     destroy_svm(m);
     return st;
   }
@@ -891,11 +1121,13 @@ int cmlb_svm_run(const cmlb_svm* m, const float* x, int64_t n_rows, int64_t ldx,
   a.prob_tol = prob_tol;
   keep_pool(m->device);
   void* scratch = nullptr;
-  CMLB_CUDA(cudaMallocAsync(&scratch, (size_t)(n_rows + 4) * sizeof(int32_t), s));
+  CMLB_CUDA(cudaMallocAsync(&scratch, (size_t)(2 * n_rows + 8) * sizeof(int32_t), s));
   a.queue_len = static_cast<int32_t*>(scratch);
-  a.queue = a.queue_len + 4;
+  a.queue2_len = a.queue_len + 1;
+  a.queue = a.queue_len + 8;
+  a.queue2 = a.queue + n_rows;
   int st = CMLB_OK;
-  if (cudaMemsetAsync(a.queue_len, 0, sizeof(int32_t), s) != cudaSuccess) st = fail(CMLB_E_DEVICE, "memset");
+  if (cudaMemsetAsync(a.queue_len, 0, 2 * sizeof(int32_t), s) != cudaSuccess) st = fail(CMLB_E_DEVICE, "memset");
   if (!st) {
     st = launch_any(m->CP, a, n_rows, m->tc_smem, s);
   }
@@ -904,15 +1136,33 @@ int cmlb_svm_run(const cmlb_svm* m, const float* x, int64_t n_rows, int64_t ldx,
                                          (int)m->x_smem);
     if (e != cudaSuccess) st = cuda_fail(e, "svm_exact smem");
   }
+  // certifying tier (float64 Gram, rigorous bound against libsvm) for the
+  // queued rows; what it cannot decide goes on to the libsvm-order exact path
+  svm::Args ax = a;
+  const bool certify = (a.is_svr ? 1 : a.pairs) <= svm::CB_MAXP && !a.no_exact;
+  if (!st && certify) {
+    cudaError_t e = cudaFuncSetAttribute(svm::svm_certify_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)svm::CB_SMEM);
+    if (e != cudaSuccess) st = cuda_fail(e, "svm_certify smem");
+    if (!st) {
+      const int grid = std::max(1, std::min<int>(2 * num_sms(m->device), (int)ceil_div(n_rows, svm::CB_ROWS)));
+      svm::svm_certify_kernel<<<grid, svm::CB_THREADS, svm::CB_SMEM, s>>>(a, m->sv_start);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) st = cuda_fail(e, "svm_certify_kernel");
+      else note_launch();
+    }
+    ax.queue = a.queue2;
+    ax.queue_len = a.queue2_len;
+  }
   if (!st) {
     const int grid = std::max(1, std::min<int>(3 * num_sms(m->device), (int)ceil_div(n_rows, svm::XR)));
-    svm::svm_exact_kernel<<<grid, svm::XTHREADS, m->x_smem, s>>>(a, m->sv_start);
+    svm::svm_exact_kernel<<<grid, svm::XTHREADS, m->x_smem, s>>>(ax, m->sv_start);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) st = cuda_fail(e, "svm_exact_kernel");
     else note_launch();
   }
   if (!st && exact_rows) {
-    cudaError_t e = cudaMemcpyAsync(exact_rows, a.queue_len, sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
+    cudaError_t e = cudaMemcpyAsync(exact_rows, ax.queue_len, sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
     if (e != cudaSuccess) st = cuda_fail(e, "exact_rows");
   }
   cudaFreeAsync(scratch, s);
