@@ -674,7 +674,7 @@ __device__ __forceinline__ void load_payload(const float* p, float (&v)[CT]) {
 // buffer f&1 of the staging area (inside the tree-chunk region) while the CTA
 // searches feature f-1's buffer (double buffering: one barrier per feature).
 // Row values are read eight features at a time.
-template <int NTT, int RPT, bool GOUT = false>
+template <int NTT, int RPT, bool GOUT = false, int GF = 8>
 __device__ __forceinline__ void rank_tile(const ForestArgs& a, uint8_t* smem, uint8_t* chunk, uint64_t* stage_bar,
                                           const int64_t (&rowk)[RPT], const uint32_t (&pb)[RPT],
                                           const int (&nbad)[RPT], const int64_t* gidx = nullptr) {
@@ -710,30 +710,30 @@ __device__ __forceinline__ void rank_tile(const ForestArgs& a, uint8_t* smem, ui
   issue_stage(0);
   // row values for features g0..g0+7; the next group's loads are issued
   // before this group's searches so their latency hides behind them
-  float xn[RPT][8];
+  float xn[RPT][GF];
   auto load_group = [&](int g) {
 #pragma unroll
     for (int k = 0; k < RPT; ++k) {
       const float* src = a.x + rowk[k] * a.ldx;
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
+      for (int j = 0; j < GF; ++j)
         xn[k][j] = (rowk[k] < a.n_rows && g + j < F) ? load_col(a.pro, src, g + j) : 0.0f;
     }
   };
   load_group(0);
-  for (int g0 = 0; g0 < F; g0 += 8) {
-    float xv[RPT][8];
+  for (int g0 = 0; g0 < F; g0 += GF) {
+    float xv[RPT][GF];
 #pragma unroll
     for (int k = 0; k < RPT; ++k)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < GF; ++j) {
         float v = xn[k][j];
         if (nbad[k] && rowk[k] < a.n_rows && g0 + j < F && (nbad[k] >= 2 || isfinite(v))) v = __int_as_float(0x7fc00000);
         xv[k][j] = v;
       }
-    if (g0 + 8 < F) load_group(g0 + 8);
+    if (g0 + GF < F) load_group(g0 + GF);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < GF; ++j) {
       const int f = g0 + j;
       if (f < F) {  // uniform across the CTA
         if (!dbl && f > 0) {
@@ -982,11 +982,11 @@ __global__ void __launch_bounds__(NTT, 1) forest_ranked_kernel(const ForestArgs 
 // ranking (stage each feature's thresholds, search every row) ran once per
 // 512-row tile and took ~30% of the walk kernel's warp time (ncu stall samples,
 // profiles/r2_skew_v4_ncu_summary.json); here a CTA ranks 2,048 rows per
-// staged feature, 4 independent searches per thread, and writes the u16 ranks
+// staged feature, 8 interleaved searches per thread, and writes the u16 ranks
 // straight into the walk tiles' interleaved layout, which the walk then
 // bulk-copies (28 KB per 512-row tile for F = 28).
-constexpr int RANK_THREADS = 512, RANK_RPT = 4;
-__global__ void __launch_bounds__(RANK_THREADS) forest_rank_kernel(const ForestArgs a) {
+constexpr int RANK_THREADS = 256, RANK_RPT = 8;
+__global__ void __launch_bounds__(RANK_THREADS, 2) forest_rank_kernel(const ForestArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ __align__(8) uint64_t stage_bar[2];
   constexpr int RPT = RANK_RPT, ROWS = RANK_THREADS * RANK_RPT;
@@ -1015,7 +1015,7 @@ __global__ void __launch_bounds__(RANK_THREADS) forest_rank_kernel(const ForestA
   }
   ForestArgs ar = a;
   ar.stage_off = 0;  // staging buffers at the start of this kernel's shared memory
-  rank_tile<RANK_THREADS, RPT, true>(ar, smem, smem, stage_bar, rowk, pb, nbad, gidx);
+  rank_tile<RANK_THREADS, RPT, true, 4>(ar, smem, smem, stage_bar, rowk, pb, nbad, gidx);
 }
 
 template <int CT, int NTT, int RPT, int TI, int DT>
