@@ -593,7 +593,7 @@ constexpr int XTHREADS = 256;
 // outputs per thread, K staged in 32-feature float64 chunks (double-buffered);
 // decision sums per (row, pair) task in ascending SV order (deterministic).
 constexpr int CB_ROWS = 64, CB_SV = 64, CB_K = 16, CB_THREADS = 256;
-constexpr int CB_KS = CB_K + 1, CB_SS = CB_SV + 1;              // padded strides (bank-conflict-free)
+constexpr int CB_KS = CB_K + 2, CB_SS = CB_SV + 1;              // padded strides (16-byte rows, conflict-free)
 constexpr int CB_TPT = 12;                                        // (row, pair) tasks per thread: pairs <= 48
 constexpr int CB_MAXP = CB_TPT * CB_THREADS / CB_ROWS;
 constexpr size_t CB_SMEM = (size_t)2 * (CB_ROWS + CB_SV) * CB_KS * 8 + (size_t)2 * CB_ROWS * CB_SS * 8 + CB_ROWS * 8;
@@ -617,7 +617,11 @@ __global__ void __launch_bounds__(CB_THREADS, 2) svm_certify_kernel(const Args a
   const int F = a.F, C = a.C;
   const int npairs = a.is_svr ? 1 : a.pairs;
   const int ntasks = CB_ROWS * npairs;
-  const int tr = tid / 16, ts = tid % 16;                          // 4 rows x 4 SVs: rows tr + 16 i, SVs ts + 16 j
+  // thread tile 4 rows x 4 SVs; a warp covers 16 rows x 32 SVs (lane = 4 b + a:
+  // rows r0 + a + 4 i, SVs s0 + b + 8 j), so each 128-bit load of two k values
+  // is one wavefront (4 distinct rows / 8 distinct SVs per warp)
+  const int warp = tid >> 5, lane = tid & 31;
+  const int r0 = 16 * (warp >> 1) + (lane & 3), s0 = 32 * (warp & 1) + (lane >> 2);
   const double gF = gamma_n(F + 3);
   constexpr double U = 1.1102230246251565e-16;
   for (int b0 = blockIdx.x * CB_ROWS; b0 < nq; b0 += gridDim.x * CB_ROWS) {
@@ -651,37 +655,76 @@ __global__ void __launch_bounds__(CB_THREADS, 2) svm_certify_kernel(const Args a
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) g[i][j] = 0.0;
-      auto stage = [&](int kc, int buf) {
+      // chunk kc: SVs by cp.async (float64 already), x by a register prefetch
+      // of the next chunk (float32 -> float64 on the way into shared memory)
+      float xpre[CB_ROWS * CB_K / CB_THREADS];
+      auto load_x = [&](int kc) {
         const int k0 = kc * CB_K;
-        double* xb = xc + buf * CB_ROWS * CB_KS;
-        double* sb = sc + buf * CB_SV * CB_KS;
-        for (int i = tid; i < CB_ROWS * CB_K; i += CB_THREADS) {
-          const int r = i / CB_K, k = i % CB_K;
-          xb[r * CB_KS + k] = (rows[r] >= 0 && k0 + k < F) ? (double)load_col(a.pro, a.x + (int64_t)rows[r] * a.ldx, k0 + k) : 0.0;
-        }
-        for (int i = tid; i < CB_SV * CB_K; i += CB_THREADS) {
-          const int jj = i / CB_K, k = i % CB_K;
-          sb[jj * CB_KS + k] = (jj < nj && k0 + k < F) ? __ldg(a.sv + (size_t)(j0 + jj) * F + k0 + k) : 0.0;
+#pragma unroll
+        for (int u = 0; u < CB_ROWS * CB_K / CB_THREADS; ++u) {
+          const int i = tid + u * CB_THREADS, r = i / CB_K, k = i % CB_K;
+          xpre[u] = (rows[r] >= 0 && k0 + k < F) ? load_col(a.pro, a.x + (int64_t)rows[r] * a.ldx, k0 + k) : 0.0f;
         }
       };
-      stage(0, 0);
+      auto store_x = [&](int buf) {
+        double* xb = xc + buf * CB_ROWS * CB_KS;
+#pragma unroll
+        for (int u = 0; u < CB_ROWS * CB_K / CB_THREADS; ++u) {
+          const int i = tid + u * CB_THREADS, r = i / CB_K, k = i % CB_K;
+          xb[r * CB_KS + k] = (double)xpre[u];
+        }
+      };
+      auto stage_s = [&](int kc, int buf) {
+        const int k0 = kc * CB_K;
+        double* sb = sc + buf * CB_SV * CB_KS;
+        for (int i = tid; i < CB_SV * CB_K / 2; i += CB_THREADS) {  // 16-byte pieces
+          const int jj = i / (CB_K / 2), kp = i % (CB_K / 2);
+          if (F & 1) {  // odd F: rows are not 16-byte aligned, plain loads
+            for (int h = 0; h < 2; ++h) {
+              const int k = k0 + 2 * kp + h;
+              sb[jj * CB_KS + 2 * kp + h] = (jj < nj && k < F) ? __ldg(a.sv + (size_t)(j0 + jj) * F + k) : 0.0;
+            }
+            continue;
+          }
+          // bytes present: 16 or 0 (F even: pieces never straddle the row end)
+          const int nbytes = (jj < nj && k0 + 2 * kp < F) ? 16 : 0;
+          const uint32_t dst = (uint32_t)__cvta_generic_to_shared(sb + jj * CB_KS + 2 * kp);
+          const double* src = nbytes ? a.sv + (size_t)(j0 + jj) * F + k0 + 2 * kp : a.sv;
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(nbytes) : "memory");
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+      };
+      load_x(0);
+      store_x(0);
+      stage_s(0, 0);
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
       __syncthreads();
       for (int kc = 0; kc < nkc; ++kc) {
-        if (kc + 1 < nkc) stage(kc + 1, (kc + 1) & 1);
+        const bool more = kc + 1 < nkc;
+        if (more) {
+          load_x(kc + 1);
+          stage_s(kc + 1, (kc + 1) & 1);
+        }
         const double* xb = xc + (kc & 1) * CB_ROWS * CB_KS;
         const double* sb = sc + (kc & 1) * CB_SV * CB_KS;
-#pragma unroll 4
-        for (int k = 0; k < CB_K; ++k) {
-          double xv[4], sv[4];
+#pragma unroll 2
+        for (int k = 0; k < CB_K; k += 2) {
+          double2 xv[4], sv[4];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) xv[i] = xb[(tr + 16 * i) * CB_KS + k];
+          for (int i = 0; i < 4; ++i) xv[i] = *reinterpret_cast<const double2*>(xb + (r0 + 4 * i) * CB_KS + k);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) sv[j] = sb[(ts + 16 * j) * CB_KS + k];
+          for (int j = 0; j < 4; ++j) sv[j] = *reinterpret_cast<const double2*>(sb + (s0 + 8 * j) * CB_KS + k);
 #pragma unroll
           for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) g[i][j] = fma(xv[i], sv[j], g[i][j]);
+            for (int j = 0; j < 4; ++j) g[i][j] = fma(xv[i].x, sv[j].x, g[i][j]);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) g[i][j] = fma(xv[i].y, sv[j].y, g[i][j]);
         }
+        if (more) store_x((kc + 1) & 1);
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         __syncthreads();
       }
       // kernel values of this tile and their error bounds against libsvm's
@@ -689,7 +732,7 @@ __global__ void __launch_bounds__(CB_THREADS, 2) svm_certify_kernel(const Args a
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const int r = tr + 16 * i, jj = ts + 16 * j;
+          const int r = r0 + 4 * i, jj = s0 + 8 * j;
           double kv = 0.0, ek = 0.0;
           if (jj < nj) {
             const double G = g[i][j], nx = nxs[r], ns = __ldg(a.ns64 + j0 + jj);
