@@ -805,7 +805,9 @@ __global__ void __launch_bounds__(NT, 1) linear_tile_kernel(const LinearArgs a) 
 }
 
 struct TileCfg { int nt, kc, st, rpt, per_sm; };
-static const TileCfg kTileCfg[] = {{128, 32, 4, 1, 2}, {128, 16, 4, 2, 2}, {128, 16, 4, 4, 1}, {64, 16, 4, 4, 2}, {128, 16, 3, 2, 2}};
+static const TileCfg kTileCfg[] = {{128, 32, 4, 1, 2}, {128, 16, 4, 2, 2}, {128, 16, 4, 4, 1}, {64, 16, 4, 4, 2}, {128, 16, 3, 2, 2},
+                                   {256, 16, 4, 2, 1}, {128, 32, 4, 2, 1}, {128, 16, 6, 2, 1}};
+constexpr int N_TILE_CFG = sizeof(kTileCfg) / sizeof(kTileCfg[0]);
 
 template <int CM>
 static LinFn tile_fn(int cfg) {
@@ -814,6 +816,9 @@ static LinFn tile_fn(int cfg) {
     case 1: return linear_tile_kernel<CM, 128, 16, 4, 2>;
     case 2: return linear_tile_kernel<CM, 128, 16, 4, 4>;
     case 3: return linear_tile_kernel<CM, 64, 16, 4, 4>;
+    case 5: return linear_tile_kernel<CM, 256, 16, 4, 2>;
+    case 6: return linear_tile_kernel<CM, 128, 32, 4, 2>;
+    case 7: return linear_tile_kernel<CM, 128, 16, 6, 2>;
     default: return linear_tile_kernel<CM, 128, 16, 3, 2>;
   }
 }
@@ -1023,7 +1028,7 @@ int cmlb_linear_run(const cmlb_linear* m, const float* x, int64_t n_rows, int64_
       return e ? std::atoi(e) : 2;
     }();
     if (lin_impl >= 1) {
-      const int cfg = std::min(lin_impl - 1, 4);
+      const int cfg = std::min(lin_impl - 1, N_TILE_CFG - 1);
       LinFn kt = cm == 2 ? tile_fn<2>(cfg) : cm == 4 ? tile_fn<4>(cfg) : cm == 8 ? tile_fn<8>(cfg)
                : cm == 10 ? tile_fn<10>(cfg) : cm == 12 ? tile_fn<12>(cfg) : tile_fn<16>(cfg);
       const TileCfg tc = kTileCfg[cfg];
