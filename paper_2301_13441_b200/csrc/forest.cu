@@ -669,12 +669,12 @@ __device__ __forceinline__ void load_payload(const float* p, float (&v)[CT]) {
 
 // Rank the CTA's row tile (both ranked kernels): for every feature f and row
 // r of the tile, rank(x[r][f]) = #{u in U_f : u < x} into the u16 rank tile at
-// the start of shared memory (layout: see the callers' pb()).
+// the start of shared memory (layout: see the callers' pb()), or (GOUT, the
+// rank pass) into the walk tiles in global memory.
 // Feature f's Eytzinger thresholds + index map are staged with TMA into
-// buffer f&1 of the staging area (inside the tree-chunk region) while the CTA
-// searches feature f-1's buffer (double buffering: one barrier per feature).
-// Row values are read eight features at a time.
-template <int NTT, int RPT, bool GOUT = false, int GF = 8>
+// buffer f&1 of the staging area while the CTA searches feature f-1's buffer
+// (double buffering: one barrier per feature).
+template <int NTT, int RPT, bool GOUT = false>
 __device__ __forceinline__ void rank_tile(const ForestArgs& a, uint8_t* smem, uint8_t* chunk, uint64_t* stage_bar,
                                           const int64_t (&rowk)[RPT], const uint32_t (&pb)[RPT],
                                           const int (&nbad)[RPT], const int64_t* gidx = nullptr) {
@@ -708,59 +708,47 @@ __device__ __forceinline__ void rank_tile(const ForestArgs& a, uint8_t* smem, ui
       bulk_g2s(mb + off, ms + off, min(32768u, mbytes - off), &stage_bar[b]);
   };
   issue_stage(0);
-  // row values for features g0..g0+7; the next group's loads are issued
-  // before this group's searches so their latency hides behind them
-  float xn[RPT][GF];
-  auto load_group = [&](int g) {
-#pragma unroll
-    for (int k = 0; k < RPT; ++k) {
-      const float* src = a.x + rowk[k] * a.ldx;
-#pragma unroll
-      for (int j = 0; j < GF; ++j)
-        xn[k][j] = (rowk[k] < a.n_rows && g + j < F) ? load_col(a.pro, src, g + j) : 0.0f;
-    }
-  };
-  load_group(0);
-  for (int g0 = 0; g0 < F; g0 += GF) {
-    float xv[RPT][GF];
+  // one feature per iteration (a rolled loop: the unrolled 8-feature groups
+  // of round 1 made the rank pass ~200 KB of SASS and 21% of its stalls were
+  // instruction fetch); the next feature's row values are loaded before this
+  // feature's searches so their latency hides behind them
+  float xn[RPT];
+  auto load_f = [&](int f) {
 #pragma unroll
     for (int k = 0; k < RPT; ++k)
+      xn[k] = (rowk[k] < a.n_rows && f < F) ? load_col(a.pro, a.x + rowk[k] * a.ldx, f) : 0.0f;
+  };
+  load_f(0);
+#pragma unroll 1
+  for (int f = 0; f < F; ++f) {
+    float xq[RPT];
 #pragma unroll
-      for (int j = 0; j < GF; ++j) {
-        float v = xn[k][j];
-        if (nbad[k] && rowk[k] < a.n_rows && g0 + j < F && (nbad[k] >= 2 || isfinite(v))) v = __int_as_float(0x7fc00000);
-        xv[k][j] = v;
-      }
-    if (g0 + GF < F) load_group(g0 + GF);
+    for (int k = 0; k < RPT; ++k) {
+      float v = xn[k];
+      if (nbad[k] && rowk[k] < a.n_rows && (nbad[k] >= 2 || isfinite(v))) v = __int_as_float(0x7fc00000);
+      xq[k] = v;
+    }
+    if (f + 1 < F) load_f(f + 1);
+    if (!dbl && f > 0) {
+      __syncthreads();  // everyone done searching f-1 in the single buffer
+      issue_stage(f);
+    }
+    mbar_wait(&stage_bar[dbl ? (f & 1) : 0], (uint32_t)((dbl ? (f >> 1) : f) & 1));
+    __syncthreads();  // stage f landed for everyone; buffer (f+1)&1 is free
+    if (dbl && f + 1 < F) issue_stage(f + 1);
+    const float* fb = stage_f(f & 1);
+    const uint16_t* mb = reinterpret_cast<const uint16_t*>(fb + cap);
+    const int nf = __ldg(a.unf + f);
+    int r[RPT];
+    count_less_eyt_n<RPT>(fb, mb, nf, xq, r);
+    if constexpr (GOUT) {  // rank kernel: straight into the walk tiles in global memory
 #pragma unroll
-    for (int j = 0; j < GF; ++j) {
-      const int f = g0 + j;
-      if (f < F) {  // uniform across the CTA
-        if (!dbl && f > 0) {
-          __syncthreads();  // everyone done searching f-1 in the single buffer
-          issue_stage(f);
-        }
-        mbar_wait(&stage_bar[dbl ? (f & 1) : 0], (uint32_t)((dbl ? (f >> 1) : f) & 1));
-        __syncthreads();  // stage f landed for everyone; buffer (f+1)&1 is free
-        if (dbl && f + 1 < F) issue_stage(f + 1);
-        const float* fb = stage_f(f & 1);
-        const uint16_t* mb = reinterpret_cast<const uint16_t*>(fb + cap);
-        const int nf = __ldg(a.unf + f);
-        float xq[RPT];
-        int r[RPT];
+      for (int k = 0; k < RPT; ++k)
+        if (rowk[k] < a.n_rows) a.ranks[gidx[k] + (int64_t)f * a.rank_rows] = (uint16_t)r[k];
+    } else {
+      uint8_t* xrow = reinterpret_cast<uint8_t*>(xr) + (size_t)f * ROWS * 2;
 #pragma unroll
-        for (int k = 0; k < RPT; ++k) xq[k] = xv[k][j];
-        count_less_eyt_n<RPT>(fb, mb, nf, xq, r);
-        if constexpr (GOUT) {  // rank kernel: straight into the walk tiles in global memory
-#pragma unroll
-          for (int k = 0; k < RPT; ++k)
-            if (rowk[k] < a.n_rows) a.ranks[gidx[k] + (int64_t)f * a.rank_rows] = (uint16_t)r[k];
-        } else {
-          uint8_t* xrow = reinterpret_cast<uint8_t*>(xr) + (size_t)f * ROWS * 2;
-#pragma unroll
-          for (int k = 0; k < RPT; ++k) *reinterpret_cast<uint16_t*>(xrow + pb[k]) = (uint16_t)r[k];
-        }
-      }
+      for (int k = 0; k < RPT; ++k) *reinterpret_cast<uint16_t*>(xrow + pb[k]) = (uint16_t)r[k];
     }
   }
 }
@@ -1015,7 +1003,7 @@ __global__ void __launch_bounds__(RANK_THREADS, 2) forest_rank_kernel(const Fore
   }
   ForestArgs ar = a;
   ar.stage_off = 0;  // staging buffers at the start of this kernel's shared memory
-  rank_tile<RANK_THREADS, RPT, true, 4>(ar, smem, smem, stage_bar, rowk, pb, nbad, gidx);
+  rank_tile<RANK_THREADS, RPT, true>(ar, smem, smem, stage_bar, rowk, pb, nbad, gidx);
 }
 
 template <int CT, int NTT, int RPT, int TI, int DT>

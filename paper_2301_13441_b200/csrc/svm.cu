@@ -707,8 +707,8 @@ __global__ void __launch_bounds__(CB_THREADS, 2) svm_certify_kernel(const Args a
         }
         const double* xb = xc + (kc & 1) * CB_ROWS * CB_KS;
         const double* sb = sc + (kc & 1) * CB_SV * CB_KS;
-#pragma unroll 2
-        for (int k = 0; k < CB_K; k += 2) {
+#pragma unroll
+        for (int k = 0; k < CB_K; k += 2) {  // fully unrolled: the loads of k + 2 issue ahead of k's DFMAs
           double2 xv[4], sv[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) xv[i] = *reinterpret_cast<const double2*>(xb + (r0 + 4 * i) * CB_KS + k);
