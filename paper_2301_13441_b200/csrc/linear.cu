@@ -834,13 +834,14 @@ static LinFn tile_fn(int cfg) {
 constexpr int LX_R = 16, LX_ST = 4, LX_NT = LX_R * 16;
 
 __global__ void __launch_bounds__(LX_NT) linear_exact_lanes_kernel(const LinearArgs a) {
-  extern __shared__ __align__(16) double wq[];        // [F][16], then the x ring [LX_ST][LX_R][32]
+  extern __shared__ __align__(16) double wq[];        // [F][16], the float64 slice, then the x ring [LX_ST][LX_R][32]
   const int nq = *a.queue_len;
   const int64_t first = (int64_t)blockIdx.x * LX_R;
   if (first >= nq) return;
   const int F = a.F, C = a.C, tid = threadIdx.x;
   stage_w_kmajor<double, LX_NT>(wq, 16, a.w, C, F);
-  float* ring = reinterpret_cast<float*>(wq + F * 16);
+  double* xd = wq + F * 16;                                  // [LX_R][32] the current slice in float64
+  float* ring = reinterpret_cast<float*>(xd + LX_R * 32);
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
   const int r = tid >> 4, c = tid & 15;
   const int nk = (F + 31) / 32;
@@ -871,20 +872,23 @@ __global__ void __launch_bounds__(LX_NT) linear_exact_lanes_kernel(const LinearA
       asm volatile("cp.async.wait_group %0;\n" ::"n"(LX_ST - 2) : "memory");
       __syncthreads();
       issue(kc + LX_ST - 1);
-      const float* xs = ring + ((kc % LX_ST) * LX_R + r) * 32;
+      // the slice in float64, converted once (each x value feeds 16 output lanes)
+      const float* xsl = ring + (kc % LX_ST) * LX_R * 32;
+      for (int i = tid; i < LX_R * 32; i += LX_NT) xd[i] = (double)xsl[i];
+      __syncthreads();
+      const double* xs = xd + r * 32;
       const int k0 = kc * 32, kn = min(32, F - k0);
       const double* wk = wq + k0 * 16 + c;
-      if (kn == 32) {
-#pragma unroll 8
-        for (int j = 0; j < 32; ++j) {
-          const double w = wk[j * 16];
-          if (act && !(a.sparse && w == 0.0)) acc = fma((double)xs[j], w, acc);
-        }
-      } else {
+      if (a.sparse) {  // CSR weights: only nonzero terms enter the sum (kernels.py:103-126)
         for (int j = 0; j < kn; ++j) {
           const double w = wk[j * 16];
-          if (act && !(a.sparse && w == 0.0)) acc = fma((double)xs[j], w, acc);
+          if (act && w != 0.0) acc = fma(xs[j], w, acc);
         }
+      } else if (kn == 32) {
+#pragma unroll 8
+        for (int j = 0; j < 32; ++j) acc = fma(xs[j], wk[j * 16], acc);  // padded lanes: w = 0
+      } else {
+        for (int j = 0; j < kn; ++j) acc = fma(xs[j], wk[j * 16], acc);
       }
     }
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
@@ -1054,7 +1058,7 @@ int cmlb_linear_run(const cmlb_linear* m, const float* x, int64_t n_rows, int64_
   CMLB_CUDA(cudaGetLastError());
   if (fixup) {
     static const bool old_fix = std::getenv("CMLB_LINEAR_FIXUP_WARP") != nullptr;
-    const size_t xb = (size_t)m->F * 16 * 8 + (size_t)LX_ST * LX_R * 32 * 4;
+    const size_t xb = (size_t)m->F * 16 * 8 + (size_t)LX_R * 32 * 8 + (size_t)LX_ST * LX_R * 32 * 4;
     if (!old_fix && m->C <= 16 && !m->pro && aligned && xb <= 200 * 1024) {
       CMLB_CUDA(cudaFuncSetAttribute(linear_exact_lanes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xb));
       int per_sm = 0;

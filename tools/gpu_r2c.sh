@@ -3,7 +3,11 @@
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-timeout 2400 python -m pytest ${PYFILES:-tests/test_gpu_rf500_ref.py tests/test_gpu_svm.py tests/test_gpu_parity.py} -m gpu -q -x ${PYARGS} > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+if [ -n "$PYK" ]; then
+  timeout 2400 python -m pytest ${PYFILES:-tests} -m gpu -q -k "$PYK" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+else
+  timeout 2400 python -m pytest ${PYFILES:-tests} -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+fi
 timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err
 for c in ${CONFIGS:-gbr1000 svc10k pipe5 dt6}; do
   timeout 900 python bench.py --config $c --steps 10 --warmup 3 > gpurun_out/cfg_$c.json 2> gpurun_out/cfg_$c.err
