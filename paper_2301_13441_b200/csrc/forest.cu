@@ -677,7 +677,8 @@ __device__ __forceinline__ void load_payload(const float* p, float (&v)[CT]) {
 template <int NTT, int RPT, bool GOUT = false>
 __device__ __forceinline__ void rank_tile(const ForestArgs& a, uint8_t* smem, uint8_t* chunk, uint64_t* stage_bar,
                                           const int64_t (&rowk)[RPT], const uint32_t (&pb)[RPT],
-                                          const int (&nbad)[RPT], const int64_t* gidx = nullptr) {
+                                          const int (&nbad)[RPT], const int64_t* gidx = nullptr,
+                                          uint64_t* empty_bar = nullptr) {
   constexpr int ROWS = NTT * RPT;
   const int tid = threadIdx.x;
   const int F = a.F;
@@ -734,13 +735,27 @@ __device__ __forceinline__ void rank_tile(const ForestArgs& a, uint8_t* smem, ui
       issue_stage(f);
     }
     mbar_wait(&stage_bar[dbl ? (f & 1) : 0], (uint32_t)((dbl ? (f >> 1) : f) & 1));
-    __syncthreads();  // stage f landed for everyone; buffer (f+1)&1 is free
-    if (dbl && f + 1 < F) issue_stage(f + 1);
+    if (dbl && empty_bar) {
+      // per-warp release (no CTA barrier per feature): buffer (f+1)&1 held
+      // feature f-1; warp 0 alone waits until every warp is done with it
+      if (threadIdx.x < 32 && f + 1 < F) {
+        if (f >= 1) mbar_wait(&empty_bar[(f + 1) & 1], (uint32_t)(((f - 1) >> 1) & 1));
+        issue_stage(f + 1);
+        __syncwarp();
+      }
+    } else {
+      __syncthreads();  // stage f landed for everyone; buffer (f+1)&1 is free
+      if (dbl && f + 1 < F) issue_stage(f + 1);
+    }
     const float* fb = stage_f(f & 1);
     const uint16_t* mb = reinterpret_cast<const uint16_t*>(fb + cap);
     const int nf = __ldg(a.unf + f);
     int r[RPT];
     count_less_eyt_n<RPT>(fb, mb, nf, xq, r);
+    if (dbl && empty_bar) {
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&empty_bar[f & 1]);
+    }
     if constexpr (GOUT) {  // rank kernel: straight into the walk tiles in global memory
 #pragma unroll
       for (int k = 0; k < RPT; ++k)
@@ -977,11 +992,14 @@ constexpr int RANK_THREADS = 256, RANK_RPT = 8;
 __global__ void __launch_bounds__(RANK_THREADS, 2) forest_rank_kernel(const ForestArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ __align__(8) uint64_t stage_bar[2];
+  __shared__ __align__(8) uint64_t empty_bar[2];
   constexpr int RPT = RANK_RPT, ROWS = RANK_THREADS * RANK_RPT;
   const int tid = threadIdx.x;
   if (tid == 0) {
     mbar_init(&stage_bar[0], 1);
     mbar_init(&stage_bar[1], 1);
+    mbar_init(&empty_bar[0], RANK_THREADS / 32);
+    mbar_init(&empty_bar[1], RANK_THREADS / 32);
     mbar_fence_init();
   }
   __syncthreads();
@@ -1003,7 +1021,7 @@ __global__ void __launch_bounds__(RANK_THREADS, 2) forest_rank_kernel(const Fore
   }
   ForestArgs ar = a;
   ar.stage_off = 0;  // staging buffers at the start of this kernel's shared memory
-  rank_tile<RANK_THREADS, RPT, true>(ar, smem, smem, stage_bar, rowk, pb, nbad, gidx);
+  rank_tile<RANK_THREADS, RPT, true>(ar, smem, smem, stage_bar, rowk, pb, nbad, gidx, empty_bar);
 }
 
 template <int CT, int NTT, int RPT, int TI, int DT>
