@@ -543,6 +543,88 @@ def cpu_baseline(wl, threads: int, target_s: float = 10.0) -> dict:
             "sample": f"{n} rows x {wl.features} of the workload's input distribution, {dt:.1f} s, {what}"}
 
 
+def reference_json(model) -> str | None:
+    """Our forest / linear model in the reference's model-JSON schema
+    (``pkg/exporter/export.py:56-153``), for timing ``mlower`` itself."""
+    def tree_nodes(t):
+        a = t.arrays
+        nodes = []
+        for i in range(len(a.is_leaf)):
+            if a.is_leaf[i]:
+                nodes.append({"leaf": [float(v) for v in np.atleast_1d(a.value[i])]})
+            else:
+                nodes.append({"feature": int(a.feature[i]), "threshold": float(a.threshold[i]),
+                              "left": int(a.left[i]), "right": int(a.right[i])})
+        return nodes
+
+    trees = getattr(model, "trees", None)
+    if trees is None and hasattr(model, "arrays"):  # single decision tree
+        obj = {"model_type": model.model_type, "n_features": int(model.n_features), "nodes": tree_nodes(model)}
+        if getattr(model, "classes", None) is not None:
+            obj["classes"] = [float(c) for c in model.classes]
+        obj["format_version"] = 1
+        return json.dumps(obj)
+    if trees is not None:
+        out = []
+        for t in trees:
+            a = t.arrays
+            nodes = []
+            for i in range(len(a.is_leaf)):
+                if a.is_leaf[i]:
+                    nodes.append({"leaf": [float(v) for v in np.atleast_1d(a.value[i])]})
+                else:
+                    nodes.append({"feature": int(a.feature[i]), "threshold": float(a.threshold[i]),
+                                  "left": int(a.left[i]), "right": int(a.right[i])})
+            out.append({"nodes": nodes})
+        obj = {"model_type": model.model_type, "n_features": int(model.n_features), "trees": out,
+               "aggregation": model.aggregation}
+        if model.aggregation == "sum":
+            obj.update(learning_rate=float(model.learning_rate), base_score=float(model.base_score))
+        if model.classes is not None:
+            obj["classes"] = [float(c) for c in model.classes]
+    elif hasattr(model, "coef"):
+        obj = {"model_type": model.model_type, "n_features": int(model.n_features),
+               "coef": [[float(v) for v in r] for r in model.coef], "intercept": [float(v) for v in model.intercept]}
+        if getattr(model, "classes", None) is not None:
+            obj["classes"] = [float(c) for c in model.classes]
+    else:
+        return None
+    obj["format_version"] = 1
+    return json.dumps(obj)
+
+
+def time_reference_itself(wl, target_s: float = 5.0):
+    """The unmodified reference (``mlower``, installed offline in baseline/_ref
+    by tools/install_reference.sh) on a bounded sample: compile once, then
+    ``execute`` on as many rows as fit ~target_s of this host's time."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "mlower")):
+        return {"unavailable": "reference not installed in baseline/_ref (tools/install_reference.sh)"}
+    sys.path.insert(0, ref)
+    try:
+        import mlower
+        from mlower.dtypes import DType
+        from mlower.tensor import Tensor
+        model = wl.model()
+        text = reference_json(model) if not isinstance(wl, (Pipe5, SVC10k)) else None
+        if text is None:
+            return {"unavailable": "no reference model family for this workload (SPEC.md:9)"}
+        compiled = mlower.compile_model(mlower.parse_model(text))
+        x = _host_sample(wl, 64, 96).astype(np.float32)
+        t0 = time.perf_counter()
+        mlower.execute(compiled.plan, Tensor.from_dense(x, DType.FLOAT32))
+        rate = 64 / max(time.perf_counter() - t0, 1e-6)
+        n = int(min(max(rate * target_s, 64), 200_000))
+        x = _host_sample(wl, n, 95).astype(np.float32)
+        t0 = time.perf_counter()
+        mlower.execute(compiled.plan, Tensor.from_dense(x, DType.FLOAT32))
+        dt = time.perf_counter() - t0
+        return {"value": n / dt, "unit": "samples/s", "cores": 1, "rows": n, "seconds": dt,
+                "what": "mlower.execute (the unmodified reference, pure Python + numpy, one process)"}
+    except Exception as e:  # report, never fail the arm
+        return {"unavailable": f"{type(e).__name__}: {e}"}
+
+
 def run_reference(args, wl):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -560,6 +642,7 @@ def run_reference(args, wl):
         "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": "port",
                          "sample": f"{n} rows per step x {args.steps} steps, {what}"},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_itself": time_reference_itself(wl),
     }
     print(json.dumps(line), flush=True)
     return 0

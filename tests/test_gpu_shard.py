@@ -171,3 +171,27 @@ def test_row_sharded_predict_is_bit_transparent(host):
         xd = torch.from_numpy(x).cuda()
         got = api.predict(compiled, xd, devices=[0, 0, 0])
         assert got.is_cuda and torch.equal(got, api.predict(compiled, xd))
+
+
+def test_row_sharded_predict_linear_svm_pipeline():
+    """Row sharding is model-agnostic (linear / SVC / scalers
+    shard rows): LogisticRegression, an SVC and the config-5 pipeline through
+    predict(devices=[0, 0]) equal the unsharded result bit for bit."""
+    import sys as _sys
+    from paper_2301_13441_b200 import api
+    from paper_2301_13441_b200.models import LinearModel
+    from bench_configs import synthetic_svc
+    _sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from workloads import config5_pipeline
+    rng = np.random.default_rng(9)
+    lm = LinearModel("logistic_regression", 96,
+                     tuple(tuple(float(v) for v in r) for r in rng.standard_normal((10, 96)).astype(np.float32)),
+                     tuple(float(v) for v in rng.standard_normal(10).astype(np.float32)), tuple(float(c) for c in range(10)))
+    svc = synthetic_svc(F=64, n_sv=400, C=4, seed=3)
+    pipe, xp = config5_pipeline(rows=50_001)
+    for model, x in ((lm, rng.standard_normal((70_001, 96)).astype(np.float32)),
+                     (svc, rng.standard_normal((20_001, 64)).astype(np.float32)), (pipe, xp)):
+        compiled = api.compile_model(model)
+        got = api.predict(compiled, x, devices=[0, 0])
+        want = api.predict(compiled, x)
+        assert np.array_equal(got, want), type(model).__name__
