@@ -158,6 +158,7 @@ struct ForestArgs {
   // the walk's interleaved row order (nullptr: the walk ranks its own tile)
   uint16_t* ranks;
   int rank_rows;
+  int vec_x;                  // rank pass: x rows 8-byte aligned, F even, no prologue (float2 loads)
 };
 
 constexpr int NT = 256;  // threads per CTA for every forest kernel
@@ -677,7 +678,7 @@ __device__ __forceinline__ void load_payload(const float* p, float (&v)[CT]) {
 template <int NTT, int RPT, bool GOUT = false>
 __device__ __forceinline__ void rank_tile(const ForestArgs& a, uint8_t* smem, uint8_t* chunk, uint64_t* stage_bar,
                                           const int64_t (&rowk)[RPT], const uint32_t (&pb)[RPT],
-                                          const int (&nbad)[RPT], const int64_t* gidx = nullptr,
+                                          const int (&nbad)[RPT], const uint32_t* gidx = nullptr,
                                           uint64_t* empty_bar = nullptr) {
   constexpr int ROWS = NTT * RPT;
   const int tid = threadIdx.x;
@@ -713,23 +714,48 @@ __device__ __forceinline__ void rank_tile(const ForestArgs& a, uint8_t* smem, ui
   // of round 1 made the rank pass ~200 KB of SASS and 21% of its stalls were
   // instruction fetch); the next feature's row values are loaded before this
   // feature's searches so their latency hides behind them
+  // Vector path (plain row-major x, 8-byte aligned rows, even F): each row's
+  // features 2g, 2g+1 are one 8-byte load, pair g+1 in flight while pair g is
+  // searched.  Otherwise one feature at a time through load_col.
+  const bool vec = a.vec_x;
   float xn[RPT];
+  float2 cur[RPT], nxt[RPT];
   auto load_f = [&](int f) {
 #pragma unroll
     for (int k = 0; k < RPT; ++k)
       xn[k] = (rowk[k] < a.n_rows && f < F) ? load_col(a.pro, a.x + rowk[k] * a.ldx, f) : 0.0f;
   };
-  load_f(0);
+  auto load2 = [&](int g, float2 (&dst)[RPT]) {
+#pragma unroll
+    for (int k = 0; k < RPT; ++k)
+      dst[k] = (rowk[k] < a.n_rows && g < F) ? __ldg(reinterpret_cast<const float2*>(a.x + rowk[k] * a.ldx + g))
+                                             : make_float2(0.f, 0.f);
+  };
+  if (vec) {
+    load2(0, cur);
+    load2(2, nxt);
+  } else {
+    load_f(0);
+  }
 #pragma unroll 1
   for (int f = 0; f < F; ++f) {
     float xq[RPT];
+    const bool hi = f & 1;
 #pragma unroll
     for (int k = 0; k < RPT; ++k) {
-      float v = xn[k];
+      float v = vec ? (hi ? cur[k].y : cur[k].x) : xn[k];
       if (nbad[k] && rowk[k] < a.n_rows && (nbad[k] >= 2 || isfinite(v))) v = __int_as_float(0x7fc00000);
       xq[k] = v;
     }
-    if (f + 1 < F) load_f(f + 1);
+    if (vec) {
+      if (hi) {
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) cur[k] = nxt[k];
+        if (f + 3 < F) load2(f + 3, nxt);
+      }
+    } else if (f + 1 < F) {
+      load_f(f + 1);
+    }
     if (!dbl && f > 0) {
       __syncthreads();  // everyone done searching f-1 in the single buffer
       issue_stage(f);
@@ -759,7 +785,7 @@ __device__ __forceinline__ void rank_tile(const ForestArgs& a, uint8_t* smem, ui
     if constexpr (GOUT) {  // rank kernel: straight into the walk tiles in global memory
 #pragma unroll
       for (int k = 0; k < RPT; ++k)
-        if (rowk[k] < a.n_rows) a.ranks[gidx[k] + (int64_t)f * a.rank_rows] = (uint16_t)r[k];
+        if (rowk[k] < a.n_rows) a.ranks[gidx[k] + (uint32_t)f * (uint32_t)a.rank_rows] = (uint16_t)r[k];
     } else {
       uint8_t* xrow = reinterpret_cast<uint8_t*>(xr) + (size_t)f * ROWS * 2;
 #pragma unroll
@@ -1004,14 +1030,16 @@ __global__ void __launch_bounds__(RANK_THREADS, 2) forest_rank_kernel(const Fore
   }
   __syncthreads();
   const int WR = a.rank_rows;
-  int64_t rowk[RPT], gidx[RPT];
+  int64_t rowk[RPT];
+  uint32_t gidx[RPT];  // offsets from this CTA's first walk tile (ROWS / WR tiles of F x WR ranks)
   uint32_t pb[RPT];
   int nbad[RPT];
 #pragma unroll
   for (int k = 0; k < RPT; ++k) {
     rowk[k] = (int64_t)blockIdx.x * ROWS + tid + k * RANK_THREADS;
     const int r = (int)(rowk[k] % WR);
-    gidx[k] = rowk[k] / WR * (int64_t)a.F * WR + (((r >> 6) << 6) | ((r & 31) << 1) | ((r >> 5) & 1));
+    gidx[k] = (uint32_t)((tid + k * RANK_THREADS) / WR) * (uint32_t)(a.F * WR) +
+              (uint32_t)(((r >> 6) << 6) | ((r & 31) << 1) | ((r >> 5) & 1));
     pb[k] = 0;
     nbad[k] = 0;
     if (a.dense_sel && rowk[k] < a.n_rows) {
@@ -1021,6 +1049,7 @@ __global__ void __launch_bounds__(RANK_THREADS, 2) forest_rank_kernel(const Fore
   }
   ForestArgs ar = a;
   ar.stage_off = 0;  // staging buffers at the start of this kernel's shared memory
+  ar.ranks = a.ranks + (int64_t)blockIdx.x * ROWS / WR * a.F * WR;  // this CTA's first walk tile
   rank_tile<RANK_THREADS, RPT, true>(ar, smem, smem, stage_bar, rowk, pb, nbad, gidx, empty_bar);
 }
 
@@ -2174,8 +2203,11 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
   CMLB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f->smem));
   if (f->variant == CMLB_FOREST_RANKED) {
     const char* rp = getenv("CMLB_RANK_PASS");
-    f->rank_pass = !(rp && atoi(rp) == 0) && 2 * (size_t)f->stage_cap * 6 <= SMEM_LIMIT;
+    f->rank_pass = !(rp && atoi(rp) == 0) && 2 * (size_t)f->stage_cap * 6 <= SMEM_LIMIT &&
+                   (RANK_THREADS * RANK_RPT) % (f->ntt * f->rpt) == 0;
   }
+  if (f->variant == CMLB_FOREST_SKEW && (RANK_THREADS * RANK_RPT) % (f->ntt * f->rpt) != 0)
+    return fail(CMLB_E_UNRESOLVED, "skew walk tile does not divide the rank pass tile");
   if (f->variant == CMLB_FOREST_SKEW || (f->variant == CMLB_FOREST_RANKED && f->rank_pass)) {
     f->rank_smem = 2 * (size_t)f->stage_cap * 6;
     CMLB_CUDA(cudaFuncSetAttribute(forest_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f->rank_smem));
@@ -2228,6 +2260,7 @@ static int run_forest(const cmlb_forest* f, const float* x, int64_t n_rows, int6
     a.rank_rows = (int)rows;
     ForestArgs ra = a;
     ra.stage_bufs = 2;
+    ra.vec_x = (!f->pro && (reinterpret_cast<uintptr_t>(x) & 7) == 0 && (ldx % 2) == 0 && (f->F % 2) == 0) ? 1 : 0;
     const int64_t rgrid = ceil_div(n_rows, (int64_t)RANK_THREADS * RANK_RPT);
     forest_rank_kernel<<<(unsigned)rgrid, RANK_THREADS, f->rank_smem, s>>>(ra);
     note_launch();

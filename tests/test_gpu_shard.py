@@ -195,3 +195,48 @@ def test_row_sharded_predict_linear_svm_pipeline():
         got = api.predict(compiled, x, devices=[0, 0])
         want = api.predict(compiled, x)
         assert np.array_equal(got, want), type(model).__name__
+
+
+def test_tree_shard_partials_under_skew():
+    """Tree-shard partials from SKEW programs (certified order-free sums): a
+    single-output regressor built from the RF500 trees' class-1 probabilities
+    (certified) -> shard partials -> pairwise merges -> finish == single program
+    == the C oracle; the shard programs really run SKEW."""
+    from dataclasses import replace
+
+    import bench
+    from paper_2301_13441_b200 import lower, shard
+    from paper_2301_13441_b200.lower import ProgramSpec
+    from paper_2301_13441_b200.models import ForestModel, TreeArrays, TreeModel
+    from paper_2301_13441_b200.runtime import DeviceProgram
+    rf, mu, sigma = bench.load_model()
+    trees = []
+    for t in rf.trees:
+        a = t.arrays
+        v = np.ascontiguousarray(a.value[:, 1:2], np.float32)
+        trees.append(TreeModel("decision_tree_regressor", 28, TreeArrays(a.is_leaf, a.feature, a.threshold, a.left,
+                                                                          a.right, v), None))
+    m = ForestModel("random_forest_regressor", 28, tuple(trees), "mean_probability", 1.0, 0.0, None)
+    spec = lower.lower_model(m).stages[0]
+    ranges, merges = shard.pairwise_tree_shards(len(spec.trees), 3)
+    x = torch.randn((40_000, 28), generator=torch.Generator(device="cuda").manual_seed(8), device="cuda")
+    x.mul_(torch.from_numpy(sigma).cuda()).add_(torch.from_numpy(mu).cuda())
+    n = x.shape[0]
+    sh = torch.cuda.current_stream().cuda_stream
+    progs, parts = [], []
+    for lo, hi in ranges:
+        p = DeviceProgram(ProgramSpec([replace(spec, trees=spec.trees[lo:hi], n_trees_total=len(spec.trees))], 28), 0)
+        assert p.forest().info()["variant"] == "skew"
+        part = torch.empty((n, 1), dtype=torch.float64, device="cuda")
+        p.forest().partial(x, part, n, 28, sh)
+        progs.append(p)
+        parts.append(part)
+    for a_, b_ in merges:
+        progs[a_].forest().merge(parts[a_], parts[b_], n, sh)
+    y = torch.empty((n, 1), dtype=torch.float32, device="cuda")
+    progs[0].forest().finish(parts[0], 1, [], n, y, sh)
+    single = DeviceProgram(ProgramSpec([spec], 28), 0)
+    assert single.forest().info()["variant"] == "skew"
+    assert torch.equal(y, single.run(x))
+    want, _ = fast.forest_predict(fast.PackedForest(m), x.cpu().numpy())
+    assert np.array_equal(y.cpu().numpy().astype(np.float64), want)
