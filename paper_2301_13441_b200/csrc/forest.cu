@@ -529,16 +529,30 @@ template <int R>
 __device__ __forceinline__ void count_less_eyt_n(const float* ue, const uint16_t* map, int n, const float (&x)[R],
                                                  int (&out)[R]) {
   const int levels = n > 0 ? 32 - __clz(n) : 0;
+  // node k (1-based) at shared address base + 4k; a level is one LDS plus
+  // setp / add / predicated add (5 SASS instructions per row-level)
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(ue) - 4u;
   uint32_t k[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) k[r] = 1u;
+  auto step = [&](uint32_t& kk, float u, float xv) {
+    asm("{\n .reg .pred p;\n setp.lt.f32 p, %1, %2;\n add.u32 %0, %3, %3;\n @p add.u32 %0, %0, 1;\n}"
+        : "=r"(kk) : "f"(u), "f"(xv), "r"(kk));
+  };
   for (int l = 0; l + 1 < levels; ++l) {
+    float u[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) k[r] = 2u * k[r] + (ue[k[r] - 1] < x[r] ? 1u : 0u);
+    for (int r = 0; r < R; ++r) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(u[r]) : "r"(base + 4u * k[r]));
+#pragma unroll
+    for (int r = 0; r < R; ++r) step(k[r], u[r], x[r]);
   }
 #pragma unroll
   for (int r = 0; r < R; ++r)
-    if ((int)k[r] <= n) k[r] = 2u * k[r] + (ue[k[r] - 1] < x[r] ? 1u : 0u);
+    if ((int)k[r] <= n) {
+      float u;
+      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(u) : "r"(base + 4u * k[r]));
+      step(k[r], u, x[r]);
+    }
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const uint32_t kk = k[r] >> __ffs(~k[r]);
@@ -718,6 +732,11 @@ __device__ __forceinline__ void rank_tile(const ForestArgs& a, uint8_t* smem, ui
   // features 2g, 2g+1 are one 8-byte load, pair g+1 in flight while pair g is
   // searched.  Otherwise one feature at a time through load_col.
   const bool vec = a.vec_x;
+  uint32_t vmask = 0;  // rows of this thread inside the batch
+#pragma unroll
+  for (int k = 0; k < RPT; ++k) vmask |= (rowk[k] < a.n_rows ? 1u : 0u) << k;
+  asm volatile("mov.b32 %0, %0;" : "+r"(vmask));  // keep the mask (ptxas re-derived it per feature)
+  uint16_t* const rbase = a.ranks;
   float xn[RPT];
   float2 cur[RPT], nxt[RPT];
   auto load_f = [&](int f) {
@@ -783,9 +802,10 @@ __device__ __forceinline__ void rank_tile(const ForestArgs& a, uint8_t* smem, ui
       if ((threadIdx.x & 31) == 0) mbar_arrive(&empty_bar[f & 1]);
     }
     if constexpr (GOUT) {  // rank kernel: straight into the walk tiles in global memory
+      uint16_t* rf = rbase + (uint32_t)f * (uint32_t)a.rank_rows;
 #pragma unroll
       for (int k = 0; k < RPT; ++k)
-        if (rowk[k] < a.n_rows) a.ranks[gidx[k] + (uint32_t)f * (uint32_t)a.rank_rows] = (uint16_t)r[k];
+        if (vmask & (1u << k)) rf[gidx[k]] = (uint16_t)r[k];
     } else {
       uint8_t* xrow = reinterpret_cast<uint8_t*>(xr) + (size_t)f * ROWS * 2;
 #pragma unroll

@@ -23,6 +23,7 @@ if [ -z "$NOPROF" ]; then
 prof prof_certify svm_certify 0 python bench.py --config svc10k --rows 200000 --steps 1 --warmup 3 --no-cpu-baseline --no-parity --e2e-steps 1
 prof prof_rank forest_rank 3 python bench.py --rows 2000000 --steps 1 --warmup 3 --no-cpu-baseline --no-parity --e2e-steps 1
 prof prof_lx linear_exact_lanes 3 python tools/linear_probe.py
+prof prof_gbr forest_ranked 3 python bench.py --config gbr1000 --rows 500000 --steps 1 --warmup 3 --no-cpu-baseline --no-parity --e2e-steps 1
 fi
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv --log-file gpurun_out/launches.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 --no-parity > gpurun_out/ncu_bench.log 2>&1
