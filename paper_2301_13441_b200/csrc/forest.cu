@@ -819,7 +819,7 @@ __global__ void __launch_bounds__(NTT, 1) forest_ranked_kernel(const ForestArgs 
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int ROWS = NTT * RPT;
   static_assert(ROWS % 64 == 0, "rank tile interleave needs 64-row groups");
-  static_assert(TI == 2 || TI == 4, "trees per step");
+  static_assert(TI == 2 || TI == 4 || TI == 8, "trees per step");
   const int tid = threadIdx.x;
   const int64_t tile = (int64_t)blockIdx.x * ROWS;
   const int F = a.F;
@@ -963,6 +963,10 @@ __global__ void __launch_bounds__(NTT, 1) forest_ranked_kernel(const ForestArgs 
     finish_tree(std::integral_constant<int, 1>{});
     finish_tree(std::integral_constant<int, 2>{});
     finish_tree(std::integral_constant<int, 3>{});
+    finish_tree(std::integral_constant<int, 4>{});
+    finish_tree(std::integral_constant<int, 5>{});
+    finish_tree(std::integral_constant<int, 6>{});
+    finish_tree(std::integral_constant<int, 7>{});
   };
 
   auto walk_chunk = [&](auto leafconst, uint32_t buf_off, int c0, int nt) {
@@ -974,9 +978,11 @@ __global__ void __launch_bounds__(NTT, 1) forest_ranked_kernel(const ForestArgs 
           if (tg + 2 < nt) walk_group(std::integral_constant<int, 2>{}, leafconst, buf_off, c0, tg + 2, nt);
           if (tg + 4 < nt) walk_group(std::integral_constant<int, 4>{}, leafconst, buf_off, c0, tg + 4, nt);
           if (tg + 6 < nt) walk_group(std::integral_constant<int, 6>{}, leafconst, buf_off, c0, tg + 6, nt);
-        } else {
+        } else if constexpr (TI == 4) {
           walk_group(std::integral_constant<int, 0>{}, leafconst, buf_off, c0, tg + 0, nt);
           if (tg + 4 < nt) walk_group(std::integral_constant<int, 4>{}, leafconst, buf_off, c0, tg + 4, nt);
+        } else {
+          walk_group(std::integral_constant<int, 0>{}, leafconst, buf_off, c0, tg + 0, nt);
         }
       }
     } else {
@@ -1605,7 +1611,7 @@ static KernelFn pick4(bool perfect, bool xs) {
 struct RankedCfg { int ntt, rpt, ti; };
 constexpr RankedCfg RANKED_CFGS[] = {
     {512, 2, 2}, {512, 2, 4}, {1024, 1, 2}, {1024, 1, 4}, {256, 2, 2}, {256, 1, 2}, {128, 2, 2}, {512, 1, 2},
-    {512, 1, 4}, {256, 2, 4}};
+    {512, 1, 4}, {256, 2, 4}, {512, 1, 8}};
 // (with the replay stack in registers, 512x1 and 256x2 threads with 4 trees per
 // step spilled on GBR1000 d10, 6x slower; with it in local memory 512x1x4 is
 // the fastest scalar shape; tools/gbr_cfg_probe.sh)
@@ -1629,6 +1635,7 @@ static KernelFn ranked_cfg(int cfg) {
     case 7: return forest_ranked_kernel<CT, 512, 1, 2, PW>;
     case 8: return forest_ranked_kernel<CT, 512, 1, 4, PW>;
     case 9: return forest_ranked_kernel<CT, 256, 2, 4, PW>;
+    case 10: return forest_ranked_kernel<CT, 512, 1, 8, PW>;
     default: return nullptr;
   }
 }
