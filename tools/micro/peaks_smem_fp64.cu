@@ -103,6 +103,30 @@ __global__ void __launch_bounds__(THREADS, 1) fp_rate(unsigned long long* cycles
   if (s == 1.2345) sink[0] = s;
 }
 
+// FP64 tensor-core MMA (mma.sync m8n8k4 f64, DMMA): 8 independent accumulator
+// tiles per warp, each instruction 8 x 8 x 4 = 256 FMAs
+__global__ void __launch_bounds__(THREADS, 1) dmma_rate(unsigned long long* cycles, double* sink, float seed) {
+  double acc[8][2];
+  double a = seed * (threadIdx.x + 1), b = seed * 0.5;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) acc[u][0] = acc[u][1] = 0.0;
+  __syncthreads();
+  const long long t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                   : "+d"(acc[u][0]), "+d"(acc[u][1]) : "d"(a), "d"(b));
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  if (threadIdx.x == 0) cycles[blockIdx.x] = (unsigned long long)(t1 - t0);
+  double s = 0;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) s += acc[u][0] + acc[u][1];
+  if (s == 1.2345) sink[0] = s;
+}
+
 template <typename K, typename... A>
 static double per_sm_clk(K kern, int sms, double ops_per_cta, A... args) {
   unsigned long long* cyc;
@@ -138,6 +162,8 @@ int main() {
   const double ffma = per_sm_clk(fp_rate<3>, sms, thread_ops, dsink, 1.0f);
   const double ffma_reg = per_sm_clk(fp_rate<4>, sms, thread_ops, dsink, 1.0f);
   const double ffma2 = per_sm_clk(fp_rate<5>, sms, thread_ops, dsink, 1.0f);  // thread instructions (2 FMAs each)
+  // DMMA: per warp-instruction 256 FMAs -> FMAs per SM per clock
+  const double dmma_fma = per_sm_clk(dmma_rate, sms, (double)(THREADS / 32) * ITERS * 8 * 256, dsink, 1.0f);
   int clk_khz = 0;
   cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev);
   printf("{\"gpu\": \"%s\", \"sms\": %d, \"sm_clock_attr_mhz\": %.0f,\n", p.name, sms, clk_khz / 1e3);
@@ -148,6 +174,8 @@ int main() {
   printf(" \"dadd_per_sm_clk\": %.2f, \"dfma_per_sm_clk\": %.2f, \"f2f_f64_f32_plus_dadd_per_sm_clk\": %.2f, "
          "\"ffma_per_sm_clk\": %.2f, \"ffma_reg_per_sm_clk\": %.2f, \"ffma2_instr_per_sm_clk\": %.2f,\n",
          dadd, dfma, f2f, ffma, ffma_reg, ffma2);
+  printf(" \"dmma_fp64_fma_per_sm_clk\": %.2f, \"dmma_fp64_tflops_at_max_clock\": %.2f,\n", dmma_fma,
+         dmma_fma * 2 * sms * 1965e6 / 1e12);
   printf(" \"fp64_fma_tflops_at_max_clock\": %.2f}\n", dfma * 2 * sms * 1965e6 / 1e12);
   return cudaDeviceSynchronize() != cudaSuccess;
 }

@@ -15,7 +15,7 @@ common = {"gpu": d["gpu"], "sms": d["sms"], "how": "tools/micro/peaks_smem_fp64.
           "8 independent ops per thread per iteration, clock64() per CTA (median CTA)", "nvidia_smi_clocks": clk}
 smem = dict(common, **{k: v for k, v in d.items() if k.startswith("smem_")})
 smem["wavefronts_per_sm_clk"] = d["smem_lds32_conflict_free_warp_instr_per_sm_clk"]
-fp = dict(common, **{k: v for k, v in d.items() if k.startswith(("dadd", "dfma", "f2f", "ffma", "fp64"))})
+fp = dict(common, **{k: v for k, v in d.items() if k.startswith(("dadd", "dfma", "f2f", "ffma", "fp64", "dmma"))})
 json.dump(smem, open("gpurun_out/peaks_smem.json", "w"), indent=1)
 json.dump(fp, open("gpurun_out/peaks_fp64.json", "w"), indent=1)
 print(json.dumps(smem)); print(json.dumps(fp))
