@@ -593,7 +593,8 @@ constexpr int XTHREADS = 256;
 // outputs per thread, K staged in 32-feature float64 chunks (double-buffered);
 // decision sums per (row, pair) task in ascending SV order (deterministic).
 constexpr int CB_ROWS = 64, CB_SV = 64, CB_K = 16, CB_THREADS = 256;
-constexpr int CB_KS = CB_K + 2, CB_SS = CB_SV + 1;              // padded strides (16-byte rows, conflict-free)
+constexpr int CB_KS = CB_K + 4, CB_SS = CB_SV + 1;              // padded strides: KS = 20 doubles puts the DMMA
+                                                                  // fragment loads of a half warp in 16 distinct bank pairs
 constexpr int CB_TPT = 12;                                        // (row, pair) tasks per thread: pairs <= 48
 constexpr int CB_MAXP = CB_TPT * CB_THREADS / CB_ROWS;
 constexpr size_t CB_SMEM = (size_t)2 * (CB_ROWS + CB_SV) * CB_KS * 8 + (size_t)2 * CB_ROWS * CB_SS * 8 + CB_ROWS * 8;
@@ -617,12 +618,17 @@ __global__ void __launch_bounds__(CB_THREADS, 2) svm_certify_kernel(const Args a
   const int F = a.F, C = a.C;
   const int npairs = a.is_svr ? 1 : a.pairs;
   const int ntasks = CB_ROWS * npairs;
-  // thread tile 4 rows x 4 SVs; a warp covers 16 rows x 32 SVs (lane = 4 b + a:
-  // rows r0 + a + 4 i, SVs s0 + b + 8 j), so each 128-bit load of two k values
-  // is one wavefront (4 distinct rows / 8 distinct SVs per warp)
+  // The Gram on the FP64 tensor pipe: mma.sync m8n8k4 f64 (DMMA, 256 FMAs per
+  // instruction; measured at the DFMA rate, 64 FMAs/clk/SM, with 1/8 of the
+  // issue slots and operand traffic).  Warp tile 32 rows x 16 SVs = 4 x 2 MMA
+  // tiles; 8 warps cover the 64 x 64 CTA tile.  Fragments (PTX m8n8k4 .f64):
+  // a = A[g][t], b = B[t][g], c = C[g][2t + {0,1}] with g = lane / 4, t = lane % 4.
   const int warp = tid >> 5, lane = tid & 31;
-  const int r0 = 16 * (warp >> 1) + (lane & 3), s0 = 32 * (warp & 1) + (lane >> 2);
-  const double gF = gamma_n(F + 3);
+  const int gq = lane >> 2, tq = lane & 3;
+  const int rw0 = 32 * (warp >> 2), sw0 = 16 * (warp & 3);
+  // the DMMA accumulation order and internal roundings are the hardware's:
+  // charge 2 roundings per term (covers round-toward-zero adds too)
+  const double gF = gamma_n(2 * F + 6);
   constexpr double U = 1.1102230246251565e-16;
   for (int b0 = blockIdx.x * CB_ROWS; b0 < nq; b0 += gridDim.x * CB_ROWS) {
     const int nb = min(CB_ROWS, nq - b0);
@@ -650,11 +656,11 @@ __global__ void __launch_bounds__(CB_THREADS, 2) svm_certify_kernel(const Args a
     const int nkc = (F + CB_K - 1) / CB_K;
     for (int j0 = 0; j0 < a.n_sv; j0 += CB_SV) {
       const int nj = min(CB_SV, a.n_sv - j0);
-      double g[4][4];
+      double g[4][2][2];  // [row block][SV block][c0, c1]
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) g[i][j] = 0.0;
+        for (int j = 0; j < 2; ++j) g[i][j][0] = g[i][j][1] = 0.0;
       // chunk kc: SVs by cp.async (float64 already), x by a register prefetch
       // of the next chunk (float32 -> float64 on the way into shared memory)
       float xpre[CB_ROWS * CB_K / CB_THREADS];
@@ -708,20 +714,18 @@ __global__ void __launch_bounds__(CB_THREADS, 2) svm_certify_kernel(const Args a
         const double* xb = xc + (kc & 1) * CB_ROWS * CB_KS;
         const double* sb = sc + (kc & 1) * CB_SV * CB_KS;
 #pragma unroll
-        for (int k = 0; k < CB_K; k += 2) {  // fully unrolled: the loads of k + 2 issue ahead of k's DFMAs
-          double2 xv[4], sv[4];
+        for (int k = 0; k < CB_K; k += 4) {
+          double af[4], bf[2];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) xv[i] = *reinterpret_cast<const double2*>(xb + (r0 + 4 * i) * CB_KS + k);
+          for (int i = 0; i < 4; ++i) af[i] = xb[(rw0 + 8 * i + gq) * CB_KS + k + tq];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) sv[j] = *reinterpret_cast<const double2*>(sb + (s0 + 8 * j) * CB_KS + k);
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) g[i][j] = fma(xv[i].x, sv[j].x, g[i][j]);
+          for (int j = 0; j < 2; ++j) bf[j] = sb[(sw0 + 8 * j + gq) * CB_KS + k + tq];
 #pragma unroll
           for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) g[i][j] = fma(xv[i].y, sv[j].y, g[i][j]);
+            for (int j = 0; j < 2; ++j)
+              asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                           : "+d"(g[i][j][0]), "+d"(g[i][j][1]) : "d"(af[i]), "d"(bf[j]));
         }
         if (more) store_x((kc + 1) & 1);
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
@@ -729,13 +733,12 @@ __global__ void __launch_bounds__(CB_THREADS, 2) svm_certify_kernel(const Args a
       }
       // kernel values of this tile and their error bounds against libsvm's
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int r = r0 + 4 * i, jj = s0 + 8 * j;
+      for (int e = 0; e < 16; ++e) {
+          const int i = e >> 2, j = (e >> 1) & 1, h = e & 1;
+          const int r = rw0 + 8 * i + gq, jj = sw0 + 8 * j + 2 * tq + h;
           double kv = 0.0, ek = 0.0;
           if (jj < nj) {
-            const double G = g[i][j], nx = nxs[r], ns = __ldg(a.ns64 + j0 + jj);
+            const double G = g[i][j][h], nx = nxs[r], ns = __ldg(a.ns64 + j0 + jj);
             // G: ours and libsvm's float64 dot products each within gamma_{F+3} sum|x s| <= gamma (nx + ns) / 2
             const double eg = gF * (nx + ns);
             if (a.kernel == CMLB_SVM_RBF) {
@@ -769,7 +772,7 @@ __global__ void __launch_bounds__(CB_THREADS, 2) svm_certify_kernel(const Args a
           }
           ks[r * CB_SS + jj] = kv;
           eks[r * CB_SS + jj] = ek;
-        }
+      }
       __syncthreads();
       // decision sums per (row, pair) task, ascending SV order (libsvm's)
 #pragma unroll
