@@ -797,10 +797,10 @@ __device__ __forceinline__ void rank_tile(const ForestArgs& a, uint8_t* smem, ui
     const int nf = __ldg(a.unf + f);
     int r[RPT];
     count_less_eyt_n<RPT>(fb, mb, nf, xq, r);
-    if (dbl && empty_bar) {
-      __syncwarp();
-      if ((threadIdx.x & 31) == 0) mbar_arrive(&empty_bar[f & 1]);
-    }
+    // every thread releases its own reads (a per-thread release the TMA
+    // refill acquires through warp 0's wait; a lane-0 arrive after __syncwarp
+    // would leave the other lanes' reads unordered for the async proxy)
+    if (dbl && empty_bar) mbar_arrive(&empty_bar[f & 1]);
     if constexpr (GOUT) {  // rank kernel: straight into the walk tiles in global memory
       uint16_t* rf = rbase + (uint32_t)f * (uint32_t)a.rank_rows;
 #pragma unroll
@@ -1050,8 +1050,8 @@ __global__ void __launch_bounds__(RANK_THREADS, 2) forest_rank_kernel(const Fore
   if (tid == 0) {
     mbar_init(&stage_bar[0], 1);
     mbar_init(&stage_bar[1], 1);
-    mbar_init(&empty_bar[0], RANK_THREADS / 32);
-    mbar_init(&empty_bar[1], RANK_THREADS / 32);
+    mbar_init(&empty_bar[0], RANK_THREADS);
+    mbar_init(&empty_bar[1], RANK_THREADS);
     mbar_fence_init();
   }
   __syncthreads();
@@ -1084,7 +1084,6 @@ __global__ void __launch_bounds__(NTT, 1) forest_skew_kernel(const ForestArgs a)
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int ROWS = NTT * RPT;
   constexpr int STEPS = 32 / TI;
-  constexpr int WARPS = NTT / 32;
   static_assert(ROWS % 64 == 0, "rank tile interleave needs 64-row groups");
   static_assert(TI == 2 || TI == 4 || TI == 8 || TI == 16, "walks per step");
   const int tid = threadIdx.x, lane = tid & 31;
@@ -1117,8 +1116,8 @@ __global__ void __launch_bounds__(NTT, 1) forest_skew_kernel(const ForestArgs a)
   if (tid == 0) {
     mbar_init(&tree_bar[0], 1);
     mbar_init(&tree_bar[1], 1);
-    mbar_init(&empty_bar[0], WARPS);
-    mbar_init(&empty_bar[1], WARPS);
+    mbar_init(&empty_bar[0], NTT);
+    mbar_init(&empty_bar[1], NTT);
     mbar_init(&stage_bar[0], 1);
     mbar_init(&stage_bar[1], 1);
     mbar_fence_init();
@@ -1249,10 +1248,9 @@ __global__ void __launch_bounds__(NTT, 1) forest_skew_kernel(const ForestArgs a)
         for (int st = 0; st < STEPS; ++st, rot += 4u) walk_step(std::false_type{}, gofs, g0 + gl, rot);
       }
     }
-    // release this buffer: one arrive per warp; thread 0 refills it with
-    // chunk ci + 2 once every warp has arrived
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_bar[ci & 1]);
+    // release this buffer: one arrive per thread (each orders its own reads
+    // before the refill); thread 0 refills it with chunk ci + 2 once all have
+    mbar_arrive(&empty_bar[ci & 1]);
     if (tid < 32 && ci + 2 < nchunks) {  // warp 0 waits as a whole (no divergent walk)
       mbar_wait(&empty_bar[ci & 1], (uint32_t)(ci >> 1) & 1u);
       if (tid == 0) issue_chunk(ci + 2);

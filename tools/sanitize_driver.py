@@ -29,7 +29,7 @@ def forest():
     from paper_2301_13441_b200.models import ForestModel
     from paper_2301_13441_b200.runtime import DeviceProgram
     model, mu, sigma = bench.load_model()
-    small = ForestModel(model.model_type, model.n_features, model.trees[:40], model.aggregation, 1.0, 0.0,
+    small = ForestModel(model.model_type, model.n_features, model.trees[:160], model.aggregation, 1.0, 0.0,
                         model.classes)
     x = (np.random.default_rng(0).standard_normal((300, 28)) * sigma + mu).astype(np.float32)
     want, _ = fast.forest_predict(fast.PackedForest(small), x)
