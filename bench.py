@@ -172,9 +172,9 @@ def _class_width(c: int) -> int:
 def forest_wavefronts_row(spec, info) -> dict:
     """Algorithmic shared-memory wavefronts per row of the ranked/skew walk:
     per tree D node-word loads + D rank loads + the payload load (CT floats,
-    CT wavefronts per warp of 32), per feature the Eytzinger search
-    (floor(log2 n_f) + 1 levels + the index-map load) and the rank store, all
-    at one wavefront per warp-wide conflict-free access, / 32 rows."""
+    CT wavefronts per warp of 32), per feature the perfect-Eytzinger search
+    (L_f = bit_length(n_f) levels, one load each; the ranks go to global
+    memory), all at one wavefront per warp-wide conflict-free access, / 32 rows."""
     if info["variant"] not in ("ranked", "skew"):
         return None
     D = int(info["depth"])
@@ -186,7 +186,7 @@ def forest_wavefronts_row(spec, info) -> dict:
     search = 0
     for f in np.unique(feats):
         nf = np.unique(thr[feats == f]).size
-        search += int(np.floor(np.log2(nf))) + 1 + 1 + 1
+        search += int(nf).bit_length()
     walk = T_walked * (2 * D + CT)
     return {"walk": walk / 32.0, "rank": search / 32.0, "total": (walk + search) / 32.0,
             "trees_walked": T_walked, "depth": D, "payload_floats": CT}

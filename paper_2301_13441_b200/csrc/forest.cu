@@ -139,11 +139,9 @@ struct ForestArgs {
   const double* classes;
   int pay_off, feat_off;      // byte offsets of payload / feature arrays inside a perfect tree blob
   // ranked variant: per-feature sorted unique thresholds
-  const float* uthr;          // per feature: sorted unique thresholds in Eytzinger (BFS) order
-  const int32_t* uoff;        // [F + 1]
-  const uint16_t* umap;       // per feature: Eytzinger position -> sorted index (even-aligned)
-  const int32_t* moff;        // [F + 1] offsets into umap (multiples of 8 entries)
-  const int32_t* unf;         // [F] distinct thresholds per feature (uoff starts are 4-aligned)
+  const float* uthr;          // per feature: perfect Eytzinger table (see rank_eyt), 2^L - 1 entries
+  const int32_t* uoff;        // [F + 1] table offsets (4-aligned)
+  const int32_t* ulev;        // [F] levels L of each feature's table (0: no thresholds)
   int node_off_bytes;         // byte offset of the node words inside a ranked tree blob
   int stage_off;              // byte offset of the ranking staging area inside the chunk area
   int stage_bufs;             // 1 or 2 staging buffers
@@ -516,48 +514,36 @@ __global__ void __launch_bounds__(NT) forest_kernel(const ForestArgs a) {
 // word (rank << 16 | feature): a tree level costs one node load and one u16
 // rank load instead of feature + threshold + float x loads.
 
-// Count of thresholds < x by an Eytzinger (breadth-first) search: level k of
-// the implicit tree is 2^k consecutive floats, so the first five levels are
-// bank-conflict-free across a warp (a power-of-two binary search over a
-// sorted array sends every lane of a step to the same bank).  The final
-// position is the lower_bound element, mapped back to its sorted index.
-// R searches of one table interleaved (a fixed trip count instead of the
-// data-dependent while loop, so the R dependent load chains overlap).  The
-// implicit tree of n nodes has L = floor(log2 n) + 1 levels, all full but the
-// last: L - 1 unconditional steps, then one step where the node exists.
+// rank(x) = #{u in U_f : u < x} for R values at once.  Each feature's sorted
+// distinct thresholds are stored as a PERFECT implicit search tree: padded with
+// +inf to 2^L - 1 entries and laid out in Eytzinger (BFS) order, node k
+// (1-based) at entry k - 1.  Descending all L levels with k = 2k + (u_k < x)
+// lands on k = 2^L + #{u < x}, so the rank is k - 2^L directly (no map back
+// from the Eytzinger position, no partial last level).  +inf padding is never
+// < x, NaN compares false everywhere (rank 0), x = +inf ranks |U_f|.  The first
+// five levels (at most 31 consecutive nodes) are bank-conflict-free across a
+// warp.  The R searches are interleaved (R independent load chains); a level
+// is one LDS plus setp / add / predicated add.
 template <int R>
-__device__ __forceinline__ void count_less_eyt_n(const float* ue, const uint16_t* map, int n, const float (&x)[R],
-                                                 int (&out)[R]) {
-  const int levels = n > 0 ? 32 - __clz(n) : 0;
-  // node k (1-based) at shared address base + 4k; a level is one LDS plus
-  // setp / add / predicated add (5 SASS instructions per row-level)
-  const uint32_t base = (uint32_t)__cvta_generic_to_shared(ue) - 4u;
-  uint32_t k[R];
+__device__ __forceinline__ void rank_eyt(uint32_t table, int levels, const float (&x)[R], uint32_t (&k)[R]) {
+  // walk the node ADDRESS a = table + 4(k - 1): k' = 2k + c is
+  // a' = 2a - (table - 4) + 4c, one IADD3 and a predicated add per level
+  const uint32_t nb = 4u - table;
 #pragma unroll
-  for (int r = 0; r < R; ++r) k[r] = 1u;
-  auto step = [&](uint32_t& kk, float u, float xv) {
-    asm("{\n .reg .pred p;\n setp.lt.f32 p, %1, %2;\n add.u32 %0, %3, %3;\n @p add.u32 %0, %0, 1;\n}"
-        : "=r"(kk) : "f"(u), "f"(xv), "r"(kk));
-  };
-  for (int l = 0; l + 1 < levels; ++l) {
+  for (int r = 0; r < R; ++r) k[r] = table;
+#pragma unroll 2
+  for (int l = 0; l < levels; ++l) {
     float u[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(u[r]) : "r"(base + 4u * k[r]));
+    for (int r = 0; r < R; ++r) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(u[r]) : "r"(k[r]));
 #pragma unroll
-    for (int r = 0; r < R; ++r) step(k[r], u[r], x[r]);
+    for (int r = 0; r < R; ++r)
+      asm("{\n .reg .pred p;\n setp.lt.f32 p, %1, %2;\n add.u32 %0, %3, %3;\n add.u32 %0, %0, %4;\n"
+          " @p add.u32 %0, %0, 4;\n}"
+          : "=&r"(k[r]) : "f"(u[r]), "f"(x[r]), "r"(k[r]), "r"(nb));
   }
 #pragma unroll
-  for (int r = 0; r < R; ++r)
-    if ((int)k[r] <= n) {
-      float u;
-      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(u) : "r"(base + 4u * k[r]));
-      step(k[r], u, x[r]);
-    }
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const uint32_t kk = k[r] >> __ffs(~k[r]);
-    out[r] = kk ? (int)map[kk - 1] : n;
-  }
+  for (int r = 0; r < R; ++r) k[r] = ((k[r] - table) >> 2) + 1u - (1u << levels);
 }
 
 __device__ __forceinline__ void cp_async4(void* smem_dst, const void* gmem_src) {
@@ -682,135 +668,65 @@ __device__ __forceinline__ void load_payload(const float* p, float (&v)[CT]) {
   }
 }
 
-// Rank the CTA's row tile (both ranked kernels): for every feature f and row
-// r of the tile, rank(x[r][f]) = #{u in U_f : u < x} into the u16 rank tile at
-// the start of shared memory (layout: see the callers' pb()), or (GOUT, the
-// rank pass) into the walk tiles in global memory.
-// Feature f's Eytzinger thresholds + index map are staged with TMA into
-// buffer f&1 of the staging area while the CTA searches feature f-1's buffer
-// (double buffering: one barrier per feature).
-template <int NTT, int RPT, bool GOUT = false>
+// Rank the CTA's row tile inside a walk kernel (RANKED with CMLB_RANK_PASS=0,
+// or a forest whose tables do not fit the rank pass): for every feature f and
+// row r of the tile, rank(x[r][f]) into the u16 rank tile at the start of
+// shared memory (layout: see the callers' pb()).  Feature f's table is staged
+// with TMA into buffer f&1 of the staging area while the CTA searches feature
+// f-1's buffer (a.stage_bufs == 2), or into one buffer (an extra barrier per
+// feature).
+template <int NTT, int RPT>
 __device__ __forceinline__ void rank_tile(const ForestArgs& a, uint8_t* smem, uint8_t* chunk, uint64_t* stage_bar,
                                           const int64_t (&rowk)[RPT], const uint32_t (&pb)[RPT],
-                                          const int (&nbad)[RPT], const uint32_t* gidx = nullptr,
-                                          uint64_t* empty_bar = nullptr) {
+                                          const int (&nbad)[RPT]) {
   constexpr int ROWS = NTT * RPT;
   const int tid = threadIdx.x;
   const int F = a.F;
   uint16_t* xr = reinterpret_cast<uint16_t*>(smem);
-  const int cap = a.stage_cap;  // thresholds per staging buffer
-  // two staging buffers when they fit (a.stage_bufs == 2: prefetch feature f+1
-  // while searching f), else one (an extra barrier per feature)
+  const int cap = a.stage_cap;  // floats per staging buffer
   const bool dbl = a.stage_bufs == 2;
-  auto stage_f = [&](int b) {
-    return reinterpret_cast<float*>(chunk + a.stage_off) + (size_t)(dbl ? b : 0) * (cap + cap / 2);
-  };
-  // feature f's Eytzinger thresholds + index map: two TMA bulk copies by
-  // thread 0 (16-byte aligned, padded arrays), completing on stage_bar
-  auto issue_stage = [&](int f) {
+  auto stage_f = [&](int b) { return reinterpret_cast<float*>(chunk + a.stage_off) + (size_t)(dbl ? b : 0) * cap; };
+  auto issue_stage = [&](int f) {  // thread 0: feature f's table, bulk copies of <= 32 KB
     if (tid != 0) return;
     const int b = dbl ? (f & 1) : 0;
-    float* fb = stage_f(b);
-    uint8_t* mb = reinterpret_cast<uint8_t*>(fb + cap);
-    const int nf = __ldg(a.unf + f);
-    const uint32_t tbytes = (uint32_t)((nf + 3) & ~3) * 4u, mbytes = (uint32_t)((nf + 7) & ~7) * 2u;
+    uint8_t* fb = reinterpret_cast<uint8_t*>(stage_f(b));
+    const uint32_t bytes = (uint32_t)(__ldg(a.uoff + f + 1) - __ldg(a.uoff + f)) * 4u;
     const uint8_t* ts = reinterpret_cast<const uint8_t*>(a.uthr + __ldg(a.uoff + f));
-    const uint8_t* ms = reinterpret_cast<const uint8_t*>(a.umap + __ldg(a.moff + f));
     fence_proxy_async();
-    mbar_expect_tx(&stage_bar[b], tbytes + mbytes);
-    for (uint32_t off = 0; off < tbytes; off += 32768u)
-      bulk_g2s(reinterpret_cast<uint8_t*>(fb) + off, ts + off, min(32768u, tbytes - off), &stage_bar[b]);
-    for (uint32_t off = 0; off < mbytes; off += 32768u)
-      bulk_g2s(mb + off, ms + off, min(32768u, mbytes - off), &stage_bar[b]);
+    mbar_expect_tx(&stage_bar[b], bytes);
+    for (uint32_t off = 0; off < bytes; off += 32768u)
+      bulk_g2s(fb + off, ts + off, min(32768u, bytes - off), &stage_bar[b]);
   };
   issue_stage(0);
-  // one feature per iteration (a rolled loop: the unrolled 8-feature groups
-  // of round 1 made the rank pass ~200 KB of SASS and 21% of its stalls were
-  // instruction fetch); the next feature's row values are loaded before this
-  // feature's searches so their latency hides behind them
-  // Vector path (plain row-major x, 8-byte aligned rows, even F): each row's
-  // features 2g, 2g+1 are one 8-byte load, pair g+1 in flight while pair g is
-  // searched.  Otherwise one feature at a time through load_col.
-  const bool vec = a.vec_x;
-  uint32_t vmask = 0;  // rows of this thread inside the batch
-#pragma unroll
-  for (int k = 0; k < RPT; ++k) vmask |= (rowk[k] < a.n_rows ? 1u : 0u) << k;
-  asm volatile("mov.b32 %0, %0;" : "+r"(vmask));  // keep the mask (ptxas re-derived it per feature)
-  uint16_t* const rbase = a.ranks;
   float xn[RPT];
-  float2 cur[RPT], nxt[RPT];
   auto load_f = [&](int f) {
 #pragma unroll
     for (int k = 0; k < RPT; ++k)
       xn[k] = (rowk[k] < a.n_rows && f < F) ? load_col(a.pro, a.x + rowk[k] * a.ldx, f) : 0.0f;
   };
-  auto load2 = [&](int g, float2 (&dst)[RPT]) {
-#pragma unroll
-    for (int k = 0; k < RPT; ++k)
-      dst[k] = (rowk[k] < a.n_rows && g < F) ? __ldg(reinterpret_cast<const float2*>(a.x + rowk[k] * a.ldx + g))
-                                             : make_float2(0.f, 0.f);
-  };
-  if (vec) {
-    load2(0, cur);
-    load2(2, nxt);
-  } else {
-    load_f(0);
-  }
+  load_f(0);
 #pragma unroll 1
   for (int f = 0; f < F; ++f) {
     float xq[RPT];
-    const bool hi = f & 1;
 #pragma unroll
     for (int k = 0; k < RPT; ++k) {
-      float v = vec ? (hi ? cur[k].y : cur[k].x) : xn[k];
+      float v = xn[k];
       if (nbad[k] && rowk[k] < a.n_rows && (nbad[k] >= 2 || isfinite(v))) v = __int_as_float(0x7fc00000);
       xq[k] = v;
     }
-    if (vec) {
-      if (hi) {
-#pragma unroll
-        for (int k = 0; k < RPT; ++k) cur[k] = nxt[k];
-        if (f + 3 < F) load2(f + 3, nxt);
-      }
-    } else if (f + 1 < F) {
-      load_f(f + 1);
-    }
+    if (f + 1 < F) load_f(f + 1);
     if (!dbl && f > 0) {
       __syncthreads();  // everyone done searching f-1 in the single buffer
       issue_stage(f);
     }
     mbar_wait(&stage_bar[dbl ? (f & 1) : 0], (uint32_t)((dbl ? (f >> 1) : f) & 1));
-    if (dbl && empty_bar) {
-      // per-warp release (no CTA barrier per feature): buffer (f+1)&1 held
-      // feature f-1; warp 0 alone waits until every warp is done with it
-      if (threadIdx.x < 32 && f + 1 < F) {
-        if (f >= 1) mbar_wait(&empty_bar[(f + 1) & 1], (uint32_t)(((f - 1) >> 1) & 1));
-        issue_stage(f + 1);
-        __syncwarp();
-      }
-    } else {
-      __syncthreads();  // stage f landed for everyone; buffer (f+1)&1 is free
-      if (dbl && f + 1 < F) issue_stage(f + 1);
-    }
-    const float* fb = stage_f(f & 1);
-    const uint16_t* mb = reinterpret_cast<const uint16_t*>(fb + cap);
-    const int nf = __ldg(a.unf + f);
-    int r[RPT];
-    count_less_eyt_n<RPT>(fb, mb, nf, xq, r);
-    // every thread releases its own reads (a per-thread release the TMA
-    // refill acquires through warp 0's wait; a lane-0 arrive after __syncwarp
-    // would leave the other lanes' reads unordered for the async proxy)
-    if (dbl && empty_bar) mbar_arrive(&empty_bar[f & 1]);
-    if constexpr (GOUT) {  // rank kernel: straight into the walk tiles in global memory
-      uint16_t* rf = rbase + (uint32_t)f * (uint32_t)a.rank_rows;
+    __syncthreads();  // stage f landed for everyone; buffer (f+1)&1 is free
+    if (dbl && f + 1 < F) issue_stage(f + 1);
+    uint32_t r[RPT];
+    rank_eyt<RPT>(smem_u32(stage_f(f & 1)), __ldg(a.ulev + f), xq, r);
+    uint8_t* xrow = reinterpret_cast<uint8_t*>(xr) + (size_t)f * ROWS * 2;
 #pragma unroll
-      for (int k = 0; k < RPT; ++k)
-        if (vmask & (1u << k)) rf[gidx[k]] = (uint16_t)r[k];
-    } else {
-      uint8_t* xrow = reinterpret_cast<uint8_t*>(xr) + (size_t)f * ROWS * 2;
-#pragma unroll
-      for (int k = 0; k < RPT; ++k) *reinterpret_cast<uint16_t*>(xrow + pb[k]) = (uint16_t)r[k];
-    }
+    for (int k = 0; k < RPT; ++k) *reinterpret_cast<uint16_t*>(xrow + pb[k]) = (uint16_t)r[k];
   }
 }
 
@@ -1041,42 +957,136 @@ __global__ void __launch_bounds__(NTT, 1) forest_ranked_kernel(const ForestArgs 
 // straight into the walk tiles' interleaved layout, which the walk then
 // bulk-copies (28 KB per 512-row tile for F = 28).
 constexpr int RANK_THREADS = 256, RANK_RPT = 8;
+// NB staging buffers: features f .. f+NB-2 are in flight while f is searched;
+// warp 0 refills the buffer feature f-1 used once every thread has released it
+// (per-thread arrive on empty_bar).  Rows: warp w owns rows [256w, 256w + 256)
+// of the CTA's 2,048; lane l handles rows R = 256w + 64p + 32h + l (p < 4,
+// h < 2), so rows R and R + 32 -- one 32-bit word of the walk tile layout --
+// belong to the same thread and every warp stores whole 128-byte lines.
+template <int NB>
 __global__ void __launch_bounds__(RANK_THREADS, 2) forest_rank_kernel(const ForestArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ __align__(8) uint64_t stage_bar[2];
-  __shared__ __align__(8) uint64_t empty_bar[2];
-  constexpr int RPT = RANK_RPT, ROWS = RANK_THREADS * RANK_RPT;
-  const int tid = threadIdx.x;
+  __shared__ __align__(8) uint64_t full_bar[NB];
+  __shared__ __align__(8) uint64_t empty_bar[NB];
+  constexpr int RPT = RANK_RPT, ROWS = RANK_THREADS * RANK_RPT, NP = RPT / 2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int F = a.F, WR = a.rank_rows;
   if (tid == 0) {
-    mbar_init(&stage_bar[0], 1);
-    mbar_init(&stage_bar[1], 1);
-    mbar_init(&empty_bar[0], RANK_THREADS);
-    mbar_init(&empty_bar[1], RANK_THREADS);
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(&full_bar[b], 1);
+      mbar_init(&empty_bar[b], RANK_THREADS);
+    }
     mbar_fence_init();
   }
   __syncthreads();
-  const int WR = a.rank_rows;
+  const uint32_t stage0 = smem_u32(smem), stage_bytes = (uint32_t)a.stage_cap * 4u;
+  auto issue = [&](int f, int b) {  // thread 0: feature f's table into buffer b
+    const uint32_t bytes = (uint32_t)(__ldg(a.uoff + f + 1) - __ldg(a.uoff + f)) * 4u;
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(a.uthr + __ldg(a.uoff + f));
+    uint8_t* dst = smem + (size_t)b * stage_bytes;
+    fence_proxy_async();
+    mbar_expect_tx(&full_bar[b], bytes);
+    for (uint32_t off = 0; off < bytes; off += 32768u)
+      bulk_g2s(dst + off, src + off, min(32768u, bytes - off), &full_bar[b]);
+  };
+  if (tid == 0)
+    for (int f = 0; f < NB - 1 && f < F; ++f) issue(f, f);
+
+  const int64_t row0 = (int64_t)blockIdx.x * ROWS;
   int64_t rowk[RPT];
-  uint32_t gidx[RPT];  // offsets from this CTA's first walk tile (ROWS / WR tiles of F x WR ranks)
-  uint32_t pb[RPT];
+  uint32_t soff[NP];  // byte offset of the (R, R + 32) word in the CTA's walk tiles, feature 0
+  uint32_t sok = 0;   // bit p: the word's walk tile exists
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    const int R = warp * 256 + 64 * p + lane;
+    rowk[2 * p] = row0 + R;
+    rowk[2 * p + 1] = row0 + R + 32;
+    const int t = R / WR, r = R % WR;
+    soff[p] = (uint32_t)t * (uint32_t)(F * WR * 2) + 4u * (uint32_t)((r >> 6) * 32 + (r & 31));
+    sok |= (row0 + (int64_t)t * WR < a.n_rows ? 1u : 0u) << p;
+  }
+  uint8_t* const rbase = reinterpret_cast<uint8_t*>(a.ranks) + (row0 / WR) * (int64_t)F * WR * 2;
+  // dense-selector NaN poisoning (the reference's 0 * inf): rows with non-finite features
   int nbad[RPT];
+  bool anybad = false;
 #pragma unroll
   for (int k = 0; k < RPT; ++k) {
-    rowk[k] = (int64_t)blockIdx.x * ROWS + tid + k * RANK_THREADS;
-    const int r = (int)(rowk[k] % WR);
-    gidx[k] = (uint32_t)((tid + k * RANK_THREADS) / WR) * (uint32_t)(a.F * WR) +
-              (uint32_t)(((r >> 6) << 6) | ((r & 31) << 1) | ((r >> 5) & 1));
-    pb[k] = 0;
     nbad[k] = 0;
     if (a.dense_sel && rowk[k] < a.n_rows) {
       const float* src = a.x + rowk[k] * a.ldx;
-      for (int f = 0; f < a.F; ++f) nbad[k] += !isfinite(load_col(a.pro, src, f));
+      for (int f = 0; f < F; ++f) nbad[k] += !isfinite(load_col(a.pro, src, f));
+    }
+    anybad |= nbad[k] != 0;
+  }
+  // row values: vec path (plain row-major x, 8-byte aligned rows, even F)
+  // loads features 2g, 2g+1 of a row as one float2, pair g+1 in flight while
+  // pair g is searched; otherwise one feature at a time through load_col
+  const bool vec = a.vec_x;
+  const float* xp[RPT];
+#pragma unroll
+  for (int k = 0; k < RPT; ++k) xp[k] = rowk[k] < a.n_rows ? a.x + rowk[k] * a.ldx : nullptr;
+  float xn[RPT];
+  float2 cur[RPT], nxt[RPT];
+  auto load_f = [&](int f) {
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) xn[k] = (xp[k] && f < F) ? load_col(a.pro, xp[k], f) : 0.0f;
+  };
+  auto load2 = [&](int g, float2 (&dst)[RPT]) {
+#pragma unroll
+    for (int k = 0; k < RPT; ++k)
+      dst[k] = (xp[k] && g < F) ? __ldg(reinterpret_cast<const float2*>(xp[k] + g)) : make_float2(0.f, 0.f);
+  };
+  if (vec) {
+    load2(0, cur);
+    load2(2, nxt);
+  } else {
+    load_f(0);
+  }
+  int b = 0;
+  uint32_t ph = 0;
+  uint32_t fo = 0;  // feature byte offset inside a walk tile
+#pragma unroll 1
+  for (int f = 0; f < F; ++f) {
+    float xq[RPT];
+    const bool hi = f & 1;
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) xq[k] = vec ? (hi ? cur[k].y : cur[k].x) : xn[k];
+    if (anybad) {
+#pragma unroll
+      for (int k = 0; k < RPT; ++k)
+        if (nbad[k] && (nbad[k] >= 2 || isfinite(xq[k]))) xq[k] = __int_as_float(0x7fc00000);
+    }
+    if (vec) {
+      if (hi) {
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) cur[k] = nxt[k];
+        if (f + 3 < F) load2(f + 3, nxt);
+      }
+    } else if (f + 1 < F) {
+      load_f(f + 1);
+    }
+    mbar_wait(&full_bar[b], ph);
+    if (warp == 0 && f + NB - 1 < F) {
+      // refill the buffer feature f-1 used with feature f+NB-1
+      const int g = f + NB - 1, gb = (b + NB - 1) % NB;
+      if (f >= 1) mbar_wait(&empty_bar[gb], (uint32_t)(((f - 1) / NB) & 1));
+      if (lane == 0) issue(g, gb);
+      __syncwarp();
+    }
+    uint32_t r[RPT];
+    rank_eyt<RPT>(stage0 + (uint32_t)b * stage_bytes, __ldg(a.ulev + f), xq, r);
+    mbar_arrive(&empty_bar[b]);  // each thread releases its own reads of buffer b
+#pragma unroll
+    for (int p = 0; p < NP; ++p)
+      if (sok & (1u << p))
+        *reinterpret_cast<uint32_t*>(rbase + fo + soff[p]) = r[2 * p] | (r[2 * p + 1] << 16);
+    fo += (uint32_t)WR * 2u;
+    if (++b == NB) {
+      b = 0;
+      ph ^= 1u;
     }
   }
-  ForestArgs ar = a;
-  ar.stage_off = 0;  // staging buffers at the start of this kernel's shared memory
-  ar.ranks = a.ranks + (int64_t)blockIdx.x * ROWS / WR * a.F * WR;  // this CTA's first walk tile
-  rank_tile<RANK_THREADS, RPT, true>(ar, smem, smem, stage_bar, rowk, pb, nbad, gidx, empty_bar);
 }
 
 template <int CT, int NTT, int RPT, int TI, int DT>
@@ -1551,11 +1561,10 @@ struct cmlb_forest {
   double* classes = nullptr;
   float* uthr = nullptr;
   int32_t* uoff = nullptr;
-  uint16_t* umap = nullptr;
-  int32_t* moff = nullptr;
-  int32_t* unf = nullptr;
+  int32_t* ulev = nullptr;
   int ntt = 256, stage_cap = 0, node_off_bytes = 0, rcfg = 0, stage_off = 0, stage_bufs = 2;
-  size_t rank_smem = 0;  // SKEW / RANKED: forest_rank_kernel's two staging buffers
+  size_t rank_smem = 0;  // SKEW / RANKED: forest_rank_kernel's staging buffers
+  int rank_nb = 3;       // forest_rank_kernel staging depth (2 or 3)
   bool rank_pass = true; // RANKED: rank in a separate pass (CMLB_RANK_PASS=0: fused per tile)
   int mma_k = 0, mma_n = 0, mma_feat_off = 0, mma_thr_off = 0, mma_pay_off = 0;
   cmlb_column_op* pro = nullptr;  // fused preprocessing
@@ -1564,7 +1573,7 @@ struct cmlb_forest {
     cudaFree(pro);
     cudaFree(blob); cudaFree(slot_leaf); cudaFree(gnode); cudaFree(node_off);
     cudaFree(gpay); cudaFree(leaf_off); cudaFree(sched); cudaFree(classes);
-    cudaFree(uthr); cudaFree(uoff); cudaFree(umap); cudaFree(moff); cudaFree(unf);
+    cudaFree(uthr); cudaFree(uoff); cudaFree(ulev);
   }
 };
 
@@ -1894,6 +1903,15 @@ static bool sums_order_free(const cmlb_forest_desc* d, int* q_out = nullptr, boo
   return std::ldexp(bound * (1.0 + 1e-12), q) < 9007199254740992.0;  // 2^53
 }
 
+// Perfect Eytzinger table of n distinct thresholds (rank_eyt): L levels,
+// 2^L - 1 nodes, stored rounded up to whole 16-byte units.
+static int eyt_levels(size_t n) {
+  int L = 0;
+  while (((size_t)1 << L) - 1 < n) ++L;
+  return L;
+}
+static size_t eyt_floats(size_t n) { return ((((size_t)1 << eyt_levels(n)) - 1) + 3) / 4 * 4; }
+
 static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out) {
   if (int s = validate(d)) return s;
   std::unique_ptr<cmlb_forest> f(new cmlb_forest());
@@ -2001,9 +2019,9 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
       f->rcfg = ci; f->rpt = rpt;
       if (ranked_for(*f) == nullptr) continue;        // not instantiated for this shape
       if ((size_t)f->F * rows / 2 > 65535) continue;  // feature word offset must fit 16 bits
-      const size_t cap = (max_nf + 7) / 8 * 8;
+      const size_t cap = eyt_floats(max_nf);
       const size_t xr = ((size_t)f->F * rows * 2 + 15) / 16 * 16;
-      if (xr + cap * 6 > SMEM_LIMIT) continue;
+      if (xr + cap * 4 > SMEM_LIMIT) continue;
       const size_t avail = SMEM_LIMIT - xr;
       // two tree buffers (double-buffered TMA), trees per buffer a multiple of 8
       int chunk = (int)(avail / (2 * (size_t)r_tree_bytes)) / 8 * 8;
@@ -2011,8 +2029,8 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
       chunk = std::min(chunk, (f->T + 7) / 8 * 8);
       const size_t buf = (size_t)chunk * r_tree_bytes;
       // staging: double buffer if it fits next to the tree buffers, else single
-      int nbufs = xr + std::max(2 * buf, 2 * cap * 6) <= SMEM_LIMIT ? 2 : 1;
-      const size_t stage_bytes = (size_t)nbufs * cap * 6;
+      int nbufs = xr + std::max(2 * buf, 2 * cap * 4) <= SMEM_LIMIT ? 2 : 1;
+      const size_t stage_bytes = (size_t)nbufs * cap * 4;
       if (xr + std::max(2 * buf, stage_bytes) > SMEM_LIMIT) continue;
       r_ntt = ntt; r_rpt = rpt;
       r_chunk = chunk;
@@ -2058,14 +2076,14 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
       if (ci < 0 || ci >= N_SKEW_CFGS) continue;
       const int rows = SKEW_CFGS[ci].ntt * SKEW_CFGS[ci].rpt;
       if ((size_t)f->F * rows / 2 > 65535) continue;
-      const size_t cap = (max_nf + 7) / 8 * 8;
+      const size_t cap = eyt_floats(max_nf);
       const size_t xr = ((size_t)f->F * rows * 2 + 15) / 16 * 16;
-      if (xr + cap * 6 > SMEM_LIMIT || xr + 2 * (size_t)s_gbytes > SMEM_LIMIT) continue;
+      if (xr + cap * 4 > SMEM_LIMIT || xr + 2 * (size_t)s_gbytes > SMEM_LIMIT) continue;
       const int G = (f->T + 31) / 32;
       const int groups = std::min<int>((int)((SMEM_LIMIT - xr) / (2 * (size_t)s_gbytes)), G);
       const size_t buf = (size_t)groups * s_gbytes;
-      const int nbufs = xr + std::max(2 * buf, 2 * cap * 6) <= SMEM_LIMIT ? 2 : 1;
-      const size_t stage_bytes = (size_t)nbufs * cap * 6;
+      const int nbufs = xr + std::max(2 * buf, 2 * cap * 4) <= SMEM_LIMIT ? 2 : 1;
+      const size_t stage_bytes = (size_t)nbufs * cap * 4;
       if (xr + std::max(2 * buf, stage_bytes) > SMEM_LIMIT) continue;
       s_cfg = ci; s_ntt = SKEW_CFGS[ci].ntt; s_rpt = SKEW_CFGS[ci].rpt; s_groups = groups;
       s_stage = (int)cap; s_stage_bufs = nbufs; s_stage_off = stage_bytes <= buf ? (int)buf : 0;
@@ -2131,45 +2149,36 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
     if (int st = upload(&f->slot_leaf, slot_leaf.data(), slot_leaf.size())) return st;
   }
   if (f->variant == CMLB_FOREST_RANKED || f->variant == CMLB_FOREST_SKEW) {
-    // per feature: Eytzinger order of the sorted unique thresholds + the map
-    // from Eytzinger position back to sorted index
+    // per feature: the sorted unique thresholds padded with +inf to a perfect
+    // implicit tree of 2^L - 1 nodes, in Eytzinger (BFS) order (rank_eyt)
     std::vector<float> uthr;
-    std::vector<uint16_t> umap;
-    std::vector<int32_t> uoff(f->F + 1, 0), moff(f->F + 1, 0), unf(f->F, 0);
+    std::vector<int32_t> uoff(f->F + 1, 0), ulev(f->F, 0);
     for (int k = 0; k < f->F; ++k) {
       const auto& u = U[k];
-      const size_t n = u.size();
-      std::vector<float> e(n);
-      std::vector<uint16_t> m(n);
+      const int L = eyt_levels(u.size());
+      const size_t P = ((size_t)1 << L) - 1;
+      std::vector<float> e(P);
       size_t next = 0;
       // in-order walk of the implicit tree assigns sorted elements to BFS slots
-      std::vector<std::pair<size_t, bool>> st;
+      std::vector<size_t> st;
       size_t node = 1;
-      while (node <= n || !st.empty()) {
-        if (node <= n) { st.push_back({node, false}); node = 2 * node; continue; }
-        node = st.back().first;
+      while (node <= P || !st.empty()) {
+        if (node <= P) { st.push_back(node); node = 2 * node; continue; }
+        node = st.back();
         st.pop_back();
-        e[node - 1] = u[next];
-        m[node - 1] = (uint16_t)next;
+        e[node - 1] = next < u.size() ? u[next] : INFINITY;
         ++next;
         node = 2 * node + 1;
       }
-      // each feature's arrays start 16-byte aligned and span whole 16-byte
-      // units, so the kernel stages them with two TMA bulk copies
-      unf[k] = (int32_t)n;
+      // each table starts 16-byte aligned and spans whole 16-byte units (TMA)
+      ulev[k] = L;
       uthr.insert(uthr.end(), e.begin(), e.end());
-      while (uthr.size() % 4) uthr.push_back(0.0f);
+      while (uthr.size() % 4) uthr.push_back(INFINITY);
       uoff[k + 1] = (int32_t)uthr.size();
-      moff[k] = (int32_t)umap.size();
-      umap.insert(umap.end(), m.begin(), m.end());
-      while (umap.size() % 8) umap.push_back(0);
     }
-    moff[f->F] = (int32_t)umap.size();
     if (int st = upload(&f->uthr, uthr.data(), uthr.size())) return st;
     if (int st = upload(&f->uoff, uoff.data(), uoff.size())) return st;
-    if (int st = upload(&f->umap, umap.data(), umap.size())) return st;
-    if (int st = upload(&f->moff, moff.data(), moff.size())) return st;
-    if (int st = upload(&f->unf, unf.data(), unf.size())) return st;
+    if (int st = upload(&f->ulev, ulev.data(), ulev.size())) return st;
   }
 
   if (f->variant == CMLB_FOREST_SKEW) {
@@ -2228,14 +2237,21 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
   CMLB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f->smem));
   if (f->variant == CMLB_FOREST_RANKED) {
     const char* rp = getenv("CMLB_RANK_PASS");
-    f->rank_pass = !(rp && atoi(rp) == 0) && 2 * (size_t)f->stage_cap * 6 <= SMEM_LIMIT &&
+    f->rank_pass = !(rp && atoi(rp) == 0) && 2 * (size_t)f->stage_cap * 4 <= SMEM_LIMIT &&
                    (RANK_THREADS * RANK_RPT) % (f->ntt * f->rpt) == 0;
   }
   if (f->variant == CMLB_FOREST_SKEW && (RANK_THREADS * RANK_RPT) % (f->ntt * f->rpt) != 0)
     return fail(CMLB_E_UNRESOLVED, "skew walk tile does not divide the rank pass tile");
   if (f->variant == CMLB_FOREST_SKEW || (f->variant == CMLB_FOREST_RANKED && f->rank_pass)) {
-    f->rank_smem = 2 * (size_t)f->stage_cap * 6;
-    CMLB_CUDA(cudaFuncSetAttribute(forest_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f->rank_smem));
+    // three staging buffers when two CTAs per SM still fit (RF500: 3 x 32 KB),
+    // else two; CMLB_RANK_NB forces one (measurement knob)
+    const size_t table = (size_t)f->stage_cap * 4;
+    f->rank_nb = 3 * table <= SMEM_LIMIT / 2 - 1024 ? 3 : 2;
+    if (const char* nb = getenv("CMLB_RANK_NB")) f->rank_nb = atoi(nb) == 2 ? 2 : 3;
+    if ((size_t)f->rank_nb * table > SMEM_LIMIT) f->rank_nb = 2;
+    f->rank_smem = (size_t)f->rank_nb * table;
+    CMLB_CUDA(cudaFuncSetAttribute(f->rank_nb == 3 ? forest_rank_kernel<3> : forest_rank_kernel<2>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f->rank_smem));
   }
   *out = f.release();
   return CMLB_OK;
@@ -2258,7 +2274,7 @@ static int run_forest(const cmlb_forest* f, const float* x, int64_t n_rows, int6
   a.agg = f->agg; a.tail = f->tail; a.out_dt = f->out_dt; a.dense_sel = f->dense_sel;
   a.n_classes = f->n_classes; a.lr = f->lr; a.base = f->base; a.classes = f->classes;
   a.pay_off = f->pay_off; a.feat_off = f->feat_off;
-  a.uthr = f->uthr; a.uoff = f->uoff; a.umap = f->umap; a.moff = f->moff; a.unf = f->unf; a.stage_cap = f->stage_cap; a.node_off_bytes = f->node_off_bytes; a.stage_off = f->stage_off; a.stage_bufs = f->stage_bufs;
+  a.uthr = f->uthr; a.uoff = f->uoff; a.ulev = f->ulev; a.stage_cap = f->stage_cap; a.node_off_bytes = f->node_off_bytes; a.stage_off = f->stage_off; a.stage_bufs = f->stage_bufs;
   KernelFn k = kernel_for(*f);
   a.mma_k = f->mma_k; a.mma_n = f->mma_n; a.mma_feat_off = f->mma_feat_off; a.mma_thr_off = f->mma_thr_off;
   a.mma_pay_off = f->mma_pay_off;
@@ -2287,7 +2303,10 @@ static int run_forest(const cmlb_forest* f, const float* x, int64_t n_rows, int6
     ra.stage_bufs = 2;
     ra.vec_x = (!f->pro && (reinterpret_cast<uintptr_t>(x) & 7) == 0 && (ldx % 2) == 0 && (f->F % 2) == 0) ? 1 : 0;
     const int64_t rgrid = ceil_div(n_rows, (int64_t)RANK_THREADS * RANK_RPT);
-    forest_rank_kernel<<<(unsigned)rgrid, RANK_THREADS, f->rank_smem, s>>>(ra);
+    if (f->rank_nb == 3)
+      forest_rank_kernel<3><<<(unsigned)rgrid, RANK_THREADS, f->rank_smem, s>>>(ra);
+    else
+      forest_rank_kernel<2><<<(unsigned)rgrid, RANK_THREADS, f->rank_smem, s>>>(ra);
     note_launch();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {

@@ -82,3 +82,23 @@ def test_json_profile_file(tmp_path, capsys):
         lower.load_profile(str(bad))
     with pytest.raises(ProfileError):
         lower.load_profile(str(tmp_path / "missing.json"))
+
+
+REF = os.path.join(ROOT, "baseline", "_ref")
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.isdir(os.path.join(REF, "mlower")), reason="reference not installed in baseline/_ref")
+@pytest.mark.parametrize("name", ["sk_rf24_d8", "sk_gbr12_d6", "sk_logreg_784x10"])
+def test_verify_against_the_reference_oracle(name, tmp_path):
+    """`verify` (reference cli.py:112-127) on the GPU path: boundary rows
+    (one per threshold, cli.py:61-68) plus random rows, compared with the
+    reference's own scalar oracle from the installed reference."""
+    mp = tmp_path / "m.json"
+    mp.write_text(gc.get(name).entry["model_json"])
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([REF, ROOT]))
+    r = subprocess.run([sys.executable, "-m", "paper_2301_13441_b200", "verify", "--model", str(mp), "--random", "300"],
+                       cwd=ROOT, capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "result: PASS" in r.stdout
+    assert "max_abs_divergence=0.0" in r.stdout or "mode=tolerance" in r.stdout

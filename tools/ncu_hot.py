@@ -17,3 +17,11 @@ print(f"total stall samples {tot_s}, warp instructions {tot_i}")
 print("-- top 40 by stall samples")
 for s, n, i, src in sorted(data, reverse=True)[:40]:
     print(f"{s / tot_s:6.3f} {n / tot_i:6.3f} {i:5d} {src[:90]}")
+print("-- top 60 by instructions executed")
+for s, n, i, src in sorted(data, key=lambda d: -d[1])[:60]:
+    print(f"{s / tot_s:6.3f} {n / tot_i:6.3f} {i:5d} {src[:90]}")
+if len(sys.argv) > 2:  # full listing of executed lines: index, warp instructions, stall samples, SASS
+    with open(sys.argv[2], "w") as fh:
+        for s, n, i, src in data:
+            if n or s:
+                fh.write(f"{i}\t{n}\t{s}\t{src[:100]}\n")
