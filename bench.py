@@ -102,21 +102,64 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi sampled during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock and throttle reasons sampled DURING the timed region
+    (B200_PROFILING.md clocks line).  NVML polled every 2 ms from a thread, so
+    even a few-millisecond region (LR, DT6 configs) gets samples; nvidia-smi
+    (-lms 50, first sample ~100 ms late) is the fallback."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, gpu: int):
-        self.gpu = gpu
+    def __init__(self, dev):
+        self.dev = dev
         self.proc = None
         self.lines = []
+        self.samples = []  # (sm_mhz, max_mhz, reasons)
+        self.stop = threading.Event()
+        self.t = None
+
+    def _nvml_handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        import torch
+        p = torch.cuda.get_device_properties(self.dev)
+        return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(
+            f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0")
+
+    def _sample(self):
+        nv, h = self.nv
+        bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+        try:
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.samples.append((float(sm), float(self.mx), {n for n, b in zip(self.NAMES, bits) if r & b}))
+        except Exception:
+            pass
+
+    def _poll(self):
+        while not self.stop.is_set():
+            self._sample()
+            self.stop.wait(0.002)
 
     def __enter__(self):
         try:
+            self.nv = self._nvml_handle()
+            self.mx = self.nv[0].nvmlDeviceGetMaxClockInfo(self.nv[1], self.nv[0].NVML_CLOCK_SM)
+            # the launch loop holds the GIL; a short switch interval lets the
+            # poller run during a few-millisecond region
+            self.switch = sys.getswitchinterval()
+            sys.setswitchinterval(1e-4)
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.t = None
+        try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                ["nvidia-smi", "-i", str(self.dev.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
                  "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -129,16 +172,26 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        if self.t is not None and self.proc is None:
+            self._sample()  # the GPU finished the region microseconds ago
+        self.stop.set()
+        if self.proc is None and self.t is not None:
+            sys.setswitchinterval(self.switch)
         if self.proc is not None:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+        elif self.t is not None:
+            self.t.join(timeout=1)
 
     def summary(self):
         sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for a, b, r in self.samples:
+            sm.append(a)
+            mx.append(b)
+            reasons |= r
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 9:
@@ -148,13 +201,13 @@ class ClockSampler:
                 mx.append(float(parts[2]))
             except ValueError:
                 continue
-            for n, v in zip(names, parts[5:9]):
+            for n, v in zip(self.NAMES, parts[5:9]):
                 if v.lower() == "active":
                     reasons.add(n)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvml 2 ms" if self.samples else "nvidia-smi 50 ms"}
 
 
 # ---------------------------------------------------------------------------
@@ -748,7 +801,7 @@ def main(argv=None):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(dev.index) as clk:
+    with ClockSampler(dev) as clk:
         t_start = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
         t_start.record(stream)

@@ -307,6 +307,10 @@ int cmlb_debug_pairwise_schedule(int64_t n, uint32_t* codes);
  * order (the SKEW variant's precondition), 0 when not, <0 on a bad
  * descriptor.  Host only. */
 int cmlb_debug_sums_order_free(const cmlb_forest_desc* desc);
+/* Rows the most recent certified linear run (class tails) sent to the float64
+ * recompute, when the process runs with CMLB_LINEAR_QSTAT set (that run then
+ * synchronizes its stream); -1 otherwise. */
+int64_t cmlb_debug_linear_queued(void);
 /* SVM fast path only, on every row, with the epilogue's per-row error bound
  * written to err (device float32 [n_rows]); CMLB_SVM_PROBE switches pipeline
  * roles off (tools/svm_pipe_probe.py). */

@@ -109,6 +109,7 @@ SIGNATURES = {
     "cmlb_columns_destroy": (None, [c_vp]),
     "cmlb_debug_pairwise_schedule": (C.c_int, [c_i64, P(C.c_uint32)]),
     "cmlb_debug_sums_order_free": (C.c_int, [P(ForestDesc)]),
+    "cmlb_debug_linear_queued": (C.c_int64, []),
 }
 
 

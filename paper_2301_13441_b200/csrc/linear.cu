@@ -25,6 +25,9 @@
 #include "common.cuh"
 #include "sm100.cuh"
 
+#include <atomic>
+static std::atomic<int64_t> g_linear_queued{-1};  // cmlb_debug_linear_queued
+
 namespace cmlb {
 
 struct LinearArgs {
@@ -491,9 +494,14 @@ __global__ void __launch_bounds__(LNT) linear_exact_rows_kernel(const LinearArgs
 // (sequential FMA chains) and sum of squares: store the label, or queue the
 // row for the float64 recompute when the n u |x| |w| bound cannot settle it.
 template <int CM>
-__device__ __forceinline__ void cert_finish(const LinearArgs& a, int64_t row, const float (&acc)[CM], float nxr) {
+__device__ __forceinline__ void cert_finish(const LinearArgs& a, int64_t row, const float (&acc)[CM], float nxr,
+                                            const float* eblk = nullptr, int kc = 0) {
   const int C = a.C;
   const float nu = (float)(a.F + 2) * 5.9604644775390625e-08f;
+  // block a-posteriori bound (eblk, see linear_tile_kernel): u' KC / (1 - KC u')
+  // x (sum_b |s_b| + |x| |w_c|), inflated by 1/16 for the float32 evaluation of
+  // the bound itself, plus n 2^-149 for underflow in the chain
+  const float ku = (float)(kc + 1) * 5.9604644775390625e-08f * 1.0625f;
   const float xn = sqrtf(nxr) * 1.0625f;
   float z[CM], e[CM];
   bool ok = true;
@@ -501,7 +509,8 @@ __device__ __forceinline__ void cert_finish(const LinearArgs& a, int64_t row, co
   for (int c = 0; c < CM; ++c) {
     if (c < C) {
       z[c] = __fadd_rn(acc[c], __ldg(a.b + c));
-      e[c] = nu * xn * __ldg(a.wnorm + c) + 2.4e-7f * (fabsf(acc[c]) + fabsf(z[c]));
+      const float chain = eblk ? ku * (eblk[c] + xn * __ldg(a.wnorm + c)) + 1e-37f : nu * xn * __ldg(a.wnorm + c);
+      e[c] = chain + 2.4e-7f * (fabsf(acc[c]) + fabsf(z[c]));
       ok = ok && (z[c] - z[c] == 0.0f) && (e[c] < 3.0e38f);
     } else {
       z[c] = 0.0f;
@@ -670,6 +679,17 @@ __device__ __forceinline__ void ffma2(float& a0, float& a1, float x, float w0, f
   asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(rp));
 }
 
+// (n0, n1) += (v.x^2, v.y^2) then += (v.z^2, v.w^2): one FFMA2 per feature pair
+__device__ __forceinline__ void ffma2_pair(float& n0, float& n1, const float4& v) {
+  unsigned long long lo, hi, ap, rp;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(lo) : "f"(v.x), "f"(v.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(hi) : "f"(v.z), "f"(v.w));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(ap) : "f"(n0), "f"(n1));
+  asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(rp) : "l"(lo), "l"(ap));
+  asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(ap) : "l"(hi), "l"(rp));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(n0), "=f"(n1) : "l"(ap));
+}
+
 template <int KC>
 __device__ __forceinline__ int lt_swz(int r, int p) {
   if constexpr (KC == 32) return p ^ (r & 7);        // 128-byte rows
@@ -720,12 +740,19 @@ __global__ void __launch_bounds__(NT, 1) linear_tile_kernel(const LinearArgs a) 
       const uint32_t boff = (uint32_t)(iss_g % ST) * (TR * KC * 4);
       const int k0 = iss_kc * KC;
       const bool full = k0 + KC <= F;
+      if (full && iss_row0 + TR <= a.n_rows) {  // whole slice of a whole tile: no zero fill
 #pragma unroll
-      for (int j = 0; j < NP; ++j) {
-        const int p = (tid + j * NT) % PC;
-        const bool ok = irow[j] && (full || k0 + 4 * p < F);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(idst[j] + boff),
-                     "l"(ok ? isrc[j] + k0 : a.x), "r"(ok ? 16 : 0) : "memory");
+        for (int j = 0; j < NP; ++j)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(idst[j] + boff), "l"(isrc[j] + k0)
+                       : "memory");
+      } else {
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+          const int p = (tid + j * NT) % PC;
+          const bool ok = irow[j] && (full || k0 + 4 * p < F);
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(idst[j] + boff),
+                       "l"(ok ? isrc[j] + k0 : a.x), "r"(ok ? 16 : 0) : "memory");
+        }
       }
       if (++iss_kc == nk) {
         iss_kc = 0;
@@ -739,12 +766,16 @@ __global__ void __launch_bounds__(NT, 1) linear_tile_kernel(const LinearArgs a) 
 #pragma unroll
   for (int s = 0; s < ST - 1; ++s) issue();
   stage_w_kmajor<float, NT>(wkm, CE, a.w, C, F);
-  float acc[RPT][CM], nx[RPT];
+  // eb: sum over slices of |partial logit| at each slice end, for the block
+  // a-posteriori bound of cert_finish (a chain's rounding error is at most
+  // u' sum_k |s_k|, and within a slice |s_k| <= |s at the slice start| + that
+  // slice's sum |x_j w_j|); ~20x tighter than n u |x| |w| on random rows
+  float acc[RPT][CM], nx[RPT], nx2[RPT], eb[RPT][CM];
 #pragma unroll
   for (int q = 0; q < RPT; ++q) {
-    nx[q] = 0.0f;
+    nx[q] = nx2[q] = 0.0f;
 #pragma unroll
-    for (int c = 0; c < CM; ++c) acc[q][c] = 0.0f;
+    for (int c = 0; c < CM; ++c) acc[q][c] = eb[q][c] = 0.0f;
   }
   int64_t row0 = (int64_t)blockIdx.x * TR;
   int kc = 0;
@@ -764,14 +795,15 @@ __global__ void __launch_bounds__(NT, 1) linear_tile_kernel(const LinearArgs a) 
         const int r = tid + q * NT;
         v[q] = *reinterpret_cast<const float4*>(xb + r * KC + (lt_swz<KC>(r, p) << 2));
       }
+      // |x|^2 as two interleaved chains (features 4p, 4p+2 and 4p+1, 4p+3): two
+      // FFMA2 per float4 instead of four FFMA
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) ffma2_pair(nx[q], nx2[q], v[q]);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         float xv[RPT];
 #pragma unroll
-        for (int q = 0; q < RPT; ++q) {
-          xv[q] = e == 0 ? v[q].x : e == 1 ? v[q].y : e == 2 ? v[q].z : v[q].w;
-          nx[q] = fmaf(xv[q], xv[q], nx[q]);
-        }
+        for (int q = 0; q < RPT; ++q) xv[q] = e == 0 ? v[q].x : e == 1 ? v[q].y : e == 2 ? v[q].z : v[q].w;
         const float4* w4 = reinterpret_cast<const float4*>(wkm + (k0 + 4 * p + e) * CE);
 #pragma unroll
         for (int c4 = 0; c4 < CE / 4; ++c4) {
@@ -788,14 +820,18 @@ __global__ void __launch_bounds__(NT, 1) linear_tile_kernel(const LinearArgs a) 
         }
       }
     }
+#pragma unroll
+    for (int q = 0; q < RPT; ++q)
+#pragma unroll
+      for (int c = 0; c < CM; ++c) eb[q][c] += fabsf(acc[q][c]);
     if (++kc == nk) {
 #pragma unroll
       for (int q = 0; q < RPT; ++q) {
         const int64_t row = row0 + tid + q * NT;
-        if (row < a.n_rows) cert_finish<CM>(a, row, acc[q], nx[q]);
-        nx[q] = 0.0f;
+        if (row < a.n_rows) cert_finish<CM>(a, row, acc[q], nx[q] + nx2[q], eb[q], KC);
+        nx[q] = nx2[q] = 0.0f;
 #pragma unroll
-        for (int c = 0; c < CM; ++c) acc[q][c] = 0.0f;
+        for (int c = 0; c < CM; ++c) acc[q][c] = eb[q][c] = 0.0f;
       }
       kc = 0;
       row0 += (int64_t)gridDim.x * TR;
@@ -806,7 +842,8 @@ __global__ void __launch_bounds__(NT, 1) linear_tile_kernel(const LinearArgs a) 
 
 struct TileCfg { int nt, kc, st, rpt, per_sm; };
 static const TileCfg kTileCfg[] = {{128, 32, 4, 1, 2}, {128, 16, 4, 2, 2}, {128, 16, 4, 4, 1}, {64, 16, 4, 4, 2}, {128, 16, 3, 2, 2},
-                                   {256, 16, 4, 2, 1}, {128, 32, 4, 2, 1}, {128, 16, 6, 2, 1}};
+                                   {256, 16, 4, 2, 1}, {128, 32, 4, 2, 1}, {128, 16, 6, 2, 1}, {256, 16, 5, 2, 1},
+                                   {256, 16, 6, 1, 1}};
 constexpr int N_TILE_CFG = sizeof(kTileCfg) / sizeof(kTileCfg[0]);
 
 template <int CM>
@@ -819,6 +856,8 @@ static LinFn tile_fn(int cfg) {
     case 5: return linear_tile_kernel<CM, 256, 16, 4, 2>;
     case 6: return linear_tile_kernel<CM, 128, 32, 4, 2>;
     case 7: return linear_tile_kernel<CM, 128, 16, 6, 2>;
+    case 8: return linear_tile_kernel<CM, 256, 16, 5, 2>;
+    case 9: return linear_tile_kernel<CM, 256, 16, 6, 1>;
     default: return linear_tile_kernel<CM, 128, 16, 3, 2>;
   }
 }
@@ -893,6 +932,82 @@ __global__ void __launch_bounds__(LX_NT) linear_exact_lanes_kernel(const LinearA
     }
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();               // ring free before the next batch's prologue
+    const float zl = act ? __fadd_rn(__double2float_rn(acc), __ldg(a.b + c)) : 0.0f;
+    float z[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) z[q] = __shfl_sync(0xffffffffu, zl, (tid & 16) + q);
+    if (c == 0 && live) {
+      if (a.tail == CMLB_LIN_ARGMAX) {
+        store_out(a.y, row, a.out_dt, a.classes[first_max<16>(z, C)]);
+      } else if (a.tail == CMLB_LIN_SIGMOID) {
+        const float pz = __double2float_rn(ref_sigmoid((double)z[0]));
+        store_out(a.y, row, a.out_dt, a.classes[pz > 0.5f ? 1 : 0]);
+      } else {
+        store_out(a.y, row, a.out_dt, a.classes[z[0] > 0.0f ? 1 : 0]);
+      }
+    }
+  }
+}
+
+// Whole-row form of linear_exact_lanes_kernel for the few rows the block
+// bound leaves (~0.03% of LR 784x10): the CTA's 16 queued rows are loaded and
+// converted to float64 once (row stride F + 1 doubles: the two rows a warp
+// reads sit in different banks), then each thread runs its output's
+// ascending-k FMA chain with no barrier inside the chain (the ring form pays
+// two barriers per 32 features).  W float64 [F][16] + rows [16][F + 1] must
+// fit shared memory (F <= 880); larger F takes the ring form.
+__global__ void __launch_bounds__(LX_NT) linear_exact_whole_kernel(const LinearArgs a) {
+  extern __shared__ __align__(16) double wq[];   // [F][16] then the rows [LX_R][F + 1]
+  const int nq = *a.queue_len;
+  const int64_t first = (int64_t)blockIdx.x * LX_R;
+  if (first >= nq) return;
+  const int F = a.F, C = a.C, tid = threadIdx.x, FP = F + 1;
+  stage_w_kmajor<double, LX_NT>(wq, 16, a.w, C, F);
+  double* xd = wq + F * 16;
+  const int r = tid >> 4, c = tid & 15;
+  const bool act = c < C;
+  const int f4 = F / 4;  // F % 4 == 0, rows 16-byte aligned (host)
+  for (int64_t qb = first; qb < nq; qb += (int64_t)gridDim.x * LX_R) {
+    const int64_t qi = qb + r;
+    const bool live = qi < nq;
+    const int64_t row = a.queue[live ? qi : qb];
+    // rows -> float64 shared memory, float4 loads, four in flight per thread
+    for (int i0 = tid; i0 < LX_R * f4; i0 += 4 * LX_NT) {
+      float4 v[4];
+      int64_t rr[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * LX_NT;
+        if (i < LX_R * f4) {
+          const int lr = i / f4;
+          rr[u] = a.queue[qb + lr < nq ? qb + lr : qb];
+          v[u] = __ldg(reinterpret_cast<const float4*>(a.x + rr[u] * a.ldx) + (i - lr * f4));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * LX_NT;
+        if (i < LX_R * f4) {
+          const int lr = i / f4, k = 4 * (i - lr * f4);
+          double* d = xd + lr * FP + k;
+          d[0] = (double)v[u].x; d[1] = (double)v[u].y; d[2] = (double)v[u].z; d[3] = (double)v[u].w;
+        }
+      }
+    }
+    __syncthreads();
+    const double* xs = xd + r * FP;
+    const double* wk = wq + c;
+    double acc = 0.0;
+    if (a.sparse) {  // CSR weights: only nonzero terms enter the sum (kernels.py:103-126)
+      for (int k = 0; k < F; ++k) {
+        const double w = wk[k * 16];
+        if (act && w != 0.0) acc = fma(xs[k], w, acc);
+      }
+    } else {
+#pragma unroll 8
+      for (int k = 0; k < F; ++k) acc = fma(xs[k], wk[k * 16], acc);  // padded lanes: w = 0
+    }
+    __syncthreads();  // rows consumed before the next batch overwrites them
     const float zl = act ? __fadd_rn(__double2float_rn(acc), __ldg(a.b + c)) : 0.0f;
     float z[16];
 #pragma unroll
@@ -1059,7 +1174,13 @@ int cmlb_linear_run(const cmlb_linear* m, const float* x, int64_t n_rows, int64_
   if (fixup) {
     static const bool old_fix = std::getenv("CMLB_LINEAR_FIXUP_WARP") != nullptr;
     const size_t xb = (size_t)m->F * 16 * 8 + (size_t)LX_R * 32 * 8 + (size_t)LX_ST * LX_R * 32 * 4;
-    if (!old_fix && m->C <= 16 && !m->pro && aligned && xb <= 200 * 1024) {
+    const size_t xw = (size_t)m->F * 16 * 8 + (size_t)LX_R * (m->F + 1) * 8;
+    if (!old_fix && m->C <= 16 && !m->pro && aligned && xw <= 220 * 1024 && !std::getenv("CMLB_LINEAR_RING")) {
+      CMLB_CUDA(cudaFuncSetAttribute(linear_exact_whole_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xw));
+      // persistent: one CTA per SM (at ~0.03% queued rows, a handful are busy)
+      const int g = (int)std::min<int64_t>(ceil_div(n_rows, (int64_t)LX_R), (int64_t)num_sms(m->device));
+      linear_exact_whole_kernel<<<g, LX_NT, xw, s>>>(a);
+    } else if (!old_fix && m->C <= 16 && !m->pro && aligned && xb <= 200 * 1024) {
       CMLB_CUDA(cudaFuncSetAttribute(linear_exact_lanes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xb));
       int per_sm = 0;
       CMLB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, linear_exact_lanes_kernel, LX_NT, xb));
@@ -1071,10 +1192,19 @@ int cmlb_linear_run(const cmlb_linear* m, const float* x, int64_t n_rows, int64_
     }
     note_launch();
     CMLB_CUDA(cudaGetLastError());
+    static const bool qstat = std::getenv("CMLB_LINEAR_QSTAT") != nullptr;  // measurement knob
+    if (qstat) {
+      int32_t q = 0;
+      CMLB_CUDA(cudaMemcpyAsync(&q, a.queue_len, sizeof(q), cudaMemcpyDeviceToHost, s));
+      CMLB_CUDA(cudaStreamSynchronize(s));
+      g_linear_queued.store(q);
+    }
     CMLB_CUDA(cudaFreeAsync(scratch, s));
   }
   return CMLB_OK;
 }
+
+int64_t cmlb_debug_linear_queued(void) { return g_linear_queued.load(); }
 
 void cmlb_linear_destroy(cmlb_linear* m) { delete m; }
 

@@ -29,6 +29,9 @@ for i in range(n):
     torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1))
 print("impl", os.environ.get("CMLB_LINEAR_IMPL", "1"), "median ms", sorted(ts[3:])[len(ts[3:]) // 2], "min", min(ts[3:]))
+if os.environ.get("CMLB_LINEAR_QSTAT"):
+    from paper_2301_13441_b200 import _native as N  # noqa: E402
+    print("queued rows (float64 recompute)", N.lib().cmlb_debug_linear_queued(), "of", x.shape[0])
 if os.environ.get("PROBE_GAPS"):
     xh = x.cpu().numpy().astype(np.float64)
     W = np.array(lm.coef, dtype=np.float64)
