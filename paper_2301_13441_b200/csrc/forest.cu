@@ -604,15 +604,32 @@ __device__ __forceinline__ uint32_t imad_u32(uint32_t a, uint32_t b, uint32_t c)
 // One level of the skewed walk: o' = 2 o + cst (+128 when rank > threshold).
 // The two adds are IMADs by opaque constants (FMA pipe); the mask, compare and
 // the rank address (caller) stay on the ALU pipe.
+// The compare rank > threshold reads the low 16-bit halves of the rank and of
+// the node word as float16: both are < 2^14, and nonnegative float16 bit
+// patterns below 0x7c00 (subnormals included; no .ftz) order exactly like the
+// integers, so one HSETP2 on the .H0 halves replaces mask + integer compare.
+#ifndef CMLB_SKEW_INT_CMP
+#define CMLB_CMP_RANK(P, RK, W) " mov.b32 {rl, rh}, " RK ";\n mov.b32 {wl, wh}, " W ";\n setp.gt.f16 " P ", rl, wl;\n"
+#define CMLB_CMP_REGS " .reg .b16 rl, rh, wl, wh;\n"
+#else
+#define CMLB_CMP_RANK(P, RK, W) " and.b32 t, " W ", 65535;\n setp.gt.u32 " P ", " RK ", t;\n"
+#define CMLB_CMP_REGS " .reg .b32 t;\n"
+#endif
 __device__ __forceinline__ uint32_t skew_next(uint32_t o, uint32_t cst, uint32_t rk, uint32_t w, const SkewConsts& k) {
   uint32_t nx;
-  asm("{\n .reg .pred p;\n .reg .b32 t;\n"
-      " and.b32 t, %4, 65535;\n"
-      " setp.gt.u32 p, %3, t;\n"
+  asm("{\n .reg .pred p;\n" CMLB_CMP_REGS
+      CMLB_CMP_RANK("p", "%3", "%4")
       " mad.lo.u32 %0, %1, %5, %2;\n"
       " @p mad.lo.u32 %0, %6, %7, %0;\n}"
       : "=&r"(nx) : "r"(o), "r"(cst), "r"(rk), "r"(w), "r"(k.two), "r"(k.one), "r"(k.c128));
   return nx;
+}
+// rank > (w & 0xffff) for the RANKED walk (same float16 compare)
+__device__ __forceinline__ bool rank_gt(uint32_t rk, uint32_t w) {
+  uint32_t r;
+  asm("{\n .reg .pred p;\n" CMLB_CMP_REGS CMLB_CMP_RANK("p", "%1", "%2") " selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(r) : "r"(rk), "r"(w));
+  return r != 0;
 }
 
 __device__ __forceinline__ double f32_to_f64_nonneg(float v, const SkewConsts& k) {
@@ -848,7 +865,7 @@ __global__ void __launch_bounds__(NTT, 1) forest_ranked_kernel(const ForestArgs 
           const uint32_t w = *reinterpret_cast<const uint32_t*>(smem + o[q][k]);
           const uint32_t rk = *reinterpret_cast<const uint16_t*>(xrb + ((w >> 14) + pb[k]));
           uint32_t nx = 2u * o[q][k] + cst[q];
-          if (rk > (w & 0xFFFFu)) nx += 4u;
+          if (rank_gt(rk, w)) nx += 4u;
           o[q][k] = nx;
         }
       }
@@ -1564,7 +1581,7 @@ struct cmlb_forest {
   int32_t* ulev = nullptr;
   int ntt = 256, stage_cap = 0, node_off_bytes = 0, rcfg = 0, stage_off = 0, stage_bufs = 2;
   size_t rank_smem = 0;  // SKEW / RANKED: forest_rank_kernel's staging buffers
-  int rank_nb = 3;       // forest_rank_kernel staging depth (2 or 3)
+  int rank_nb = 2;       // forest_rank_kernel staging depth (2 or 3)
   bool rank_pass = true; // RANKED: rank in a separate pass (CMLB_RANK_PASS=0: fused per tile)
   int mma_k = 0, mma_n = 0, mma_feat_off = 0, mma_thr_off = 0, mma_pay_off = 0;
   cmlb_column_op* pro = nullptr;  // fused preprocessing
@@ -2243,11 +2260,11 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
   if (f->variant == CMLB_FOREST_SKEW && (RANK_THREADS * RANK_RPT) % (f->ntt * f->rpt) != 0)
     return fail(CMLB_E_UNRESOLVED, "skew walk tile does not divide the rank pass tile");
   if (f->variant == CMLB_FOREST_SKEW || (f->variant == CMLB_FOREST_RANKED && f->rank_pass)) {
-    // three staging buffers when two CTAs per SM still fit (RF500: 3 x 32 KB),
-    // else two; CMLB_RANK_NB forces one (measurement knob)
+    // two staging buffers (RF500: 2 x 32 KB; three measured 0.6% slower,
+    // profiles/r2_tuning/rank_nb*.json); CMLB_RANK_NB=3 forces three
     const size_t table = (size_t)f->stage_cap * 4;
-    f->rank_nb = 3 * table <= SMEM_LIMIT / 2 - 1024 ? 3 : 2;
-    if (const char* nb = getenv("CMLB_RANK_NB")) f->rank_nb = atoi(nb) == 2 ? 2 : 3;
+    f->rank_nb = 2;
+    if (const char* nb = getenv("CMLB_RANK_NB")) f->rank_nb = atoi(nb) == 3 ? 3 : 2;
     if ((size_t)f->rank_nb * table > SMEM_LIMIT) f->rank_nb = 2;
     f->rank_smem = (size_t)f->rank_nb * table;
     CMLB_CUDA(cudaFuncSetAttribute(f->rank_nb == 3 ? forest_rank_kernel<3> : forest_rank_kernel<2>,
