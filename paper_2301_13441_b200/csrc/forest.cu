@@ -1011,48 +1011,48 @@ __global__ void __launch_bounds__(RANK_THREADS, 2) forest_rank_kernel(const Fore
     for (int f = 0; f < NB - 1 && f < F; ++f) issue(f, f);
 
   const int64_t row0 = (int64_t)blockIdx.x * ROWS;
-  int64_t rowk[RPT];
+  // row k of this thread: rowb + 32 k (k = 2p + h), in the batch for k < nk
+  const int64_t rowb = row0 + warp * 256 + lane;
+  const int64_t nk64 = (a.n_rows - rowb + 31) / 32;
+  const int nk = nk64 <= 0 ? 0 : nk64 >= RPT ? RPT : (int)nk64;
   uint32_t soff[NP];  // byte offset of the (R, R + 32) word in the CTA's walk tiles, feature 0
   uint32_t sok = 0;   // bit p: the word's walk tile exists
 #pragma unroll
   for (int p = 0; p < NP; ++p) {
     const int R = warp * 256 + 64 * p + lane;
-    rowk[2 * p] = row0 + R;
-    rowk[2 * p + 1] = row0 + R + 32;
     const int t = R / WR, r = R % WR;
     soff[p] = (uint32_t)t * (uint32_t)(F * WR * 2) + 4u * (uint32_t)((r >> 6) * 32 + (r & 31));
     sok |= (row0 + (int64_t)t * WR < a.n_rows ? 1u : 0u) << p;
   }
   uint8_t* const rbase = reinterpret_cast<uint8_t*>(a.ranks) + (row0 / WR) * (int64_t)F * WR * 2;
-  // dense-selector NaN poisoning (the reference's 0 * inf): rows with non-finite features
-  int nbad[RPT];
-  bool anybad = false;
-#pragma unroll
-  for (int k = 0; k < RPT; ++k) {
-    nbad[k] = 0;
-    if (a.dense_sel && rowk[k] < a.n_rows) {
-      const float* src = a.x + rowk[k] * a.ldx;
-      for (int f = 0; f < F; ++f) nbad[k] += !isfinite(load_col(a.pro, src, f));
+  const float* const xb = a.x + (nk > 0 ? rowb : 0) * a.ldx;
+  const int64_t xstride = 32 * a.ldx;
+  // dense-selector NaN poisoning (the reference's 0 * inf): bit k of bad1 /
+  // bad2 marks row k with exactly one / at least two non-finite features
+  uint32_t bad1 = 0, bad2 = 0;
+  if (a.dense_sel) {
+    for (int k = 0; k < nk; ++k) {
+      int nb = 0;
+      for (int f = 0; f < F; ++f) nb += !isfinite(load_col(a.pro, xb + k * xstride, f));
+      bad1 |= (nb == 1 ? 1u : 0u) << k;
+      bad2 |= (nb >= 2 ? 1u : 0u) << k;
     }
-    anybad |= nbad[k] != 0;
   }
+  const bool anybad = (bad1 | bad2) != 0;
   // row values: vec path (plain row-major x, 8-byte aligned rows, even F)
   // loads features 2g, 2g+1 of a row as one float2, pair g+1 in flight while
   // pair g is searched; otherwise one feature at a time through load_col
   const bool vec = a.vec_x;
-  const float* xp[RPT];
-#pragma unroll
-  for (int k = 0; k < RPT; ++k) xp[k] = rowk[k] < a.n_rows ? a.x + rowk[k] * a.ldx : nullptr;
   float xn[RPT];
   float2 cur[RPT], nxt[RPT];
   auto load_f = [&](int f) {
 #pragma unroll
-    for (int k = 0; k < RPT; ++k) xn[k] = (xp[k] && f < F) ? load_col(a.pro, xp[k], f) : 0.0f;
+    for (int k = 0; k < RPT; ++k) xn[k] = (k < nk && f < F) ? load_col(a.pro, xb + k * xstride, f) : 0.0f;
   };
   auto load2 = [&](int g, float2 (&dst)[RPT]) {
 #pragma unroll
     for (int k = 0; k < RPT; ++k)
-      dst[k] = (xp[k] && g < F) ? __ldg(reinterpret_cast<const float2*>(xp[k] + g)) : make_float2(0.f, 0.f);
+      dst[k] = (k < nk && g < F) ? __ldg(reinterpret_cast<const float2*>(xb + k * xstride + g)) : make_float2(0.f, 0.f);
   };
   if (vec) {
     load2(0, cur);
@@ -1072,7 +1072,7 @@ __global__ void __launch_bounds__(RANK_THREADS, 2) forest_rank_kernel(const Fore
     if (anybad) {
 #pragma unroll
       for (int k = 0; k < RPT; ++k)
-        if (nbad[k] && (nbad[k] >= 2 || isfinite(xq[k]))) xq[k] = __int_as_float(0x7fc00000);
+        if (((bad2 >> k) & 1u) || (((bad1 >> k) & 1u) && isfinite(xq[k]))) xq[k] = __int_as_float(0x7fc00000);
     }
     if (vec) {
       if (hi) {
