@@ -159,6 +159,22 @@ __device__ __forceinline__ void flush(const Args& a, int cur, const double (&acc
   }
 }
 
+// Vote-robust class: with `unc` marking the pairs whose sign is not certain,
+// class w is libsvm's answer for EVERY resolution of those pairs when its
+// certain votes beat every other class's certain-plus-uncertain votes
+// (strictly for lower-indexed classes, which win ties).  Returns w, or -1.
+__device__ __forceinline__ int robust_vote(const int* vmin, const int* unc, int C) {
+  int w = 0;
+  for (int c = 1; c < C; ++c)
+    if (vmin[c] > vmin[w]) w = c;
+  for (int c = 0; c < C; ++c) {
+    if (c == w) continue;
+    const int hi = vmin[c] + unc[c];
+    if (c < w ? !(vmin[w] > hi) : !(vmin[w] >= hi)) return -1;
+  }
+  return w;
+}
+
 template <int CP>
 __global__ void __launch_bounds__(THREADS, 1) svm_tc_kernel(const Args a) {
   constexpr int CPS = (CP + 3) & ~3;  // w row stride (16-byte aligned rows)
@@ -455,23 +471,47 @@ __global__ void __launch_bounds__(THREADS, 1) svm_tc_kernel(const Args a) {
           if (a.dec_out) a.dec_out[row] = v;
         }
       } else {
-        int vote[MAXC];
-        for (int c = 0; c < a.C; ++c) vote[c] = 0;
+        // certain votes (vote) and uncertain pairs per class (unc): a pair is
+        // uncertain when |dec| is inside its tolerance
+        int vote[MAXC], unc[MAXC];
+        for (int c = 0; c < a.C; ++c) vote[c] = unc[c] = 0;
+        bool any_unc = false, nonfin = false;
         int p = 0;
         for (int i = 0; i < a.C; ++i) {
           for (int j = i + 1; j < a.C; ++j, ++p) {
             const double v = dec[p] + (double)a.intercept[p];
             dec[p] = v;
             const float tol_p = a.prob_tol ? tol : 4.0f * (errc[i] + errc[j]) + 1e-30f;
-            exact = exact || !(fabs(v) > (double)tol_p);
-            if (v > 0) ++vote[i]; else ++vote[j];
+            nonfin = nonfin || !isfinite(v);
+            if (!(fabs(v) > (double)tol_p)) {
+              any_unc = true;
+              ++unc[i];
+              ++unc[j];
+            } else if (v > 0) {
+              ++vote[i];
+            } else {
+              ++vote[j];
+            }
           }
         }
-        if (a.no_exact) exact = false;
-        if (!exact) {
-          int best = 0;
+        // uncertain pairs need the exact path only when they could change the
+        // class (or when the decision values themselves are wanted)
+        int best = -1;
+        if (!exact && !nonfin && (!any_unc || !a.dec_out)) best = robust_vote(vote, unc, a.C);
+        exact = best < 0;
+        if (a.no_exact && exact) {  // debug probe: vote with the fast-path signs as they are
+          for (int c = 0; c < a.C; ++c) vote[c] = 0;
+          p = 0;
+          for (int i = 0; i < a.C; ++i)
+            for (int j = i + 1; j < a.C; ++j, ++p) {
+              if (dec[p] > 0) ++vote[i]; else ++vote[j];
+            }
+          best = 0;
           for (int c = 1; c < a.C; ++c)
             if (vote[c] > vote[best]) best = c;
+          exact = false;
+        }
+        if (!exact) {
           store_out(a.y, row, a.out_dt, a.classes[best]);
           if (a.dec_out)
             for (int q = 0; q < a.pairs; ++q) a.dec_out[row * a.pairs + q] = dec[q];
@@ -612,7 +652,8 @@ __global__ void __launch_bounds__(CB_THREADS, 2) svm_certify_kernel(const Args a
   double* eks = ks + CB_ROWS * CB_SS;                              // [CB_ROWS][CB_SS] |K_ours - K_libsvm| bounds
   double* nxs = eks + CB_ROWS * CB_SS;                             // [CB_ROWS] |x|^2
   __shared__ int32_t rows[CB_ROWS];
-  __shared__ int undecided[CB_ROWS];
+  __shared__ int undecided[CB_ROWS];                 // non-finite feature: the exact kernel decides
+  __shared__ unsigned long long uncm[CB_ROWS];       // bit p: pair p inside its bound
   const int tid = threadIdx.x;
   const int nq = *a.queue_len;
   const int F = a.F, C = a.C;
@@ -647,6 +688,7 @@ __global__ void __launch_bounds__(CB_THREADS, 2) svm_certify_kernel(const Args a
       }
       nxs[tid] = sacc;
       undecided[tid] = nf;
+      uncm[tid] = 0ull;
     }
     double dsum[CB_TPT], esum[CB_TPT];
     float asum[CB_TPT];  // sum |w K|, rounded up (an upper bound is all the certificate needs)
@@ -811,15 +853,41 @@ __global__ void __launch_bounds__(CB_THREADS, 2) svm_certify_kernel(const Args a
       const double rho = (double)a.intercept[p];
       const double dec = __dsub_rn(dsum[q], -rho);
       const double tol2 = esum[q] + 2.0 * gamma_n(a.n_sv + 2) * (asum[q] + fabs(rho)) + 1e-300;
-      if (!a.is_svr && !(fabs(dec) > tol2)) atomicOr(&undecided[r], 1);
+      if (a.is_svr) {
+        if (!(fabs(dec) > tol2)) atomicOr(&undecided[r], 1);
+      } else if (!(fabs(dec) > tol2)) {
+        atomicOr(&uncm[r], 1ull << p);
+      }
       decs[r * npairs + p] = dec;
     }
     __syncthreads();
     if (tid < nb) {
       const int64_t row = rows[tid];
       const double* d = decs + tid * npairs;
-      if (undecided[tid]) {
+      int best = -1;
+      bool exact = undecided[tid] != 0;
+      if (!exact && !a.is_svr && uncm[tid]) {
+        // uncertain pairs matter only if they could change the class
+        exact = a.dec_out != nullptr;
+        if (!exact) {
+          int vmin[MAXC], unc[MAXC];
+          for (int c = 0; c < C; ++c) vmin[c] = unc[c] = 0;
+          int p = 0;
+          for (int i = 0; i < C; ++i)
+            for (int j = i + 1; j < C; ++j, ++p) {
+              if (!isfinite(d[p])) exact = true;
+              if ((uncm[tid] >> p) & 1ull) { ++unc[i]; ++unc[j]; }
+              else if (d[p] > 0) ++vmin[i];
+              else ++vmin[j];
+            }
+          if (!exact) best = robust_vote(vmin, unc, C);
+          exact = best < 0;
+        }
+      }
+      if (exact) {
         a.queue2[atomicAdd(a.queue2_len, 1)] = (int32_t)row;
+      } else if (best >= 0) {
+        store_out(a.y, row, a.out_dt, a.classes[best]);
       } else if (a.is_svr) {
         store_out(a.y, row, a.out_dt, (double)(float)d[0]);
         if (a.dec_out) a.dec_out[row] = d[0];
