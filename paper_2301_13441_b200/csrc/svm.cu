@@ -1,3 +1,4 @@
+#include <cstdio>
 // Kernel SVM operator (SVC / NuSVC / SVR / NuSVR) on sm_100a.
 //
 // Semantics (not in the reference): libsvm's dense
@@ -95,6 +96,29 @@ struct Args {
   const double* ns64;      // [n_sv] |sv|^2 in float64 (certifying tier)
   int32_t* queue2;         // rows the float64 certifying tier could not decide -> libsvm-order exact path
   int32_t* queue2_len;
+  // pair tier: rows whose only uncertain pair is p (and whose decision values
+  // are not wanted) -- the certifying tier then needs the SVs of p's two
+  // classes only.  Unsorted entries from the fast path, then bucketed by pair.
+  int32_t* pq_row;         // [n_rows]
+  int32_t* pq_pair;        // [n_rows]
+  unsigned long long* pq_sign;  // [n_rows] bit q: dec_q > 0 (the fast path's certain signs)
+  unsigned long long* pq_unc;   // [n_rows] bit q: pair q uncertain in the fast path
+  int32_t* pq_len;
+  int32_t* pcount;         // [pairs] entries per pair
+  int32_t* pcur;           // [pairs] scatter cursors
+  int32_t* ps_row;         // [n_rows] bucketed by pair
+  unsigned long long* ps_sign;
+  unsigned long long* ps_unc;
+  // full certifying tier, SV-split: row blocks below cap_blocks are cut into
+  // units of CB_SPAN SVs on separate CTAs (one CTA walking all SVs of a block
+  // is latency-bound: 12 ms for a 64-row block of config 4b); partial decision
+  // sums meet in cacc ([3][cap_blocks * 64][pairs]: sum w K, sum |w| errK,
+  // sum |w K|) and svm_certify_finish_kernel decides
+  double* cacc;
+  int32_t* cflag;          // [cap_blocks * 64] non-finite feature
+  int cap_blocks;
+  double* pacc;            // pair tier: [3][n_rows] partial sums per bucketed entry
+  int32_t* pflag;          // [n_rows] non-finite feature
 };
 
 __host__ __device__ inline int pair_index(int a, int b, int C) {  // a < b
@@ -157,6 +181,13 @@ __device__ __forceinline__ void flush(const Args& a, int cur, const double (&acc
       dec[p] += acc[o];
     }
   }
+}
+
+// SVR: every value within tol of v rounds to the same float32 (rounding is
+// monotone), so the reference's float32 output equals ours.
+__device__ __forceinline__ bool f32_round_certain(double v, double tol) {
+  const double lo = __dsub_rd(v, tol), hi = __dadd_ru(v, tol);
+  return isfinite(lo) && isfinite(hi) && __double2float_rn(lo) == __double2float_rn(hi);
 }
 
 // Vote-robust class: with `unc` marking the pairs whose sign is not certain,
@@ -464,7 +495,7 @@ __global__ void __launch_bounds__(THREADS, 1) svm_tc_kernel(const Args a) {
       bool exact = !(tol < 3.0e38f);
       if (a.is_svr) {
         const double v = dec[0] + (double)a.intercept[0];
-        exact = exact || !(fabs(v) * 4.76837158203125e-07 > (double)tol);  // need rel. error < 2^-21
+        exact = exact || !f32_round_certain(v, (double)tol);
         if (a.no_exact) exact = false;
         if (!exact) {
           store_out(a.y, row, a.out_dt, (double)(float)v);
@@ -476,6 +507,8 @@ __global__ void __launch_bounds__(THREADS, 1) svm_tc_kernel(const Args a) {
         int vote[MAXC], unc[MAXC];
         for (int c = 0; c < a.C; ++c) vote[c] = unc[c] = 0;
         bool any_unc = false, nonfin = false;
+        int n_unc = 0;
+        unsigned long long signs = 0ull, uncmask = 0ull;
         int p = 0;
         for (int i = 0; i < a.C; ++i) {
           for (int j = i + 1; j < a.C; ++j, ++p) {
@@ -483,10 +516,13 @@ __global__ void __launch_bounds__(THREADS, 1) svm_tc_kernel(const Args a) {
             dec[p] = v;
             const float tol_p = a.prob_tol ? tol : 4.0f * (errc[i] + errc[j]) + 1e-30f;
             nonfin = nonfin || !isfinite(v);
+            if (p < 64 && v > 0) signs |= 1ull << p;
             if (!(fabs(v) > (double)tol_p)) {
               any_unc = true;
               ++unc[i];
               ++unc[j];
+              ++n_unc;
+              if (p < 64) uncmask |= 1ull << p;
             } else if (v > 0) {
               ++vote[i];
             } else {
@@ -515,6 +551,25 @@ __global__ void __launch_bounds__(THREADS, 1) svm_tc_kernel(const Args a) {
           store_out(a.y, row, a.out_dt, a.classes[best]);
           if (a.dec_out)
             for (int q = 0; q < a.pairs; ++q) a.dec_out[row * a.pairs + q] = dec[q];
+        } else if (a.pq_row && n_unc >= 1 && !nonfin && !a.dec_out && !(tol >= 3.0e38f)) {
+          // the pair tier resolves the uncertain pair between the strongest
+          // contenders from its two classes' SVs; what stays uncertain after
+          // that goes on to the full certifying tier
+          int p_best = -1, s_best = -1;
+          p = 0;
+          for (int i = 0; i < a.C; ++i)
+            for (int j = i + 1; j < a.C; ++j, ++p)
+              if ((uncmask >> p) & 1ull) {
+                const int sc = min(vote[i] + unc[i], vote[j] + unc[j]);
+                if (sc > s_best) { s_best = sc; p_best = p; }
+              }
+          const int q = atomicAdd(a.pq_len, 1);
+          a.pq_row[q] = (int32_t)row;
+          a.pq_pair[q] = p_best;
+          a.pq_sign[q] = signs;
+          a.pq_unc[q] = uncmask;
+          atomicAdd(a.pcount + p_best, 1);
+          exact = false;
         }
       }
       if (exact) a.queue[atomicAdd(a.queue_len, 1)] = (int32_t)row;
@@ -638,12 +693,18 @@ constexpr int CB_KS = CB_K + 4, CB_SS = CB_SV + 1;              // padded stride
 constexpr int CB_TPT = 12;                                        // (row, pair) tasks per thread: pairs <= 48
 constexpr int CB_MAXP = CB_TPT * CB_THREADS / CB_ROWS;
 constexpr size_t CB_SMEM = (size_t)2 * (CB_ROWS + CB_SV) * CB_KS * 8 + (size_t)2 * CB_ROWS * CB_SS * 8 + CB_ROWS * 8;
+constexpr int CB_SPAN = 4 * CB_SV;                               // SVs per split unit
+constexpr int CB_CAP_BLOCKS = 256;                               // split row blocks (16,384 rows)
 
 __device__ __forceinline__ double gamma_n(int n) {
   const double nu = n * 1.1102230246251565e-16;  // n * 2^-53
   return nu / (1.0 - nu);
 }
 
+// PAIR: the pair tier -- blocks of 64 rows that share their one uncertain pair
+// p = (ca, cb); only the SVs of classes ca and cb enter the Gram, only pair p's
+// decision is formed, and the other pairs' signs come from the fast path.
+template <bool PAIR>
 __global__ void __launch_bounds__(CB_THREADS, 2) svm_certify_kernel(const Args a, const int* n_sv_start) {
   extern __shared__ __align__(16) uint8_t csm[];
   double* xc = reinterpret_cast<double*>(csm);                  // [2][CB_ROWS][CB_KS]
@@ -654,11 +715,40 @@ __global__ void __launch_bounds__(CB_THREADS, 2) svm_certify_kernel(const Args a
   __shared__ int32_t rows[CB_ROWS];
   __shared__ int undecided[CB_ROWS];                 // non-finite feature: the exact kernel decides
   __shared__ unsigned long long uncm[CB_ROWS];       // bit p: pair p inside its bound
+  __shared__ int pblk[65], poff[65], punits[65];     // PAIR: per-pair unit / entry prefix sums, units per block
   const int tid = threadIdx.x;
-  const int nq = *a.queue_len;
   const int F = a.F, C = a.C;
   const int npairs = a.is_svr ? 1 : a.pairs;
-  const int ntasks = CB_ROWS * npairs;
+  const int ntasks = PAIR ? CB_ROWS : CB_ROWS * npairs;
+  int nblocks, sblocks = 0, nsplit = 1;
+  if constexpr (PAIR) {
+    if (tid == 0) {
+      // units: (row block of a pair's bucket, group of CB_SPAN / CB_SV SV tiles
+      // of the pair's two classes)
+      int usum = 0, esum0 = 0, qa = 0, qr = 0;
+      for (int q = 0; q < a.pairs; ++q) {
+        const int qb = qa + 1 + qr;  // pair q = (qa, qb)
+        const int ta = (n_sv_start[qa + 1] - n_sv_start[qa] + CB_SV - 1) / CB_SV;
+        const int tb = (n_sv_start[qb + 1] - n_sv_start[qb] + CB_SV - 1) / CB_SV;
+        punits[q] = (ta + tb + CB_SPAN / CB_SV - 1) / (CB_SPAN / CB_SV);
+        pblk[q] = usum;
+        poff[q] = esum0;
+        const int c = a.pcount[q];
+        usum += (c + CB_ROWS - 1) / CB_ROWS * punits[q];
+        esum0 += c;
+        if (++qr == C - 1 - qa) { ++qa; qr = 0; }
+      }
+      pblk[a.pairs] = usum;
+      poff[a.pairs] = esum0;
+    }
+    __syncthreads();
+    nblocks = pblk[a.pairs];
+  } else {
+    const int nrb = (*a.queue_len + CB_ROWS - 1) / CB_ROWS;
+    sblocks = a.cacc ? min(nrb, a.cap_blocks) : 0;
+    nsplit = (a.n_sv + CB_SPAN - 1) / CB_SPAN;
+    nblocks = sblocks * nsplit + (nrb - sblocks);  // split units, then whole blocks
+  }
   // The Gram on the FP64 tensor pipe: mma.sync m8n8k4 f64 (DMMA, 256 FMAs per
   // instruction; measured at the DFMA rate, 64 FMAs/clk/SM, with 1/8 of the
   // issue slots and operand traffic).  Warp tile 32 rows x 16 SVs = 4 x 2 MMA
@@ -671,9 +761,50 @@ __global__ void __launch_bounds__(CB_THREADS, 2) svm_certify_kernel(const Args a
   // charge 2 roundings per term (covers round-toward-zero adds too)
   const double gF = gamma_n(2 * F + 6);
   constexpr double U = 1.1102230246251565e-16;
-  for (int b0 = blockIdx.x * CB_ROWS; b0 < nq; b0 += gridDim.x * CB_ROWS) {
-    const int nb = min(CB_ROWS, nq - b0);
-    if (tid < CB_ROWS) rows[tid] = tid < nb ? a.queue[b0 + tid] : -1;
+  for (int blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
+    int nb, bp = 0;  // rows in this block; PAIR: their shared pair
+    int rb = 0, jlo = 0, jhi = a.n_sv;  // general: row block and SV range of this unit
+    bool split = false;
+    int pfirst = 0, pgroup = 0;  // PAIR: first sorted entry of the block, SV tile group of the unit
+    if constexpr (PAIR) {
+      while (blk >= pblk[bp + 1]) ++bp;
+      const int ub = blk - pblk[bp];
+      pgroup = ub % punits[bp];
+      const int first = (ub / punits[bp]) * CB_ROWS;
+      pfirst = poff[bp] + first;
+      nb = min(CB_ROWS, a.pcount[bp] - first);
+      if (tid < CB_ROWS) rows[tid] = tid < nb ? a.ps_row[pfirst + tid] : -1;
+      split = true;
+    } else {
+      if (blk < sblocks * nsplit) {
+        rb = blk / nsplit;
+        jlo = (blk % nsplit) * CB_SPAN;
+        jhi = min(a.n_sv, jlo + CB_SPAN);
+        split = true;
+      } else {
+        rb = sblocks + (blk - sblocks * nsplit);
+      }
+      const int b0 = rb * CB_ROWS;
+      nb = min(CB_ROWS, *a.queue_len - b0);
+      if (tid < CB_ROWS) rows[tid] = tid < nb ? a.queue[b0 + tid] : -1;
+    }
+    // SV segments: every SV, or (PAIR) the SVs of the block pair's two classes
+    int pca = 0, pcb = 0;
+    if constexpr (PAIR) {
+      int rem = bp;
+      while (rem >= C - 1 - pca) { rem -= C - 1 - pca; ++pca; }
+      pcb = pca + 1 + rem;
+    }
+    int seg_lo[2] = {jlo, 0}, seg_hi[2] = {jhi, 0};
+    if constexpr (PAIR) {  // this unit's tiles of the concatenated class-ca, class-cb SV lists
+      const int sa = n_sv_start[pca], ea = n_sv_start[pca + 1], sb = n_sv_start[pcb], eb = n_sv_start[pcb + 1];
+      const int ta = (ea - sa + CB_SV - 1) / CB_SV, tb = (eb - sb + CB_SV - 1) / CB_SV;
+      const int t0 = pgroup * (CB_SPAN / CB_SV), t1 = min(t0 + CB_SPAN / CB_SV, ta + tb);
+      seg_lo[0] = sa + CB_SV * min(t0, ta);
+      seg_hi[0] = min(ea, sa + CB_SV * min(t1, ta));
+      seg_lo[1] = sb + CB_SV * (max(t0, ta) - ta);
+      seg_hi[1] = t1 > ta ? min(eb, sb + CB_SV * (t1 - ta)) : seg_lo[1];
+    }
     __syncthreads();
     if (tid < CB_ROWS) {  // |x|^2 in float64 and the non-finite check
       double sacc = 0.0;
@@ -696,8 +827,9 @@ __global__ void __launch_bounds__(CB_THREADS, 2) svm_certify_kernel(const Args a
     for (int q = 0; q < CB_TPT; ++q) dsum[q] = esum[q] = 0.0, asum[q] = 0.0f;
     __syncthreads();
     const int nkc = (F + CB_K - 1) / CB_K;
-    for (int j0 = 0; j0 < a.n_sv; j0 += CB_SV) {
-      const int nj = min(CB_SV, a.n_sv - j0);
+    for (int sg = 0; sg < 2; ++sg)
+    for (int j0 = seg_lo[sg]; j0 < seg_hi[sg]; j0 += CB_SV) {
+      const int nj = min(CB_SV, seg_hi[sg] - j0);
       double g[4][2][2];  // [row block][SV block][c0, c1]
 #pragma unroll
       for (int i = 0; i < 4; ++i)
@@ -821,7 +953,7 @@ __global__ void __launch_bounds__(CB_THREADS, 2) svm_certify_kernel(const Args a
       for (int q = 0; q < CB_TPT; ++q) {
         const int task = tid + q * CB_THREADS;
         if (task >= ntasks) break;
-        const int r = task % CB_ROWS, p = task / CB_ROWS;
+        const int r = task % CB_ROWS, p = PAIR ? bp : task / CB_ROWS;
         auto add = [&](const float* coefrow, int lo, int hi) {
           for (int j = max(lo, j0); j < min(hi, j0 + nj); ++j) {
             const double w = (double)__ldg(coefrow + j);
@@ -843,6 +975,34 @@ __global__ void __launch_bounds__(CB_THREADS, 2) svm_certify_kernel(const Args a
       }
       __syncthreads();  // ks / eks reused by the next tile
     }
+    if constexpr (PAIR) {  // partial sums of this unit's SVs -> the sorted entry's accumulators
+      if (tid < nb) {
+        const size_t i = (size_t)pfirst + tid, np = (size_t)a.n_rows;
+        atomicAdd(a.pacc + i, dsum[0]);
+        atomicAdd(a.pacc + np + i, esum[0]);
+        atomicAdd(a.pacc + 2 * np + i, (double)asum[0]);
+        if (undecided[tid]) a.pflag[i] = 1;
+      }
+      __syncthreads();
+      continue;
+    }
+    if (split) {  // partial sums of this unit's SVs -> the block's accumulators
+      const size_t nacc = (size_t)a.cap_blocks * CB_ROWS * npairs;
+#pragma unroll
+      for (int q = 0; q < CB_TPT; ++q) {
+        const int task = tid + q * CB_THREADS;
+        if (task >= ntasks) break;
+        const int r = task % CB_ROWS, p = task / CB_ROWS;
+        if (r >= nb) continue;
+        const size_t i = ((size_t)rb * CB_ROWS + r) * npairs + p;
+        atomicAdd(a.cacc + i, dsum[q]);
+        atomicAdd(a.cacc + nacc + i, esum[q]);
+        atomicAdd(a.cacc + 2 * nacc + i, (double)asum[q]);
+      }
+      if (tid < nb && undecided[tid]) a.cflag[rb * CB_ROWS + tid] = 1;
+      __syncthreads();
+      continue;
+    }
     // certify: a row is decided when every pair clears its bound
     double* decs = xc;  // [CB_ROWS][npairs <= 48]: 24.6 KB over the free staging buffers (xc + sc, 34.8 KB)
 #pragma unroll
@@ -854,7 +1014,7 @@ __global__ void __launch_bounds__(CB_THREADS, 2) svm_certify_kernel(const Args a
       const double dec = __dsub_rn(dsum[q], -rho);
       const double tol2 = esum[q] + 2.0 * gamma_n(a.n_sv + 2) * (asum[q] + fabs(rho)) + 1e-300;
       if (a.is_svr) {
-        if (!(fabs(dec) > tol2)) atomicOr(&undecided[r], 1);
+        if (!f32_round_certain(dec, tol2)) atomicOr(&undecided[r], 1);
       } else if (!(fabs(dec) > tol2)) {
         atomicOr(&uncm[r], 1ull << p);
       }
@@ -908,6 +1068,147 @@ __global__ void __launch_bounds__(CB_THREADS, 2) svm_certify_kernel(const Args a
       }
     }
     __syncthreads();
+  }
+}
+
+// Decisions of the SV-split row blocks of the full certifying tier (see
+// Args::cacc): the same certificate as the in-CTA finalize, with the summation
+// bound widened for the split (partial sums per unit, then <= n_sv / CB_SPAN
+// float64 atomic additions in any order: gamma_{n_sv + 64}).
+__global__ void __launch_bounds__(128) svm_certify_finish_kernel(const Args a) {
+  const int nq = *a.queue_len;
+  const int n = min(nq, a.cap_blocks * CB_ROWS);
+  const int npairs = a.is_svr ? 1 : a.pairs;
+  const int C = a.C;
+  const size_t nacc = (size_t)a.cap_blocks * CB_ROWS * npairs;
+  const double gs = 2.0 * gamma_n(a.n_sv + 64);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int64_t row = a.queue[i];
+    bool exact = a.cflag[i] != 0;
+    double d[CB_MAXP];
+    unsigned long long uncm = 0ull;
+    for (int p = 0; p < npairs; ++p) {
+      const size_t k = (size_t)i * npairs + p;
+      const double rho = (double)a.intercept[p];
+      const double dec = __dsub_rn(a.cacc[k], -rho);
+      const double tol2 = a.cacc[nacc + k] * (1.0 + 1e-9) + gs * (a.cacc[2 * nacc + k] * (1.0 + 1e-12) + fabs(rho)) +
+                          1e-300;
+      d[p] = dec;
+      if (a.is_svr) {
+        if (!f32_round_certain(dec, tol2)) exact = true;
+      } else if (!(fabs(dec) > tol2)) {
+        uncm |= 1ull << p;
+      }
+    }
+    int best = -1;
+    if (!exact && !a.is_svr && uncm) {
+      exact = a.dec_out != nullptr;
+      if (!exact) {
+        int vmin[MAXC], unc[MAXC];
+        for (int c = 0; c < C; ++c) vmin[c] = unc[c] = 0;
+        int p = 0;
+        for (int ci = 0; ci < C; ++ci)
+          for (int cj = ci + 1; cj < C; ++cj, ++p) {
+            if (!isfinite(d[p])) exact = true;
+            if ((uncm >> p) & 1ull) { ++unc[ci]; ++unc[cj]; }
+            else if (d[p] > 0) ++vmin[ci];
+            else ++vmin[cj];
+          }
+        if (!exact) best = robust_vote(vmin, unc, C);
+        exact = best < 0;
+      }
+    }
+    if (exact) {
+      a.queue2[atomicAdd(a.queue2_len, 1)] = (int32_t)row;
+    } else if (best >= 0) {
+      store_out(a.y, row, a.out_dt, a.classes[best]);
+    } else if (a.is_svr) {
+      store_out(a.y, row, a.out_dt, (double)(float)d[0]);
+      if (a.dec_out) a.dec_out[row] = d[0];
+    } else {
+      int vote[MAXC];
+      for (int c = 0; c < C; ++c) vote[c] = 0;
+      int p = 0;
+      for (int ci = 0; ci < C; ++ci)
+        for (int cj = ci + 1; cj < C; ++cj, ++p) {
+          if (d[p] > 0) ++vote[ci]; else ++vote[cj];
+        }
+      int bc = 0;
+      for (int c = 1; c < C; ++c)
+        if (vote[c] > vote[bc]) bc = c;
+      store_out(a.y, row, a.out_dt, a.classes[bc]);
+      if (a.dec_out)
+        for (int q = 0; q < npairs; ++q) a.dec_out[row * npairs + q] = d[q];
+    }
+  }
+}
+
+// Pair tier decisions: the entry's pair resolved from the summed units, the
+// other pairs' signs from the fast path; rows still open go to the full tier.
+__global__ void __launch_bounds__(128) svm_pair_finish_kernel(const Args a, const int* n_sv_start) {
+  __shared__ int off[65];
+  const int C = a.C;
+  if (threadIdx.x == 0) {
+    int e = 0;
+    for (int q = 0; q < a.pairs; ++q) {
+      off[q] = e;
+      e += a.pcount[q];
+    }
+    off[a.pairs] = e;
+  }
+  __syncthreads();
+  const int n = *a.pq_len;
+  const size_t np = (size_t)a.n_rows;
+  const double gs = 2.0 * gamma_n(a.n_sv + 64);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int bp = 0;
+    while (i >= off[bp + 1]) ++bp;
+    const int64_t row = a.ps_row[i];
+    const double rho = (double)a.intercept[bp];
+    const double dec = __dsub_rn(a.pacc[i], -rho);
+    const double tol2 = a.pacc[np + i] * (1.0 + 1e-9) + gs * (a.pacc[2 * np + i] * (1.0 + 1e-12) + fabs(rho)) + 1e-300;
+    if (a.pflag[i] || !(fabs(dec) > tol2)) {
+      a.queue2[atomicAdd(a.queue2_len, 1)] = (int32_t)row;
+      continue;
+    }
+    unsigned long long sg = a.ps_sign[i] & ~(1ull << bp);
+    if (dec > 0) sg |= 1ull << bp;
+    const unsigned long long un = a.ps_unc[i] & ~(1ull << bp);
+    int vote[MAXC], unc[MAXC];
+    for (int c = 0; c < C; ++c) vote[c] = unc[c] = 0;
+    int q = 0;
+    for (int ci = 0; ci < C; ++ci)
+      for (int cj = ci + 1; cj < C; ++cj, ++q) {
+        if ((un >> q) & 1ull) { ++unc[ci]; ++unc[cj]; }
+        else if ((sg >> q) & 1ull) ++vote[ci];
+        else ++vote[cj];
+      }
+    const int best = robust_vote(vote, unc, C);
+    if (best >= 0) store_out(a.y, row, a.out_dt, a.classes[best]);
+    else a.queue[atomicAdd(a.queue_len, 1)] = (int32_t)row;  // the full certifying tier decides
+  }
+}
+
+// Pair tier: bucket the fast path's one-uncertain-pair rows by that pair
+// (counting sort: per-pair offsets from the counts, cursors by atomics; the
+// order inside a bucket does not matter -- every row is decided on its own).
+__global__ void __launch_bounds__(256) svm_pair_scatter_kernel(const Args a) {
+  __shared__ int off[64];
+  if (threadIdx.x == 0) {
+    int e = 0;
+    for (int q = 0; q < a.pairs; ++q) {
+      off[q] = e;
+      e += a.pcount[q];
+    }
+  }
+  __syncthreads();
+  const int n = *a.pq_len;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int q = a.pq_pair[i];
+    const int dst = off[q] + atomicAdd(a.pcur + q, 1);
+    a.ps_row[dst] = a.pq_row[i];
+    a.ps_sign[dst] = a.pq_sign[i];
+    a.ps_unc[dst] = a.pq_unc[i];
   }
 }
 
@@ -1234,14 +1535,51 @@ int cmlb_svm_run(const cmlb_svm* m, const float* x, int64_t n_rows, int64_t ldx,
   }();
   a.prob_tol = prob_tol;
   keep_pool(m->device);
+  // scratch: counters (queue lengths, 64 pair counts, 64 pair cursors), the
+  // two row queues, and the pair tier's entries (unsorted + bucketed)
+  const bool certify = (a.is_svr ? 1 : a.pairs) <= svm::CB_MAXP && !a.no_exact;
+  static const bool no_pair_tier = std::getenv("CMLB_SVM_NO_PAIR_TIER") != nullptr;  // measurement knob
+  const bool pair_tier = certify && !a.is_svr && !decision && a.pairs <= 64 && !no_pair_tier;
+  const size_t nhead = 256;  // int32 slots
+  const int npairs_c = a.is_svr ? 1 : a.pairs;
+  const int cap_blocks = certify ? (int)std::min<int64_t>(svm::CB_CAP_BLOCKS, ceil_div(n_rows, svm::CB_ROWS)) : 0;
+  const size_t nacc = (size_t)cap_blocks * svm::CB_ROWS * npairs_c;
+  const size_t acc_bytes = nacc * 3 * sizeof(double) + (size_t)cap_blocks * svm::CB_ROWS * sizeof(int32_t);
+  // pair tier: [pacc 3 x n doubles][pflag n int32] zeroed with the head
+  const size_t pacc_bytes = pair_tier ? (size_t)n_rows * 3 * sizeof(double) + ((size_t)n_rows * 4 + 7) / 8 * 8 : 0;
+  const size_t zero_bytes = acc_bytes + pacc_bytes;
+  const size_t bytes = zero_bytes + (nhead + 2 * (size_t)n_rows) * sizeof(int32_t) +
+                       (pair_tier ? (size_t)n_rows * (3 * sizeof(int32_t) + 4 * sizeof(unsigned long long)) : 0);
   void* scratch = nullptr;
-  CMLB_CUDA(cudaMallocAsync(&scratch, (size_t)(2 * n_rows + 8) * sizeof(int32_t), s));
-  a.queue_len = static_cast<int32_t*>(scratch);
-  a.queue2_len = a.queue_len + 1;
-  a.queue = a.queue_len + 8;
+  CMLB_CUDA(cudaMallocAsync(&scratch, bytes, s));
+  // [cacc doubles][cflag int32][head int32 ...]
+  a.cacc = cap_blocks ? static_cast<double*>(scratch) : nullptr;
+  a.cflag = reinterpret_cast<int32_t*>(static_cast<double*>(scratch) + nacc * 3);
+  a.cap_blocks = cap_blocks;
+  a.pacc = reinterpret_cast<double*>(static_cast<uint8_t*>(scratch) + acc_bytes);  // 8-aligned: acc_bytes % 8 == 0
+  a.pflag = reinterpret_cast<int32_t*>(a.pacc + (pair_tier ? 3 * (size_t)n_rows : 0));
+  int32_t* head = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(scratch) + zero_bytes);
+  a.queue_len = head;
+  a.queue2_len = head + 1;
+  a.pq_len = head + 2;
+  a.pcount = head + 64;
+  a.pcur = head + 128;
+  a.queue = head + nhead;
   a.queue2 = a.queue + n_rows;
+  if (pair_tier) {
+    unsigned long long* sg = reinterpret_cast<unsigned long long*>(a.queue2 + n_rows);  // 8-aligned: nhead + 2n int32
+    a.pq_sign = sg;
+    a.ps_sign = sg + n_rows;
+    a.pq_unc = sg + 2 * n_rows;
+    a.ps_unc = sg + 3 * n_rows;
+    a.pq_row = reinterpret_cast<int32_t*>(sg + 4 * n_rows);
+    a.pq_pair = a.pq_row + n_rows;
+    a.ps_row = a.pq_pair + n_rows;
+  } else {
+    a.pq_row = nullptr;
+  }
   int st = CMLB_OK;
-  if (cudaMemsetAsync(a.queue_len, 0, 2 * sizeof(int32_t), s) != cudaSuccess) st = fail(CMLB_E_DEVICE, "memset");
+  if (cudaMemsetAsync(scratch, 0, zero_bytes + nhead * sizeof(int32_t), s) != cudaSuccess) st = fail(CMLB_E_DEVICE, "memset");
   if (!st) {
     st = launch_any(m->CP, a, n_rows, m->tc_smem, s);
   }
@@ -1253,16 +1591,48 @@ int cmlb_svm_run(const cmlb_svm* m, const float* x, int64_t n_rows, int64_t ldx,
   // certifying tier (float64 Gram, rigorous bound against libsvm) for the
   // queued rows; what it cannot decide goes on to the libsvm-order exact path
   svm::Args ax = a;
-  const bool certify = (a.is_svr ? 1 : a.pairs) <= svm::CB_MAXP && !a.no_exact;
   if (!st && certify) {
-    cudaError_t e = cudaFuncSetAttribute(svm::svm_certify_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const int grid = std::max(1, std::min<int>(2 * num_sms(m->device), (int)ceil_div(n_rows, svm::CB_ROWS)));
+    if (pair_tier) {
+      svm::svm_pair_scatter_kernel<<<std::max(1, std::min<int>(2 * num_sms(m->device), (int)ceil_div(n_rows, 256))),
+                                     256, 0, s>>>(a);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) st = cuda_fail(e, "svm_pair_scatter_kernel");
+      else note_launch();
+      if (!st) e = cudaFuncSetAttribute(svm::svm_certify_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)svm::CB_SMEM);
+      if (!st && e != cudaSuccess) st = cuda_fail(e, "svm_certify smem");
+      if (!st) {
+        svm::svm_certify_kernel<true><<<8 * num_sms(m->device), svm::CB_THREADS, svm::CB_SMEM, s>>>(a, m->sv_start);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) st = cuda_fail(e, "svm_certify_kernel<pair>");
+        else note_launch();
+      }
+      if (!st) {
+        svm::svm_pair_finish_kernel<<<std::max(1, std::min<int>(num_sms(m->device), (int)ceil_div(n_rows, 128))), 128, 0,
+                                      s>>>(a, m->sv_start);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) st = cuda_fail(e, "svm_pair_finish_kernel");
+        else note_launch();
+      }
+    }
+    cudaError_t e = cudaFuncSetAttribute(svm::svm_certify_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)svm::CB_SMEM);
-    if (e != cudaSuccess) st = cuda_fail(e, "svm_certify smem");
+    if (!st && e != cudaSuccess) st = cuda_fail(e, "svm_certify smem");
     if (!st) {
-      const int grid = std::max(1, std::min<int>(2 * num_sms(m->device), (int)ceil_div(n_rows, svm::CB_ROWS)));
-      svm::svm_certify_kernel<<<grid, svm::CB_THREADS, svm::CB_SMEM, s>>>(a, m->sv_start);
+      // split units: up to cap_blocks x ceil(n_sv / CB_SPAN) CTAs of work
+      const int ugrid = std::max(grid, (int)std::min<int64_t>(8 * num_sms(m->device),
+                                                               (int64_t)cap_blocks * ceil_div(a.n_sv, svm::CB_SPAN)));
+      svm::svm_certify_kernel<false><<<ugrid, svm::CB_THREADS, svm::CB_SMEM, s>>>(a, m->sv_start);
       e = cudaGetLastError();
       if (e != cudaSuccess) st = cuda_fail(e, "svm_certify_kernel");
+      else note_launch();
+    }
+    if (!st && cap_blocks) {
+      svm::svm_certify_finish_kernel<<<std::max(1, std::min<int>(num_sms(m->device), (int)ceil_div((int64_t)cap_blocks * svm::CB_ROWS, 128))),
+                                       128, 0, s>>>(a);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) st = cuda_fail(e, "svm_certify_finish_kernel");
       else note_launch();
     }
     ax.queue = a.queue2;
@@ -1274,6 +1644,21 @@ int cmlb_svm_run(const cmlb_svm* m, const float* x, int64_t n_rows, int64_t ldx,
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) st = cuda_fail(e, "svm_exact_kernel");
     else note_launch();
+  }
+  static const char* dump_unc = std::getenv("CMLB_SVM_DUMP_UNC");  // measurement knob: fast-path uncertain-pair masks
+  if (!st && pair_tier && dump_unc) {
+    int32_t nq = 0;
+    cudaMemcpyAsync(&nq, a.pq_len, sizeof(nq), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    std::vector<unsigned long long> h((size_t)nq);
+    if (nq) cudaMemcpy(h.data(), a.pq_unc, (size_t)nq * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    int32_t ql[3] = {0, 0, 0};
+    cudaMemcpy(ql, a.queue_len, 3 * sizeof(int32_t), cudaMemcpyDeviceToHost);
+    std::fprintf(stderr, "svm queues: rows %lld pair-tier %d full-certify %d exact %d\n", (long long)n_rows, ql[2], ql[0], ql[1]);
+    if (FILE* fh = std::fopen(dump_unc, "wb")) {
+      std::fwrite(h.data(), sizeof(unsigned long long), h.size(), fh);
+      std::fclose(fh);
+    }
   }
   if (!st && exact_rows) {
     cudaError_t e = cudaMemcpyAsync(exact_rows, ax.queue_len, sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
