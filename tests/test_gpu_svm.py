@@ -104,6 +104,30 @@ def test_svm_vs_c_oracle_random(F, n_sv, C, kernel):
     assert n_exact < 0.25 * len(x), n_exact
 
 
+@pytest.mark.parametrize("F,n_sv,C,kernel", [(784, 1000, 10, "rbf"), (100, 600, 6, "rbf"), (64, 513, 4, "poly"),
+                                              (50, 257, 5, "sigmoid")])
+def test_svm_classes_only_vote_robust_and_pair_tier(F, n_sv, C, kernel):
+    """Classes without decision values: rows with uncertain pairs are settled
+    by the vote-robust check, the pair tier (one decisive pair from its two
+    classes' SVs) or the SV-split certifying tier -- every class must still
+    equal the libsvm-order oracle, including near-tie rows built on the
+    boundary between two classes' support vectors."""
+    m = _synthetic_svc(F, n_sv, C, kernel, seed=F + n_sv + 1)
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal((4096, F)).astype(np.float32)
+    sv = np.asarray(m.support_vectors, np.float32)
+    ns = np.cumsum((0,) + tuple(m.n_support))
+    for r in range(512):  # midpoints between SVs of different classes: small decision margins
+        ca, cb = rng.choice(C, 2, replace=False)
+        ja = rng.integers(ns[ca], ns[ca + 1])
+        jb = rng.integers(ns[cb], ns[cb + 1])
+        t = np.float32(rng.uniform(0.45, 0.55))
+        x[r] = t * sv[ja] + (1 - t) * sv[jb]
+    y, _, n_exact = run_svm(m, x, decision=False)
+    _, vote = ext.svm_decision(m, x)
+    np.testing.assert_array_equal(y.ravel(), np.asarray(m.classes, np.float64)[vote])
+
+
 def test_svm_nonfinite_rows_take_exact_path():
     m = _synthetic_svc(40, 300, 3, "rbf", seed=3)
     x = np.random.default_rng(1).standard_normal((300, 40)).astype(np.float32)
