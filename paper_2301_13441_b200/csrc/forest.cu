@@ -142,6 +142,8 @@ struct ForestArgs {
   const float* uthr;          // per feature: perfect Eytzinger table (see rank_eyt), 2^L - 1 entries
   const int32_t* uoff;        // [F + 1] table offsets (4-aligned)
   const int32_t* ulev;        // [F] levels L of each feature's table (0: no thresholds)
+  const uint4* uprm;          // [F] bucket tables (rank_bkt): {scale, offset, last bucket, start-table byte offset | steps << 20}
+  int rank_bkt;               // 1: bucket tables (default), 0: perfect Eytzinger tables (CMLB_RANK_EYT=1)
   int node_off_bytes;         // byte offset of the node words inside a ranked tree blob
   int stage_off;              // byte offset of the ranking staging area inside the chunk area
   int stage_bufs;             // 1 or 2 staging buffers
@@ -655,6 +657,39 @@ __device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
   return v;
 }
 
+// rank(x) by a bucket table: b(x) = clamp(floor(fma(x, s, c)), 0, B - 1) is
+// monotone in x, so every threshold of an earlier bucket is < x and every one
+// of a later bucket is > x; rank(x) = start[b(x)] + #{u in bucket b(x) : u < x}.
+// The bucket's slice of the sorted thresholds is searched by binary lifting
+// with the feature's fixed step count T (2^T - 1 >= its largest bucket): the
+// slots past the bucket hold later buckets' thresholds (> x) or +inf padding,
+// so they never count.  NaN lands in bucket 0 and compares false (rank 0);
+// +inf lands in the last bucket and counts every threshold.  The host builds
+// start[] with the same float operations (fmaf, clamp, floor).
+template <int R>
+__device__ __forceinline__ void rank_bkt(uint32_t base, uint4 prm, const float (&x)[R], uint32_t (&out)[R]) {
+  const float s = __uint_as_float(prm.x), c = __uint_as_float(prm.y), bmax = __uint_as_float(prm.z);
+  const uint32_t soff = prm.w & 0xFFFFFu, T = prm.w >> 20;
+  uint32_t q[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const float t = fminf(fmaxf(__fmaf_rn(x[r], s, c), 0.0f), bmax);
+    const uint32_t b = (uint32_t)__float2int_rd(t);
+    q[r] = base + 4u * lds_u16(base + soff + 2u * b) - 4u;  // address of u[start - 1]
+  }
+  for (uint32_t st4 = (4u << T) >> 1; st4 >= 4u; st4 >>= 1) {
+    float u[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(u[r]) : "r"(q[r] + st4));
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (u[r] < x[r]) q[r] += st4;
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) out[r] = (q[r] + 4u - base) >> 2;
+}
+
+
 template <int CT>
 __device__ __forceinline__ void load_payload_shared(uint32_t addr, float (&v)[CT]) {
   if constexpr (CT == 1) {
@@ -740,7 +775,8 @@ __device__ __forceinline__ void rank_tile(const ForestArgs& a, uint8_t* smem, ui
     __syncthreads();  // stage f landed for everyone; buffer (f+1)&1 is free
     if (dbl && f + 1 < F) issue_stage(f + 1);
     uint32_t r[RPT];
-    rank_eyt<RPT>(smem_u32(stage_f(f & 1)), __ldg(a.ulev + f), xq, r);
+    if (a.rank_bkt) rank_bkt<RPT>(smem_u32(stage_f(f & 1)), __ldg(a.uprm + f), xq, r);
+    else rank_eyt<RPT>(smem_u32(stage_f(f & 1)), __ldg(a.ulev + f), xq, r);
     uint8_t* xrow = reinterpret_cast<uint8_t*>(xr) + (size_t)f * ROWS * 2;
 #pragma unroll
     for (int k = 0; k < RPT; ++k) *reinterpret_cast<uint16_t*>(xrow + pb[k]) = (uint16_t)r[k];
@@ -1097,7 +1133,8 @@ __global__ void __launch_bounds__(RANK_THREADS, 2) forest_rank_kernel(const Fore
       __syncwarp();
     }
     uint32_t r[RPT];
-    rank_eyt<RPT>(stage0 + (uint32_t)b * stage_bytes, __ldg(a.ulev + f), xq, r);
+    if (a.rank_bkt) rank_bkt<RPT>(stage0 + (uint32_t)b * stage_bytes, __ldg(a.uprm + f), xq, r);
+    else rank_eyt<RPT>(stage0 + (uint32_t)b * stage_bytes, __ldg(a.ulev + f), xq, r);
     mbar_arrive(&empty_bar[b]);  // each thread releases its own reads of buffer b
 #pragma unroll
     for (int p = 0; p < NP; ++p)
@@ -1584,6 +1621,8 @@ struct cmlb_forest {
   float* uthr = nullptr;
   int32_t* uoff = nullptr;
   int32_t* ulev = nullptr;
+  uint4* uprm = nullptr;
+  int rank_bkt = 1;
   int ntt = 256, stage_cap = 0, node_off_bytes = 0, rcfg = 0, stage_off = 0, stage_bufs = 2;
   size_t rank_smem = 0;  // SKEW / RANKED: forest_rank_kernel's staging buffers
   int rank_nb = 2;       // forest_rank_kernel staging depth (2 or 3)
@@ -1595,7 +1634,7 @@ struct cmlb_forest {
     cudaFree(pro);
     cudaFree(blob); cudaFree(slot_leaf); cudaFree(gnode); cudaFree(node_off);
     cudaFree(gpay); cudaFree(leaf_off); cudaFree(sched); cudaFree(classes);
-    cudaFree(uthr); cudaFree(uoff); cudaFree(ulev);
+    cudaFree(uthr); cudaFree(uoff); cudaFree(ulev); cudaFree(uprm);
   }
 };
 
@@ -1941,6 +1980,95 @@ static int eyt_levels(size_t n) {
 }
 static size_t eyt_floats(size_t n) { return ((((size_t)1 << eyt_levels(n)) - 1) + 3) / 4 * 4; }
 
+// The per-feature rank tables, both formats (rank_eyt / rank_bkt), packed
+// back to back in 16-byte units (each feature's block is one TMA transfer).
+struct RankTables {
+  std::vector<float> thr;        // blocks
+  std::vector<int32_t> off;      // [F + 1] block offsets (floats)
+  std::vector<int32_t> lev;      // [F] Eytzinger levels
+  std::vector<uint4> prm;        // [F] bucket parameters
+  size_t cap = 0;                // largest block (floats)
+};
+
+static int bkt_bucket(float v, float s, float c, float bmax) {
+  return (int)std::floor(std::fmin(std::fmax(std::fmaf(v, s, c), 0.0f), bmax));
+}
+
+static void build_rank_tables(const std::vector<std::vector<float>>& U, bool bkt, RankTables& t) {
+  const int F = (int)U.size();
+  t.thr.clear();
+  t.off.assign(F + 1, 0);
+  t.lev.assign(F, 0);
+  t.prm.assign(F, make_uint4(0, 0, 0, 0));
+  t.cap = 4;
+  for (int k = 0; k < F; ++k) {
+    const auto& u = U[k];  // sorted, unique
+    const size_t n = u.size();
+    std::vector<float> e;
+    if (!bkt) {
+      // sorted thresholds padded with +inf to a perfect implicit tree of
+      // 2^L - 1 nodes, in Eytzinger (BFS) order
+      const int L = eyt_levels(n);
+      const size_t P = ((size_t)1 << L) - 1;
+      e.assign(P, INFINITY);
+      size_t next = 0;
+      std::vector<size_t> st;
+      size_t node = 1;
+      while (node <= P || !st.empty()) {
+        if (node <= P) { st.push_back(node); node = 2 * node; continue; }
+        node = st.back();
+        st.pop_back();
+        e[node - 1] = next < n ? u[next] : INFINITY;
+        ++next;
+        node = 2 * node + 1;
+      }
+      t.lev[k] = L;
+    } else {
+      // bucket table: B buckets over [u_0, u_n-1] (B = 2n rounded up to a
+      // power of two, <= 8192), start[b] = #{u : bucket(u) < b}
+      int B = 1;
+      while (B < 8192 && (size_t)B < 2 * n) B *= 2;
+      float sc = 0.0f, c0 = 0.0f;
+      if (n >= 2) {
+        sc = (float)B / (u[n - 1] - u[0]);
+        if (!(sc < 1e30f)) sc = 1e30f;
+        c0 = -u[0] * sc;
+      }
+      const float bmax = (float)(B - 1);
+      std::vector<int> cnt(B, 0);
+      for (float v : u) ++cnt[bkt_bucket(v, sc, c0, bmax)];
+      int mx = 0;
+      for (int b = 0; b < B; ++b) mx = std::max(mx, cnt[b]);
+      int T = 0;
+      while ((1 << T) - 1 < mx) ++T;
+      const size_t pad = (size_t)1 << T;  // binary lifting reads at most 2^T - 1 slots past a bucket's start
+      e.assign(u.begin(), u.end());
+      e.resize(n + pad, INFINITY);
+      const uint32_t soff = (uint32_t)e.size() * 4u;
+      std::vector<uint16_t> start(B);
+      int acc = 0;
+      for (int b = 0; b < B; ++b) { start[b] = (uint16_t)acc; acc += cnt[b]; }
+      const size_t nw = (B + 1) / 2;
+      for (size_t w = 0; w < nw; ++w) {
+        const uint32_t lo = start[2 * w], hi = 2 * w + 1 < (size_t)B ? start[2 * w + 1] : 0u;
+        uint32_t word = lo | (hi << 16);
+        float fw;
+        std::memcpy(&fw, &word, 4);
+        e.push_back(fw);
+      }
+      uint32_t us, uc, ub;
+      std::memcpy(&us, &sc, 4);
+      std::memcpy(&uc, &c0, 4);
+      std::memcpy(&ub, &bmax, 4);
+      t.prm[k] = make_uint4(us, uc, ub, soff | ((uint32_t)T << 20));
+    }
+    while (e.size() % 4) e.push_back(INFINITY);
+    t.thr.insert(t.thr.end(), e.begin(), e.end());
+    t.off[k + 1] = (int32_t)t.thr.size();
+    t.cap = std::max(t.cap, e.size());
+  }
+}
+
 static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out) {
   if (int s = validate(d)) return s;
   std::unique_ptr<cmlb_forest> f(new cmlb_forest());
@@ -2016,6 +2144,9 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
   // ranked plan: per-feature sorted unique thresholds, smem split between the
   // u16 rank tile, two staging buffers (ranking) and the tree chunk (walk)
   std::vector<std::vector<float>> U;
+  RankTables rtab;
+  static const bool rank_eyt_env = getenv("CMLB_RANK_EYT") != nullptr;  // measurement knob
+  f->rank_bkt = rank_eyt_env ? 0 : 1;
   const int saved_rpt = f->rpt;
   bool ranked_ok = D >= 1 && D <= PERFECT_MAX_DEPTH && f->CT <= 8 && f->agg != CMLB_AGG_NONE;
   int r_ntt = 0, r_rpt = 0, r_chunk = 0, r_tree_bytes = 0, r_node_off = 0, r_stage = 0, r_stage_off = 0, r_stage_bufs = 2;
@@ -2029,6 +2160,7 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
       u.erase(std::unique(u.begin(), u.end()), u.end());
       max_nf = std::max(max_nf, u.size());
     }
+    build_rank_tables(U, f->rank_bkt != 0, rtab);
     const int ni_r = (1 << D) - 1, ns_r = 1 << D;
     r_node_off = ns_r * f->CT * 4;
     r_tree_bytes = (int)(((size_t)r_node_off + (size_t)ni_r * 4 + 15) / 16 * 16);
@@ -2048,7 +2180,7 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
       f->rcfg = ci; f->rpt = rpt;
       if (ranked_for(*f) == nullptr) continue;        // not instantiated for this shape
       if ((size_t)f->F * rows / 2 > 65535) continue;  // feature word offset must fit 16 bits
-      const size_t cap = eyt_floats(max_nf);
+      const size_t cap = rtab.cap;
       const size_t xr = ((size_t)f->F * rows * 2 + 15) / 16 * 16;
       if (xr + cap * 4 > SMEM_LIMIT) continue;
       const size_t avail = SMEM_LIMIT - xr;
@@ -2105,7 +2237,7 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
       if (ci < 0 || ci >= N_SKEW_CFGS) continue;
       const int rows = SKEW_CFGS[ci].ntt * SKEW_CFGS[ci].rpt;
       if ((size_t)f->F * rows / 2 > 65535) continue;
-      const size_t cap = eyt_floats(max_nf);
+      const size_t cap = rtab.cap;
       const size_t xr = ((size_t)f->F * rows * 2 + 15) / 16 * 16;
       if (xr + cap * 4 > SMEM_LIMIT || xr + 2 * (size_t)s_gbytes > SMEM_LIMIT) continue;
       const int G = (f->T + 31) / 32;
@@ -2178,36 +2310,10 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
     if (int st = upload(&f->slot_leaf, slot_leaf.data(), slot_leaf.size())) return st;
   }
   if (f->variant == CMLB_FOREST_RANKED || f->variant == CMLB_FOREST_SKEW) {
-    // per feature: the sorted unique thresholds padded with +inf to a perfect
-    // implicit tree of 2^L - 1 nodes, in Eytzinger (BFS) order (rank_eyt)
-    std::vector<float> uthr;
-    std::vector<int32_t> uoff(f->F + 1, 0), ulev(f->F, 0);
-    for (int k = 0; k < f->F; ++k) {
-      const auto& u = U[k];
-      const int L = eyt_levels(u.size());
-      const size_t P = ((size_t)1 << L) - 1;
-      std::vector<float> e(P);
-      size_t next = 0;
-      // in-order walk of the implicit tree assigns sorted elements to BFS slots
-      std::vector<size_t> st;
-      size_t node = 1;
-      while (node <= P || !st.empty()) {
-        if (node <= P) { st.push_back(node); node = 2 * node; continue; }
-        node = st.back();
-        st.pop_back();
-        e[node - 1] = next < u.size() ? u[next] : INFINITY;
-        ++next;
-        node = 2 * node + 1;
-      }
-      // each table starts 16-byte aligned and spans whole 16-byte units (TMA)
-      ulev[k] = L;
-      uthr.insert(uthr.end(), e.begin(), e.end());
-      while (uthr.size() % 4) uthr.push_back(INFINITY);
-      uoff[k + 1] = (int32_t)uthr.size();
-    }
-    if (int st = upload(&f->uthr, uthr.data(), uthr.size())) return st;
-    if (int st = upload(&f->uoff, uoff.data(), uoff.size())) return st;
-    if (int st = upload(&f->ulev, ulev.data(), ulev.size())) return st;
+    if (int st = upload(&f->uthr, rtab.thr.data(), rtab.thr.size())) return st;
+    if (int st = upload(&f->uoff, rtab.off.data(), rtab.off.size())) return st;
+    if (int st = upload(&f->ulev, rtab.lev.data(), rtab.lev.size())) return st;
+    if (int st = upload(&f->uprm, rtab.prm.data(), rtab.prm.size())) return st;
   }
 
   if (f->variant == CMLB_FOREST_SKEW) {
@@ -2303,7 +2409,7 @@ static int run_forest(const cmlb_forest* f, const float* x, int64_t n_rows, int6
   a.agg = f->agg; a.tail = f->tail; a.out_dt = f->out_dt; a.dense_sel = f->dense_sel;
   a.n_classes = f->n_classes; a.lr = f->lr; a.base = f->base; a.classes = f->classes;
   a.pay_off = f->pay_off; a.feat_off = f->feat_off;
-  a.uthr = f->uthr; a.uoff = f->uoff; a.ulev = f->ulev; a.stage_cap = f->stage_cap; a.node_off_bytes = f->node_off_bytes; a.stage_off = f->stage_off; a.stage_bufs = f->stage_bufs;
+  a.uthr = f->uthr; a.uoff = f->uoff; a.ulev = f->ulev; a.uprm = f->uprm; a.rank_bkt = f->rank_bkt; a.stage_cap = f->stage_cap; a.node_off_bytes = f->node_off_bytes; a.stage_off = f->stage_off; a.stage_bufs = f->stage_bufs;
   KernelFn k = kernel_for(*f);
   a.mma_k = f->mma_k; a.mma_n = f->mma_n; a.mma_feat_off = f->mma_feat_off; a.mma_thr_off = f->mma_thr_off;
   a.mma_pay_off = f->mma_pay_off;
