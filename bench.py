@@ -222,12 +222,33 @@ def _class_width(c: int) -> int:
     return 32
 
 
+def _bucket_steps(u: np.ndarray) -> int:
+    """Binary-lifting steps of one feature's bucket table (forest.cu
+    build_rank_tables): B = 2n rounded up to a power of two (<= 8192) buckets
+    over [u_0, u_n-1]; T = bits of the largest bucket count."""
+    n = u.size
+    B = 1
+    while B < 8192 and B < 2 * n:
+        B *= 2
+    if n >= 2:
+        s = np.float32(B) / (u[-1] - u[0])
+        s = s if s < np.float32(1e30) else np.float32(1e30)
+        c = np.float32(-u[0] * s)
+        t = (u.astype(np.float64) * np.float64(s) + np.float64(c)).astype(np.float32)
+        b = np.floor(np.clip(t, 0, B - 1)).astype(np.int64)
+    else:
+        b = np.zeros(n, np.int64)
+    mx = int(np.bincount(b, minlength=B).max()) if n else 0
+    return int(mx).bit_length()
+
+
 def forest_wavefronts_row(spec, info) -> dict:
     """Algorithmic shared-memory wavefronts per row of the ranked/skew walk:
     per tree D node-word loads + D rank loads + the payload load (CT floats,
-    CT wavefronts per warp of 32), per feature the perfect-Eytzinger search
-    (L_f = bit_length(n_f) levels, one load each; the ranks go to global
-    memory), all at one wavefront per warp-wide conflict-free access, / 32 rows."""
+    CT wavefronts per warp of 32), per feature the bucket-table search (the
+    start lookup + T_f binary-lifting steps, T_f from the same bucketing as
+    forest.cu build_rank_tables; the ranks go to global memory), all at one
+    wavefront per warp-wide conflict-free access, / 32 rows."""
     if info["variant"] not in ("ranked", "skew"):
         return None
     D = int(info["depth"])
@@ -239,7 +260,7 @@ def forest_wavefronts_row(spec, info) -> dict:
     search = 0
     for f in np.unique(feats):
         nf = np.unique(thr[feats == f]).size
-        search += int(nf).bit_length()
+        search += 1 + _bucket_steps(np.unique(thr[feats == f]).astype(np.float32))
     walk = T_walked * (2 * D + CT)
     return {"walk": walk / 32.0, "rank": search / 32.0, "total": (walk + search) / 32.0,
             "trees_walked": T_walked, "depth": D, "payload_floats": CT}
