@@ -1712,7 +1712,8 @@ static KernelFn ranked_for(const cmlb_forest& f) {
   const bool pw = f.C == 1;
   // the scalar (GBDT) shape with its depth as a constant: no level-loop control
   // in the walk (GBR1000 d10: ~10% of the walk's instructions)
-  if (pw && f.CT == 1 && f.rcfg == 8 && !getenv("CMLB_RANKED_RUNTIME_DEPTH")) {
+  static const bool runtime_depth = getenv("CMLB_RANKED_RUNTIME_DEPTH") != nullptr;  // measurement knob
+  if (pw && f.CT == 1 && f.rcfg == 8 && !runtime_depth) {
     if (f.depth == 10) return forest_ranked_kernel<1, 512, 1, 4, true, 10>;
     if (f.depth == 8) return forest_ranked_kernel<1, 512, 1, 4, true, 8>;
     if (f.depth == 6) return forest_ranked_kernel<1, 512, 1, 4, true, 6>;
