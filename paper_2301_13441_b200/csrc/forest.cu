@@ -2146,8 +2146,7 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
   // u16 rank tile, two staging buffers (ranking) and the tree chunk (walk)
   std::vector<std::vector<float>> U;
   RankTables rtab;
-  static const bool rank_eyt_env = getenv("CMLB_RANK_EYT") != nullptr;  // measurement knob
-  f->rank_bkt = rank_eyt_env ? 0 : 1;
+  f->rank_bkt = getenv("CMLB_RANK_EYT") ? 0 : 1;  // measurement knob (read per create, like CMLB_RANK_PASS)
   const int saved_rpt = f->rpt;
   bool ranked_ok = D >= 1 && D <= PERFECT_MAX_DEPTH && f->CT <= 8 && f->agg != CMLB_AGG_NONE;
   int r_ntt = 0, r_rpt = 0, r_chunk = 0, r_tree_bytes = 0, r_node_off = 0, r_stage = 0, r_stage_off = 0, r_stage_bufs = 2;
@@ -2162,6 +2161,12 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
       max_nf = std::max(max_nf, u.size());
     }
     build_rank_tables(U, f->rank_bkt != 0, rtab);
+    if (f->rank_bkt && 2 * rtab.cap * 4 > SMEM_LIMIT) {
+      // clustered thresholds made a bucket table too large for two staging
+      // buffers: the perfect Eytzinger tables are bounded by 2^14 floats
+      f->rank_bkt = 0;
+      build_rank_tables(U, false, rtab);
+    }
     const int ni_r = (1 << D) - 1, ns_r = 1 << D;
     r_node_off = ns_r * f->CT * 4;
     r_tree_bytes = (int)(((size_t)r_node_off + (size_t)ni_r * 4 + 15) / 16 * 16);

@@ -292,3 +292,50 @@ def test_auto_picks_skew_for_certified_large_forests():
     model, _, _ = bench.load_model()
     prog = api.compile_model(model).program(0)
     assert prog.forest().info()["variant"] == "skew"
+
+
+def _clustered_forest(rng, T, depth, F, C):
+    """A forest whose thresholds crowd into a few tiny intervals (plus far
+    outliers): bucket tables get large buckets (many binary-lifting steps)."""
+    m = _synthetic_forest(rng, T, depth, F, C)
+    from paper_2301_13441_b200.models import ForestModel, TreeArrays, TreeModel
+    trees = []
+    for t in m.trees:
+        a = t.arrays
+        thr = a.threshold.copy()
+        k = np.flatnonzero(~a.is_leaf)
+        pick = rng.random(k.size)
+        thr[k] = np.where(pick < 0.8, np.float32(1.0) + rng.integers(0, 4000, k.size).astype(np.float32) * np.float32(1e-7),
+                          np.where(pick < 0.9, np.float32(-3e6), np.float32(5e30))).astype(np.float32)
+        trees.append(TreeModel(t.model_type, F, TreeArrays(a.is_leaf, a.feature, thr, a.left, a.right, a.value), None))
+    return ForestModel(m.model_type, F, tuple(trees), m.aggregation, 1.0, 0.0, m.classes)
+
+
+@pytest.mark.parametrize("eyt", [0, 1])
+@pytest.mark.parametrize("rank_pass", [1, 0])
+def test_rank_tables_and_fused_ranking(eyt, rank_pass, monkeypatch):
+    """Both rank-table formats (bucket tables, CMLB_RANK_EYT=1 Eytzinger) and
+    both ranking placements (the rank pass, CMLB_RANK_PASS=0 per-tile in the
+    RANKED walk) are bit-exact, on ordinary and on clustered thresholds."""
+    if eyt:
+        monkeypatch.setenv("CMLB_RANK_EYT", "1")
+    if not rank_pass:
+        monkeypatch.setenv("CMLB_RANK_PASS", "0")
+    rng = np.random.default_rng(500 + 2 * eyt + rank_pass)
+    cases = [(_synthetic_forest(rng, 96, 8, 28, 2), 28), (_synthetic_forest(rng, 130, 7, 20, 1, True), 20),
+             (_clustered_forest(rng, 80, 7, 6, 2), 6)]
+    for m, F in cases:
+        x = rng.standard_normal((40_000, F)).astype(np.float32)
+        x[: 20_000] = np.float32(1.0) + rng.integers(-10, 4010, (20_000, F)).astype(np.float32) * np.float32(1e-7)
+        x[::101, 2] = np.nan
+        x[::103, 1] = np.inf
+        x[::107, 0] = -np.inf
+        x[::109, 3] = -0.0
+        want, want_leaves = fast.forest_predict(fast.PackedForest(m), x, want_leaves=True)
+        for variant in (N.FOREST_AUTO, N.FOREST_RANKED):
+            prog = DeviceProgram(lower.lower_model(m), 0, forest_variant=variant)
+            leaves = torch.empty((x.shape[0], len(m.trees)), dtype=torch.int32, device="cuda")
+            y = prog.run(torch.from_numpy(x).cuda(), leaf_out=leaves).cpu().numpy().astype(np.float64)
+            np.testing.assert_array_equal(leaves.cpu().numpy(), want_leaves)
+            assert _same(y, want), (variant, prog.forest().info())
+            prog.close()
