@@ -772,6 +772,7 @@ def main(argv=None):
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="time eager program runs instead of CUDA graph replays")
     ap.add_argument("--variant", default="auto", choices=["auto", "ranked", "skew", "perfect", "general", "mma"],
                     help="force a forest kernel variant (measurement; default: the measured AUTO choice)")
     args = ap.parse_args(argv)
@@ -816,6 +817,19 @@ def main(argv=None):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    # the timed steps replay one CUDA graph of the program (DeviceProgram.capture):
+    # same kernels, one host call per step instead of the per-stage Python path
+    graph_launches = None
+    if not args.no_graph:
+        try:
+            graph, graph_launches = prog.capture(x, y, bad=bad)
+            step = graph.replay  # noqa: F811
+            for _ in range(args.warmup):
+                step()
+            torch.cuda.synchronize()
+        except Exception as e:  # capture unsupported for this program: eager steps
+            print(f"bench: CUDA graph capture failed ({e}); timing eager runs", file=sys.stderr)
+            graph_launches = None
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     launches0 = N.lib().cmlb_launch_count()
@@ -833,6 +847,8 @@ def main(argv=None):
         t_end.record(stream)
         torch.cuda.synchronize()
     launches = N.lib().cmlb_launch_count() - launches0
+    if graph_launches is not None:
+        launches = graph_launches * args.steps  # replays bypass the library's launch counter
     if world > 1:
         dist.barrier()
     elapsed_ms = t_start.elapsed_time(t_end)
@@ -873,6 +889,7 @@ def main(argv=None):
         cfg = wl.config(n, world, info)
         if info is not None:
             cfg.update({"variant": info["variant"], "chunk": info["chunk_trees"], "rows_per_cta": info["rows_per_cta"]})
+        cfg["launch"] = "cuda-graph replay of the program" if graph_launches is not None else "eager program runs"
         line = {
             "metric": wl.metric, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,

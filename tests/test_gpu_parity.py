@@ -339,3 +339,23 @@ def test_rank_tables_and_fused_ranking(eyt, rank_pass, monkeypatch):
             np.testing.assert_array_equal(leaves.cpu().numpy(), want_leaves)
             assert _same(y, want), (variant, prog.forest().info())
             prog.close()
+
+
+def test_cuda_graph_capture_replays_the_program():
+    """DeviceProgram.capture records one run as a CUDA graph (the bench's
+    timed steps replay it): replays equal eager runs, with the input refilled
+    in place between replays, and report the kernels of one run."""
+    rng = np.random.default_rng(77)
+    m = _synthetic_forest(rng, 96, 8, 28, 2)
+    prog = DeviceProgram(lower.lower_model(m), 0)
+    x = torch.from_numpy(rng.standard_normal((50_000, 28)).astype(np.float32)).cuda()
+    y = torch.empty((50_000, prog.out_cols), dtype=torch.int64 if prog.out_dtype == "int64" else
+                    prog.run(x[:1]).dtype, device="cuda")
+    g, launches = prog.capture(x, y)
+    assert launches >= 1
+    for seed in (1, 2):
+        x.copy_(torch.from_numpy(np.random.default_rng(seed).standard_normal((50_000, 28)).astype(np.float32)))
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(y, prog.run(x))
+    prog.close()
