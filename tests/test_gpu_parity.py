@@ -349,8 +349,7 @@ def test_cuda_graph_capture_replays_the_program():
     m = _synthetic_forest(rng, 96, 8, 28, 2)
     prog = DeviceProgram(lower.lower_model(m), 0)
     x = torch.from_numpy(rng.standard_normal((50_000, 28)).astype(np.float32)).cuda()
-    y = torch.empty((50_000, prog.out_cols), dtype=torch.int64 if prog.out_dtype == "int64" else
-                    prog.run(x[:1]).dtype, device="cuda")
+    y = torch.empty_like(prog.run(x))
     g, launches = prog.capture(x, y)
     assert launches >= 1
     for seed in (1, 2):
