@@ -117,8 +117,9 @@ struct Args {
   double* cacc;
   int32_t* cflag;          // [cap_blocks * 64] non-finite feature
   int cap_blocks;
-  double* pacc;            // pair tier: [3][n_rows] partial sums per bucketed entry
-  int32_t* pflag;          // [n_rows] non-finite feature
+  double* pacc;            // pair tier: [3][pq_cap] partial sums per bucketed entry
+  int32_t* pflag;          // [pq_cap] non-finite feature
+  int pq_cap;              // pair-tier capacity (rows past it take the full tier)
 };
 
 __host__ __device__ inline int pair_index(int a, int b, int C) {  // a < b
@@ -564,12 +565,14 @@ __global__ void __launch_bounds__(THREADS, 1) svm_tc_kernel(const Args a) {
                 if (sc > s_best) { s_best = sc; p_best = p; }
               }
           const int q = atomicAdd(a.pq_len, 1);
-          a.pq_row[q] = (int32_t)row;
-          a.pq_pair[q] = p_best;
-          a.pq_sign[q] = signs;
-          a.pq_unc[q] = uncmask;
-          atomicAdd(a.pcount + p_best, 1);
-          exact = false;
+          if (q < a.pq_cap) {
+            a.pq_row[q] = (int32_t)row;
+            a.pq_pair[q] = p_best;
+            a.pq_sign[q] = signs;
+            a.pq_unc[q] = uncmask;
+            atomicAdd(a.pcount + p_best, 1);
+            exact = false;
+          }
         }
       }
       if (exact) a.queue[atomicAdd(a.queue_len, 1)] = (int32_t)row;
@@ -977,7 +980,7 @@ __global__ void __launch_bounds__(CB_THREADS, 2) svm_certify_kernel(const Args a
     }
     if constexpr (PAIR) {  // partial sums of this unit's SVs -> the sorted entry's accumulators
       if (tid < nb) {
-        const size_t i = (size_t)pfirst + tid, np = (size_t)a.n_rows;
+        const size_t i = (size_t)pfirst + tid, np = (size_t)a.pq_cap;
         atomicAdd(a.pacc + i, dsum[0]);
         atomicAdd(a.pacc + np + i, esum[0]);
         atomicAdd(a.pacc + 2 * np + i, (double)asum[0]);
@@ -1157,8 +1160,8 @@ __global__ void __launch_bounds__(128) svm_pair_finish_kernel(const Args a, cons
     off[a.pairs] = e;
   }
   __syncthreads();
-  const int n = *a.pq_len;
-  const size_t np = (size_t)a.n_rows;
+  const int n = min(*a.pq_len, a.pq_cap);
+  const size_t np = (size_t)a.pq_cap;
   const double gs = 2.0 * gamma_n(a.n_sv + 64);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     int bp = 0;
@@ -1202,7 +1205,7 @@ __global__ void __launch_bounds__(256) svm_pair_scatter_kernel(const Args a) {
     }
   }
   __syncthreads();
-  const int n = *a.pq_len;
+  const int n = min(*a.pq_len, a.pq_cap);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int q = a.pq_pair[i];
     const int dst = off[q] + atomicAdd(a.pcur + q, 1);
@@ -1546,10 +1549,12 @@ int cmlb_svm_run(const cmlb_svm* m, const float* x, int64_t n_rows, int64_t ldx,
   const size_t nacc = (size_t)cap_blocks * svm::CB_ROWS * npairs_c;
   const size_t acc_bytes = nacc * 3 * sizeof(double) + (size_t)cap_blocks * svm::CB_ROWS * sizeof(int32_t);
   // pair tier: [pacc 3 x n doubles][pflag n int32] zeroed with the head
-  const size_t pacc_bytes = pair_tier ? (size_t)n_rows * 3 * sizeof(double) + ((size_t)n_rows * 4 + 7) / 8 * 8 : 0;
+  // pair-tier capacity: 1/8 of the batch (>= 64K rows); config 4b queues 0.15%
+  const int64_t pq_cap = pair_tier ? std::min<int64_t>(n_rows, std::max<int64_t>(65536, n_rows / 8)) : 0;
+  const size_t pacc_bytes = pair_tier ? (size_t)pq_cap * 3 * sizeof(double) + ((size_t)pq_cap * 4 + 7) / 8 * 8 : 0;
   const size_t zero_bytes = acc_bytes + pacc_bytes;
   const size_t bytes = zero_bytes + (nhead + 2 * (size_t)n_rows) * sizeof(int32_t) +
-                       (pair_tier ? (size_t)n_rows * (3 * sizeof(int32_t) + 4 * sizeof(unsigned long long)) : 0);
+                       (pair_tier ? (size_t)pq_cap * (3 * sizeof(int32_t) + 4 * sizeof(unsigned long long)) : 0);
   void* scratch = nullptr;
   CMLB_CUDA(cudaMallocAsync(&scratch, bytes, s));
   // [cacc doubles][cflag int32][head int32 ...]
@@ -1557,7 +1562,8 @@ int cmlb_svm_run(const cmlb_svm* m, const float* x, int64_t n_rows, int64_t ldx,
   a.cflag = reinterpret_cast<int32_t*>(static_cast<double*>(scratch) + nacc * 3);
   a.cap_blocks = cap_blocks;
   a.pacc = reinterpret_cast<double*>(static_cast<uint8_t*>(scratch) + acc_bytes);  // 8-aligned: acc_bytes % 8 == 0
-  a.pflag = reinterpret_cast<int32_t*>(a.pacc + (pair_tier ? 3 * (size_t)n_rows : 0));
+  a.pflag = reinterpret_cast<int32_t*>(a.pacc + 3 * (size_t)pq_cap);
+  a.pq_cap = (int)pq_cap;
   int32_t* head = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(scratch) + zero_bytes);
   a.queue_len = head;
   a.queue2_len = head + 1;
@@ -1569,12 +1575,12 @@ int cmlb_svm_run(const cmlb_svm* m, const float* x, int64_t n_rows, int64_t ldx,
   if (pair_tier) {
     unsigned long long* sg = reinterpret_cast<unsigned long long*>(a.queue2 + n_rows);  // 8-aligned: nhead + 2n int32
     a.pq_sign = sg;
-    a.ps_sign = sg + n_rows;
-    a.pq_unc = sg + 2 * n_rows;
-    a.ps_unc = sg + 3 * n_rows;
-    a.pq_row = reinterpret_cast<int32_t*>(sg + 4 * n_rows);
-    a.pq_pair = a.pq_row + n_rows;
-    a.ps_row = a.pq_pair + n_rows;
+    a.ps_sign = sg + pq_cap;
+    a.pq_unc = sg + 2 * pq_cap;
+    a.ps_unc = sg + 3 * pq_cap;
+    a.pq_row = reinterpret_cast<int32_t*>(sg + 4 * pq_cap);
+    a.pq_pair = a.pq_row + pq_cap;
+    a.ps_row = a.pq_pair + pq_cap;
   } else {
     a.pq_row = nullptr;
   }
@@ -1650,6 +1656,7 @@ int cmlb_svm_run(const cmlb_svm* m, const float* x, int64_t n_rows, int64_t ldx,
     int32_t nq = 0;
     cudaMemcpyAsync(&nq, a.pq_len, sizeof(nq), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
+    nq = std::min(nq, a.pq_cap);
     std::vector<unsigned long long> h((size_t)nq);
     if (nq) cudaMemcpy(h.data(), a.pq_unc, (size_t)nq * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     int32_t ql[3] = {0, 0, 0};
