@@ -2398,6 +2398,31 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
   return CMLB_OK;
 }
 
+// Fused-prologue forests (column transformers, feature compaction): the
+// forest's F columns, transformed, into a dense [n][ldo] buffer for the rank
+// pass.  Gathered per row inside the rank pass, every feature of every row was
+// its own scattered 4-byte load (2,048 rows x 256 B per CTA thrash L1); here
+// consecutive threads take consecutive (row, feature) outputs, so a warp's
+// reads stay inside one or two rows and the writes are contiguous.
+__global__ void __launch_bounds__(256) forest_gather_kernel(const float* __restrict__ x, int64_t ldx,
+                                                            const cmlb_column_op* pro, int64_t n_rows, int F,
+                                                            float* __restrict__ out, int ldo) {
+  const int64_t total = n_rows * F;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / F;
+    const int c = (int)(i - r * F);
+    out[r * ldo + c] = load_col(pro, x + r * ldx, c);
+  }
+}
+
+static bool getenv_gather_off() {  // measurement knob: CMLB_FOREST_GATHER=0 ranks through the fused prologue
+  static const bool off = [] {
+    const char* e = getenv("CMLB_FOREST_GATHER");
+    return e && atoi(e) == 0;
+  }();
+  return off;
+}
+
 static int run_forest(const cmlb_forest* f, const float* x, int64_t n_rows, int64_t ldx, void* y,
                       int32_t* leaf_out, double* partial, void* stream) {
   if (!f) return fail(CMLB_E_VALIDATION, "null forest");
@@ -2432,6 +2457,7 @@ static int run_forest(const cmlb_forest* f, const float* x, int64_t n_rows, int6
   if (grid > 0x7fffffff) return fail(CMLB_E_INPUT, "too many rows for one launch");
   cudaStream_t s = (cudaStream_t)stream;
   void* ranks = nullptr;
+  void* xt = nullptr;  // transformed columns for the rank pass (fused-prologue forests)
   if (f->variant == CMLB_FOREST_SKEW || (f->variant == CMLB_FOREST_RANKED && f->rank_pass)) {
     // rank pass first (forest_rank_kernel), into stream-ordered scratch laid
     // out as the walk's tiles; freed in stream order after the walk
@@ -2443,6 +2469,20 @@ static int run_forest(const cmlb_forest* f, const float* x, int64_t n_rows, int6
     ForestArgs ra = a;
     ra.stage_bufs = 2;
     ra.vec_x = (!f->pro && (reinterpret_cast<uintptr_t>(x) & 7) == 0 && (ldx % 2) == 0 && (f->F % 2) == 0) ? 1 : 0;
+    if (f->pro && !getenv_gather_off()) {
+      // transformed columns first (dense, even row stride), then the rank
+      // pass reads them pairwise like a plain input
+      const int ldo = f->F + (f->F & 1);
+      CMLB_CUDA(cudaMallocAsync(&xt, (size_t)n_rows * ldo * sizeof(float), s));
+      const int64_t tot = n_rows * f->F;
+      const int gg = (int)std::min<int64_t>(ceil_div(tot, 256), (int64_t)num_sms(f->device) * 16);
+      forest_gather_kernel<<<gg, 256, 0, s>>>(x, ldx, f->pro, n_rows, f->F, static_cast<float*>(xt), ldo);
+      note_launch();
+      ra.x = static_cast<const float*>(xt);
+      ra.ldx = ldo;
+      ra.pro = nullptr;
+      ra.vec_x = 1;
+    }
     const int64_t rgrid = ceil_div(n_rows, (int64_t)RANK_THREADS * RANK_RPT);
     if (f->rank_nb == 3)
       forest_rank_kernel<3><<<(unsigned)rgrid, RANK_THREADS, f->rank_smem, s>>>(ra);
@@ -2450,6 +2490,7 @@ static int run_forest(const cmlb_forest* f, const float* x, int64_t n_rows, int6
       forest_rank_kernel<2><<<(unsigned)rgrid, RANK_THREADS, f->rank_smem, s>>>(ra);
     note_launch();
     cudaError_t e = cudaGetLastError();
+    if (xt) cudaFreeAsync(xt, s);
     if (e != cudaSuccess) {
       cudaFreeAsync(ranks, s);
       return cuda_fail(e, "forest_rank_kernel");
