@@ -362,7 +362,14 @@ __global__ void __launch_bounds__(NT) forest_kernel(const ForestArgs a) {
       const int64_t row = tile + r;
       const float* src = a.x + row * a.ldx;
       if (row < a.n_rows) {
-        for (int f = 0; f < F; ++f) xs[f * ROWS + r] = load_col(a.pro, src, f);
+        // unrolled so a thread keeps several independent row loads in flight
+        if (a.pro == nullptr) {
+#pragma unroll 8
+          for (int f = 0; f < F; ++f) xs[f * ROWS + r] = __ldg(src + f);
+        } else {
+#pragma unroll 4
+          for (int f = 0; f < F; ++f) xs[f * ROWS + r] = load_col(a.pro, src, f);
+        }
         if (a.dense_sel) poison_row(xs, ROWS, F, r);
       } else {
         for (int f = 0; f < F; ++f) xs[f * ROWS + r] = 0.0f;
@@ -1626,6 +1633,7 @@ struct cmlb_forest {
   int ntt = 256, stage_cap = 0, node_off_bytes = 0, rcfg = 0, stage_off = 0, stage_bufs = 2;
   size_t rank_smem = 0;  // SKEW / RANKED: forest_rank_kernel's staging buffers
   int rank_nb = 2;       // forest_rank_kernel staging depth (2 or 3)
+  size_t small_smem = 0; // PERFECT / GENERAL one-row-per-thread kernel (small batches)
   bool rank_pass = true; // RANKED: rank in a separate pass (CMLB_RANK_PASS=0: fused per tile)
   int mma_k = 0, mma_n = 0, mma_feat_off = 0, mma_thr_off = 0, mma_pay_off = 0;
   cmlb_column_op* pro = nullptr;  // fused preprocessing
@@ -1779,6 +1787,21 @@ static KernelFn kernel_for(const cmlb_forest& f) {
     case 8: return pick4<8, 2, false>(perfect, f.xs);
     case 16: return pick4<16, 1, false>(perfect, f.xs);
     default: return pick4<32, 1, false>(perfect, f.xs);
+  }
+}
+
+// PERFECT / GENERAL at one row per thread: a batch too small to give every SM
+// two CTAs at the planned rows per thread (config 1: 100k rows were 98 CTAs of
+// 1,024 rows, latency-bound at 13% warp occupancy) runs 256-row CTAs instead.
+static KernelFn small_kernel_for(const cmlb_forest& f) {
+  if (f.variant != CMLB_FOREST_PERFECT && f.variant != CMLB_FOREST_GENERAL) return nullptr;
+  if (f.rpt <= 1) return nullptr;
+  const bool perfect = f.variant == CMLB_FOREST_PERFECT;
+  const bool pw = f.C == 1 && f.agg != CMLB_AGG_NONE;
+  switch (f.CT) {
+    case 1: return pw ? pick4<1, 1, true>(perfect, f.xs) : pick4<1, 1, false>(perfect, f.xs);
+    case 2: return pick4<2, 1, false>(perfect, f.xs);
+    default: return nullptr;
   }
 }
 
@@ -2376,6 +2399,11 @@ static int make_forest(const cmlb_forest_desc* d, int device, cmlb_forest** out)
   KernelFn k = kernel_for(*f);
   if (!k) return fail(CMLB_E_UNRESOLVED, "no kernel instantiation for this forest shape");
   CMLB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f->smem));
+  if (KernelFn ks = small_kernel_for(*f)) {
+    const size_t xs1 = f->xs ? (size_t)f->F * NT * sizeof(float) : 0;
+    f->small_smem = (f->variant == CMLB_FOREST_PERFECT ? (size_t)f->chunk_trees * f->tree_bytes : 0) + xs1;
+    CMLB_CUDA(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f->small_smem));
+  }
   if (f->variant == CMLB_FOREST_RANKED) {
     const char* rp = getenv("CMLB_RANK_PASS");
     f->rank_pass = !(rp && atoi(rp) == 0) && 2 * (size_t)f->stage_cap * 4 <= SMEM_LIMIT &&
@@ -2452,7 +2480,16 @@ static int run_forest(const cmlb_forest* f, const float* x, int64_t n_rows, int6
   a.k1 = 1u; a.k2 = 2u; a.k128 = 128u; a.k2p29 = 1u << 29; a.kexp = 0x38000000u;
   const bool rk = f->variant == CMLB_FOREST_RANKED || f->variant == CMLB_FOREST_SKEW;
   const int threads = rk ? f->ntt : (f->variant == CMLB_FOREST_MMA ? MMA2_THREADS : NT);
-  const int64_t rows = f->variant == CMLB_FOREST_MMA ? (int64_t)MMA_M : (int64_t)threads * f->rpt;
+  int64_t rows = f->variant == CMLB_FOREST_MMA ? (int64_t)MMA_M : (int64_t)threads * f->rpt;
+  size_t smem = f->smem;
+  if (KernelFn ks = small_kernel_for(*f)) {
+    if (ceil_div(n_rows, rows) < 2 * (int64_t)num_sms(f->device)) {  // small batch: 256-row CTAs
+      k = ks;
+      rows = NT;
+      smem = f->small_smem;
+      a.rows_per_cta = NT;
+    }
+  }
   const int64_t grid = ceil_div(n_rows, rows);
   if (grid > 0x7fffffff) return fail(CMLB_E_INPUT, "too many rows for one launch");
   cudaStream_t s = (cudaStream_t)stream;
@@ -2496,7 +2533,7 @@ static int run_forest(const cmlb_forest* f, const float* x, int64_t n_rows, int6
       return cuda_fail(e, "forest_rank_kernel");
     }
   }
-  k<<<(unsigned)grid, threads, f->smem, s>>>(a);
+  k<<<(unsigned)grid, threads, smem, s>>>(a);
   note_launch();
   cudaError_t e = cudaGetLastError();
   if (ranks) cudaFreeAsync(ranks, s);
