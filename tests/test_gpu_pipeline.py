@@ -73,3 +73,24 @@ def test_pipeline_rf_large_vs_oracle():
     got = api.predict(api.compile_model(m), x)
     want, _ = ext.predict(m, x)
     np.testing.assert_array_equal(np.asarray(got, np.float64).reshape(want.shape), want)
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_pipeline_cuda_graph_replay(name):
+    """Every fused pipeline program replays as one CUDA graph
+    (DeviceProgram.capture, the bench's timed form) with the same outputs;
+    programs with membership checks report through the bad-row slot."""
+    case = gc.ext_get(name)
+    prog = api.compile_model(case.model).program(0)
+    x = torch.from_numpy(np.ascontiguousarray(case.x, np.float32)).cuda()
+    want = prog.run(x)
+    y = torch.empty_like(want)
+    bad = torch.full((1,), -1, dtype=torch.int64, device="cuda") if prog.has_checks else None
+    g, launches = prog.capture(x, y, bad=bad)
+    assert launches >= 1
+    y.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(y, want)
+    if bad is not None:
+        assert int(bad.item()) == -1
