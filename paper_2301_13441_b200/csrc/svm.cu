@@ -733,7 +733,7 @@ __global__ void __launch_bounds__(CB_THREADS, 2) svm_certify_kernel(const Args a
         const int qb = qa + 1 + qr;  // pair q = (qa, qb)
         const int ta = (n_sv_start[qa + 1] - n_sv_start[qa] + CB_SV - 1) / CB_SV;
         const int tb = (n_sv_start[qb + 1] - n_sv_start[qb] + CB_SV - 1) / CB_SV;
-        punits[q] = (ta + tb + CB_SPAN / CB_SV - 1) / (CB_SPAN / CB_SV);
+        punits[q] = max(1, (ta + tb + CB_SPAN / CB_SV - 1) / (CB_SPAN / CB_SV));
         pblk[q] = usum;
         poff[q] = esum0;
         const int c = a.pcount[q];
