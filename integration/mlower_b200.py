@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import ctypes as C
 import ctypes.util
+import functools
 import os
 import threading
 import weakref
@@ -36,6 +37,7 @@ from paper_2301_13441_b200.lower import ForestSpec, lower_plan
 _NP = {"bool": np.uint8, "int8": np.int8, "int16": np.int16, "int32": np.int32, "float32": np.float32}
 
 
+@functools.lru_cache(maxsize=None)
 def _cudart():
     for name in ("libcudart.so.12", ctypes.util.find_library("cudart") or "", "/usr/local/cuda/lib64/libcudart.so"):
         if not name:
@@ -64,6 +66,24 @@ class _DeviceForest:
         N.check(self.lib.cmlb_forest_create(C.byref(d), 0, C.byref(h)))
         del keep
         self.h, self.n_in, self.out_cols, self.out_dtype = h, n_in, out_cols, out_dtype
+        self.lock = threading.Lock()
+        self.dx, self.dy, self.cap_x, self.cap_y = C.c_void_p(), C.c_void_p(), 0, 0  # grow-only device buffers
+
+    def _ensure(self, rt, nx: int, ny: int):
+        if nx > self.cap_x:
+            if self.cap_x:
+                rt.cudaFree(self.dx)
+            self.cap_x = 0
+            if rt.cudaMalloc(C.byref(self.dx), nx):
+                raise MemoryError("cudaMalloc failed")
+            self.cap_x = nx
+        if ny > self.cap_y:
+            if self.cap_y:
+                rt.cudaFree(self.dy)
+            self.cap_y = 0
+            if rt.cudaMalloc(C.byref(self.dy), ny):
+                raise MemoryError("cudaMalloc failed")
+            self.cap_y = ny
 
     def run(self, x: np.ndarray) -> np.ndarray:
         rt = _cudart()
@@ -71,22 +91,22 @@ class _DeviceForest:
         y = np.empty((n, self.out_cols), _NP[self.out_dtype])
         if n == 0:
             return y
-        dx, dy = C.c_void_p(), C.c_void_p()
-        if rt.cudaMalloc(C.byref(dx), x.nbytes) or rt.cudaMalloc(C.byref(dy), y.nbytes):
-            raise MemoryError("cudaMalloc failed")
-        try:
-            if rt.cudaMemcpy(dx, x.ctypes.data, x.nbytes, _H2D):
+        with self.lock:  # one call at a time per plan: the device buffers are the plan's
+            self._ensure(rt, x.nbytes, y.nbytes)
+            if rt.cudaMemcpy(self.dx, x.ctypes.data, x.nbytes, _H2D):
                 raise RuntimeError("cudaMemcpy H2D failed")
-            N.check(self.lib.cmlb_forest_run(self.h, dx, n, x.shape[1], dy, None, None))  # legacy stream
-            if rt.cudaMemcpy(y.ctypes.data, dy, y.nbytes, _D2H):  # synchronizes with the kernel
+            N.check(self.lib.cmlb_forest_run(self.h, self.dx, n, x.shape[1], self.dy, None, None))  # legacy stream
+            if rt.cudaMemcpy(y.ctypes.data, self.dy, y.nbytes, _D2H):  # synchronizes with the kernel
                 raise RuntimeError("cudaMemcpy D2H failed")
-        finally:
-            rt.cudaFree(dx)
-            rt.cudaFree(dy)
         return y
 
     def __del__(self):
         try:
+            rt = _cudart()
+            if self.cap_x:
+                rt.cudaFree(self.dx)
+            if self.cap_y:
+                rt.cudaFree(self.dy)
             self.lib.cmlb_forest_destroy(self.h)
         except Exception:
             pass
