@@ -1163,7 +1163,6 @@ __global__ void __launch_bounds__(NTT, 1) forest_skew_kernel(const ForestArgs a)
   static_assert(ROWS % 64 == 0, "rank tile interleave needs 64-row groups");
   static_assert(TI == 2 || TI == 4 || TI == 8 || TI == 16, "walks per step");
   const int tid = threadIdx.x, lane = tid & 31;
-  const int64_t tile = (int64_t)blockIdx.x * ROWS;
   const int F = a.F;
   const uint32_t chunk_off = (uint32_t)(((size_t)F * ROWS * 2 + 15) & ~(size_t)15);
   uint8_t* chunk = smem + chunk_off;
@@ -1179,16 +1178,24 @@ __global__ void __launch_bounds__(NTT, 1) forest_skew_kernel(const ForestArgs a)
   const int T = a.T;
   const int G = (T + 31) >> 5;
   const int nchunks = (G + a.chunk_trees - 1) / a.chunk_trees;
-  auto issue_chunk = [&](int ci) {  // thread 0 only
-    const int g0 = ci * a.chunk_trees;
+  // chunks are numbered in sequence across this CTA's tiles (cs): buffer
+  // cs & 1, phase cs >> 1; chunk cs holds groups of chunk cs % nchunks
+  auto issue_chunk = [&](int cs) {  // thread 0 only
+    const int g0 = (cs % nchunks) * a.chunk_trees;
     const uint32_t bytes = (uint32_t)min(a.chunk_trees, G - g0) * gbytes;
-    uint8_t* dst = chunk + (ci & 1) * buf_bytes;
+    uint8_t* dst = chunk + (cs & 1) * buf_bytes;
     const uint8_t* src = a.blob + (size_t)g0 * gbytes;
     fence_proxy_async();
-    mbar_expect_tx(&tree_bar[ci & 1], bytes);
+    mbar_expect_tx(&tree_bar[cs & 1], bytes);
     for (uint32_t off = 0; off < bytes; off += 32768u)
-      bulk_g2s(dst + off, src + off, min(32768u, bytes - off), &tree_bar[ci & 1]);
+      bulk_g2s(dst + off, src + off, min(32768u, bytes - off), &tree_bar[cs & 1]);
   };
+  // persistent (precomputed ranks, grid < tiles): this CTA's tiles are
+  // blockIdx.x + i * gridDim.x; the tree ring runs on across tile boundaries,
+  // so the next tile's first groups stream in while this tile finishes
+  const int64_t ntiles = (a.n_rows + ROWS - 1) / ROWS;
+  const int my_tiles = (int)((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x);
+  const int total_chunks = my_tiles * nchunks;
   if (tid == 0) {
     mbar_init(&tree_bar[0], 1);
     mbar_init(&tree_bar[1], 1);
@@ -1200,7 +1207,9 @@ __global__ void __launch_bounds__(NTT, 1) forest_skew_kernel(const ForestArgs a)
   }
   __syncthreads();
   if (tid == 0 && a.stage_off) issue_chunk(0);
-
+  int cbase = 0;  // sequence number of this tile's first chunk
+  for (int it = 0; it < my_tiles; ++it, cbase += nchunks) {
+  const int64_t tile = ((int64_t)blockIdx.x + (int64_t)it * gridDim.x) * ROWS;
   int64_t rowk[RPT];
   uint32_t pb[RPT];
   int nbad[RPT];
@@ -1218,12 +1227,12 @@ __global__ void __launch_bounds__(NTT, 1) forest_skew_kernel(const ForestArgs a)
   if (a.ranks) {  // ranks precomputed (forest_rank_kernel): one bulk copy of this tile
     if (tid == 0) {
       const uint32_t bytes = (uint32_t)F * ROWS * 2u;
-      const uint8_t* src = reinterpret_cast<const uint8_t*>(a.ranks + (int64_t)blockIdx.x * F * ROWS);
+      const uint8_t* src = reinterpret_cast<const uint8_t*>(a.ranks + (tile / ROWS) * F * ROWS);
       fence_proxy_async();
       mbar_expect_tx(&stage_bar[0], bytes);
       for (uint32_t off = 0; off < bytes; off += 32768u) bulk_g2s(smem + off, src + off, min(32768u, bytes - off), &stage_bar[0]);
     }
-    mbar_wait(&stage_bar[0], 0);
+    mbar_wait(&stage_bar[0], (uint32_t)(it & 1));
   } else {
     rank_tile<NTT, RPT>(a, smem, chunk, stage_bar, rowk, pb, nbad);
   }
@@ -1303,17 +1312,20 @@ __global__ void __launch_bounds__(NTT, 1) forest_skew_kernel(const ForestArgs a)
     }
   };
 
-  __syncthreads();  // ranks complete; staging buffers no longer read
-  if (tid == 0) {
-    if (!a.stage_off) issue_chunk(0);
-    if (nchunks > 1) issue_chunk(1);
+  if (it == 0) {
+    __syncthreads();  // ranks complete; staging buffers no longer read
+    if (tid == 0) {
+      if (!a.stage_off) issue_chunk(0);
+      if (total_chunks > 1) issue_chunk(1);
+    }
   }
   const uint32_t rot0 = 4u * (uint32_t)lane;
   for (int ci = 0; ci < nchunks; ++ci) {
+    const int cs = cbase + ci;
     const int g0 = ci * a.chunk_trees;
     const int ng = min(a.chunk_trees, G - g0);
-    mbar_wait(&tree_bar[ci & 1], (uint32_t)(ci >> 1) & 1u);
-    const uint32_t buf_off = chunk_off + (uint32_t)(ci & 1) * buf_bytes;
+    mbar_wait(&tree_bar[cs & 1], (uint32_t)(cs >> 1) & 1u);
+    const uint32_t buf_off = chunk_off + (uint32_t)(cs & 1) * buf_bytes;
     for (int gl = 0; gl < ng; ++gl) {
       const uint32_t gofs = buf_off + (uint32_t)gl * gbytes;
       uint32_t rot = rot0;
@@ -1326,10 +1338,10 @@ __global__ void __launch_bounds__(NTT, 1) forest_skew_kernel(const ForestArgs a)
     }
     // release this buffer: one arrive per thread (each orders its own reads
     // before the refill); thread 0 refills it with chunk ci + 2 once all have
-    mbar_arrive(&empty_bar[ci & 1]);
-    if (tid < 32 && ci + 2 < nchunks) {  // warp 0 waits as a whole (no divergent walk)
-      mbar_wait(&empty_bar[ci & 1], (uint32_t)(ci >> 1) & 1u);
-      if (tid == 0) issue_chunk(ci + 2);
+    mbar_arrive(&empty_bar[cs & 1]);
+    if (tid < 32 && cs + 2 < total_chunks) {  // warp 0 waits as a whole (no divergent walk)
+      mbar_wait(&empty_bar[cs & 1], (uint32_t)(cs >> 1) & 1u);
+      if (tid == 0) issue_chunk(cs + 2);
       __syncwarp();
     }
   }
@@ -1344,6 +1356,8 @@ __global__ void __launch_bounds__(NTT, 1) forest_skew_kernel(const ForestArgs a)
 #pragma unroll
     for (int c = 0; c < CT; ++c) r.acc[c] = flush_tiny(acc[k][c]);
     finish_row<CT, false>(a, rowk[k], r, none);
+  }
+  __syncthreads();  // every warp done with this tile's ranks before the next tile's copy lands
   }
 }
 
@@ -2533,7 +2547,16 @@ static int run_forest(const cmlb_forest* f, const float* x, int64_t n_rows, int6
       return cuda_fail(e, "forest_rank_kernel");
     }
   }
-  k<<<(unsigned)grid, threads, smem, s>>>(a);
+  // SKEW with precomputed ranks runs persistent: one CTA per SM walks its
+  // share of the tiles (CMLB_SKEW_PERSIST=0: one CTA per tile)
+  int64_t lgrid = grid;
+  static const bool skew_persist = [] {
+    const char* e = getenv("CMLB_SKEW_PERSIST");
+    return !(e && atoi(e) == 0);
+  }();
+  if (f->variant == CMLB_FOREST_SKEW && a.ranks && skew_persist)
+    lgrid = std::min<int64_t>(grid, num_sms(f->device));
+  k<<<(unsigned)lgrid, threads, smem, s>>>(a);
   note_launch();
   cudaError_t e = cudaGetLastError();
   if (ranks) cudaFreeAsync(ranks, s);
