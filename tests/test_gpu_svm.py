@@ -168,3 +168,24 @@ def test_config4b_fitted_svc_65536_rows_against_libsvm_oracle():
     got = y.cpu().numpy().astype(np.float64).ravel()
     bad = np.flatnonzero(got != want)
     assert bad.size == 0, f"{bad.size} of {n} classes differ (exact-path rows {int(ex.item())})"
+
+
+def test_svm_all_rows_uncertain_overflow_tiers():
+    """Rows on the decision boundary (a linear-kernel SVC, every row projected
+    onto its hyperplane): nearly every row is queued, overflowing the pair
+    tier's capacity (1/8 of the batch, >= 64K rows) into the full certifying
+    tier, whose first 16,384 rows take the SV-split units and the rest the
+    in-CTA path, and on to the libsvm-order exact kernel -- every class must
+    still equal libsvm's."""
+    m = _synthetic_svc(16, 96, 2, "linear", seed=21)
+    sv = np.asarray(m.support_vectors, np.float64)
+    w = (np.asarray(m.dual_coef, np.float64)[0][:, None] * sv).sum(0)
+    b = float(np.asarray(m.intercept, np.float64)[0])
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((150_000, 16))
+    x -= ((x @ w + b) / (w @ w))[:, None] * w[None, :]   # w.x + b = 0 up to rounding
+    x = x.astype(np.float32)
+    y, _, n_exact = run_svm(m, x, decision=False)
+    _, vote = ext.svm_decision(m, x)
+    np.testing.assert_array_equal(y.ravel(), np.asarray(m.classes, np.float64)[vote])
+    assert n_exact > 0  # some rows sit inside even the float64 bound
