@@ -58,6 +58,20 @@ def svm():
     got = api.predict(api.compile_model(m), torch.from_numpy(x).cuda()).cpu().numpy().astype(np.float64).ravel()
     _, vote = ext.svm_decision(m, x)
     assert np.array_equal(got, np.asarray(m.classes, np.float64)[vote])
+    # rows on a linear SVC's hyperplane: every row takes the pair tier (scatter,
+    # SV-split units, finish), the full certifying tier and the exact kernel
+    from paper_2301_13441_b200.extmodels import SVMModel
+    m2 = synthetic_svc(F=16, n_sv=96, C=2, seed=21)
+    m2 = SVMModel(m2.model_type, m2.n_features, "linear", m2.gamma, m2.coef0, m2.degree, m2.support_vectors,
+                  m2.dual_coef, m2.intercept, m2.n_support, m2.classes)
+    sv = np.asarray(m2.support_vectors, np.float64)
+    w = (np.asarray(m2.dual_coef, np.float64)[0][:, None] * sv).sum(0)
+    b = float(np.asarray(m2.intercept, np.float64)[0])
+    x2 = np.random.default_rng(5).standard_normal((200, 16))
+    x2 = (x2 - ((x2 @ w + b) / (w @ w))[:, None] * w[None, :]).astype(np.float32)
+    got = api.predict(api.compile_model(m2), torch.from_numpy(x2).cuda()).cpu().numpy().astype(np.float64).ravel()
+    _, vote = ext.svm_decision(m2, x2)
+    assert np.array_equal(got, np.asarray(m2.classes, np.float64)[vote])
 
 
 def linear():
